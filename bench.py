@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark: split-FP16 SGEMM effective TFLOPS (2MNK/t) on B200 (BASELINE.json metric).
+
+One "step" = one whole split3_sgemm call (max-abs + split of A and B + tcgen05 GEMM with the
+fused epilogue) on N x N FP32 inputs already resident in HBM.  Default workload:
+configs[1], N = 16384, 3-term (BASELINE.json).  Inputs are 1 GiB per matrix (> 126 MB L2),
+so no L2 flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--n 16384] [--terms 3|4|1]
+  python bench.py --impl reference ...     # the CPU oracle (oracle/) as it stands
+
+Multi-GPU (torchrun, one rank per GPU): 2-D C-tile partition (paper_2011_11188_b200.dist);
+each rank owns one n x n tile of a (pr*n) x (pc*n) x n problem (weak scaling), inputs start
+sharded and the FP16 plane panels are all-gathered over NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=30)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="split3", choices=["split3", "reference"])
+    p.add_argument("--n", type=int, default=16384)
+    p.add_argument("--terms", type=int, default=3, choices=[1, 3, 4])
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-target-s", type=float, default=12.0)
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return {"hbm": d["hbm_gbs"], "tc_burst": d["bf16_tflops"],
+                "tc_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "src": "measured"}
+    except Exception:
+        return {"hbm": 6650.0, "tc_burst": 1590.0, "tc_sustained": 1400.0, "src": "fallback"}
+
+
+# ----------------------------------------------------------------- clocks -----
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (the profiling recipe's clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "power_w_max": max(pw),
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------- cpu oracle -----
+def cpu_oracle_sample(A_host: np.ndarray, B_host: np.ndarray, terms: int, target_s: float):
+    """Time oracle.sgemm_sampled on R x R sampled outputs of the full-size problem."""
+    import oracle
+
+    N = A_host.shape[0]
+    K = A_host.shape[1]
+    Nc = B_host.shape[1]
+    rng = np.random.Generator(np.random.PCG64(1234))
+
+    def run(R):
+        rows = np.sort(rng.choice(A_host.shape[0], R, replace=False))
+        cols = np.sort(rng.choice(Nc, R, replace=False))
+        t = time.perf_counter()
+        oracle.sgemm_sampled(A_host, B_host, rows, cols, terms=terms)
+        return time.perf_counter() - t
+
+    r0 = min(32, N, Nc)
+    t0 = run(r0)
+    r1 = min(2 * r0, N, Nc)
+    t1 = run(r1)
+    per_r2 = max((t1 - t0) / max(r1 * r1 - r0 * r0, 1), 1e-9)
+    fixed = max(t0 - per_r2 * r0 * r0, 0.0)
+    R = int(np.sqrt(max(target_s - fixed, 0.0) / per_r2))
+    R = int(max(r1, min(R, 1024, N, Nc)))
+    dt = run(R)
+    flops = 2.0 * R * R * K
+    return {"value": flops / dt / 1e12, "unit": "TFLOPS", "cores": oracle.num_threads(),
+            "kind": "oracle", "seconds": dt,
+            "sample": f"{R}x{R} sampled outputs of the {A_host.shape[0]}x{Nc}x{K} product "
+                      f"(fp64 oracle: full-matrix max-abs, split of the sampled rows/cols, "
+                      f"{terms}-term Eq. A_2); value = 2*R*R*K / time"}
+
+
+# ------------------------------------------------------------ reference arm ---
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    from workloads import numpy_matrix
+
+    n = args.n
+    # the oracle's own inputs (same recipe as the GPU arm: uniform[-1,1], seeds 0/1)
+    A = numpy_matrix("uniform", n, n, seed=0)
+    B = numpy_matrix("uniform", n, n, seed=1)
+    per_step_target = max(2.0, min(20.0, 150.0 / max(args.steps + args.warmup, 1)))
+    info = cpu_oracle_sample(A, B, args.terms, per_step_target)
+    R = int(info["sample"].split("x")[0])
+    rng = np.random.Generator(np.random.PCG64(99))
+    times = []
+    for i in range(args.warmup + args.steps):
+        rows = np.sort(rng.choice(n, R, replace=False))
+        cols = np.sort(rng.choice(n, R, replace=False))
+        t = time.perf_counter()
+        oracle.sgemm_sampled(A, B, rows, cols, terms=args.terms)
+        dt = time.perf_counter() - t
+        if i >= args.warmup:
+            times.append(dt)
+    t_total = sum(times)
+    value = 2.0 * R * R * n * len(times) / t_total / 1e12
+    line = {
+        "impl": "reference", "metric": "split-FP16 SGEMM effective TFLOPS (2MNK/t)",
+        "value": value, "unit": "TFLOPS", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_total / max(len(times), 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(args, world),
+        "cpu_baseline": {"value": value, "unit": "TFLOPS", "cores": oracle.num_threads(),
+                         "kind": "oracle", "sample": info["sample"] + " per step"},
+        "e2e": {"value": value, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world):
+    name = {3: "3-term", 4: "4-term", 1: "1-term control"}[args.terms]
+    pr, pc = grid_shape(world)
+    return {"workload": f"square N={args.n} FP32 uniform[-1,1], {name} split-FP16 GEMM"
+                        + (f", 2-D tiles {pr}x{pc}" if world > 1 else ""),
+            "M": args.n * pr, "N": args.n * pc, "K": args.n, "terms": args.terms,
+            "parallelism": f"2d-tile {pr}x{pc}" if world > 1 else "single",
+            "l2": "inputs 1 GiB/matrix > 126 MB L2: no flush needed"}
+
+
+def grid_shape(world):
+    from paper_2011_11188_b200.dist import grid_for
+
+    return grid_for(world)
+
+
+# ------------------------------------------------------------------- main -----
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+
+    from paper_2011_11188_b200 import split3 as s3
+    from workloads import torch_matrix
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    n = args.n
+    h = s3.Handle(local)
+    four, one = args.terms == 4, args.terms == 1
+
+    if world == 1:
+        A = torch_matrix("uniform", n, n, seed=0, device=dev)
+        B = torch_matrix("uniform", n, n, seed=1, device=dev)
+        C = torch.empty((n, n), dtype=torch.float32, device=dev)
+
+        def step():
+            h.sgemm(A, B, out=C, four_term=four, one_term=one)
+    else:
+        from paper_2011_11188_b200.dist import TileGemm
+
+        tg = TileGemm(h, n, world, rank, four_term=four, one_term=one, seed=0)
+
+        def step():
+            tg.run()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = h.last_launch_count() if world == 1 else tg.launches_per_step()
+
+    gpu_idx = local
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        try:
+            gpu_idx = int(vis.split(",")[local])
+        except ValueError:
+            pass
+    sampler = ClockSampler(gpu_idx)
+    h.timing_enable(True)
+    h.timing_read()
+    sampler.start()
+    time.sleep(0.3)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = sampler.stop()
+    h.timing_enable(False)
+    split_ms, gemm_ms, ncalls = h.timing_read()
+    t_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([t_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_ms = float(t.item())
+    M_loc = N_loc = K = n
+    flops_step = 2.0 * M_loc * N_loc * K * world
+    value = flops_step * args.steps / (t_ms / 1e3) / 1e12
+    pk = peaks()
+
+    # roofline of the dominant kernel (the tcgen05 GEMM): algorithmic FP16 FLOPs per launch
+    n_prod = {3: 3, 4: 4, 1: 1}[args.terms]
+    gemm_avg_ms = gemm_ms / max(ncalls, 1)
+    achieved = n_prod * 2.0 * M_loc * N_loc * K / (gemm_avg_ms / 1e3) / 1e12 if ncalls else None
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "gemm3_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get(str(n), {}).get(str(args.terms))
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": "gemm3_kernel", "achieved": achieved,
+                "peak": pk["tc_sustained"], "unit": "TFLOP/s",
+                "frac": (achieved / pk["tc_sustained"]) if achieved else None,
+                "traffic": traffic,
+                "peak_src": f"{pk['src']} bf16_tflops_sustained (fp16 = bf16 nominal rate)",
+                "frac_of_burst": (achieved / pk["tc_burst"]) if achieved else None,
+                "gemm_share_of_step": gemm_ms / max(t_ms, 1e-9) if ncalls else None,
+                "split_ms_per_step": split_ms / max(ncalls, 1),
+                "split_hbm_gbs": (12.0 * 2 * n * n / (split_ms / max(ncalls, 1) / 1e3) / 1e9)
+                if ncalls and split_ms > 0 else None}
+
+    # e2e through the C-ABI with HOST buffers (H2D of A, B and D2H of C inside the timed region)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        Ah = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+        Bh = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+        Ch = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+        Ah.copy_(A)
+        Bh.copy_(B)
+        del C
+        flags = (s3.FOUR_TERM if four else 0) | (s3.ONE_TERM if one else 0)
+        h.sgemm_host_ptr(n, n, n, Ah.data_ptr(), Bh.data_ptr(), Ch.data_ptr(), flags)   # warm
+        torch.cuda.synchronize()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(stream)
+        for _ in range(args.e2e_steps):
+            h.sgemm_host_ptr(n, n, n, Ah.data_ptr(), Bh.data_ptr(), Ch.data_ptr(), flags)
+        x1.record(stream)
+        torch.cuda.synchronize()
+        te = x0.elapsed_time(x1) / args.e2e_steps
+        e2e = {"value": 2.0 * n ** 3 / (te / 1e3) / 1e12, "unit": "TFLOPS",
+               "h2d_bytes_per_step": 2 * n * n * 4, "d2h_bytes_per_step": n * n * 4,
+               "ms_per_step": te, "api": "split3_sgemm_host (pinned host buffers)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_oracle_sample(A.cpu().numpy(), B.cpu().numpy(), args.terms, args.cpu_target_s)
+        except Exception as ex:   # reported, never silently replaced
+            cpu = {"value": None, "error": repr(ex)}
+
+    if rank == 0:
+        line = {
+            "metric": "split-FP16 SGEMM effective TFLOPS (2MNK/t)",
+            "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f16x3->f32" if args.terms == 3 else
+            ("f16x4->f32" if args.terms == 4 else "f16->f32"),
+            "data": "synthetic", "config": workload_config(args, world),
+            "frac_of_peak_over_3": value / world / (pk["tc_burst"] / n_prod),
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,152 @@
+/*
+ * split3.h — C ABI of the B200 (sm_100a) split-FP16 SGEMM.
+ *
+ * The method (arXiv 2011.11188, Appendix A; "PAPER.md:L" = line L of the paper text):
+ *   Eq. A_1:   A ~= a1*A1 + a2*A2,  B ~= b1*B1 + b2*B2   (A1, A2, B1, B2 in FP16)
+ *   PAPER.md:18-20:           a2 = 2^-11 * a1,     b2 = 2^-11 * b1
+ *   Eq. A_2: C ~= a1b1*A1B1 + a1b2*A1B2 + a2b1*A2B1 + a2b2*A2B2
+ *   PAPER.md:21-24:           a2b2 = 2^-22 a1b1 "may be optionally dropped" -> 3 FP16 GEMMs
+ *   PAPER.md:282-285:         FP16 inputs, FP32 accumulation on tensor cores
+ * Scale rule (the paper gives only its purpose; DESIGN.md §3 R1):
+ *   a1 = 2^sA, sA = 0 if max|A| == 0 else max(floor(log2 max|A|) - 14, -127), over finite entries.
+ * Epilogue (DESIGN.md §3 R7): C = (D_hi + 2^-11 * D_mid [+ 2^-22 * D_lo]) * 2^(sA+sB)
+ *   with D_hi = A1*B1, D_mid = A1*B2 + A2*B1, D_lo = A2*B2 accumulated in FP32 (TMEM).
+ *
+ * Conventions for every entry point:
+ *  - Matrices are ROW-MAJOR.  A is M x K (lda >= max(1,K)), B is K x N (ldb >= max(1,N)),
+ *    C is M x N (ldc >= max(1,N)).  Leading dimensions are in elements.
+ *  - All matrix/workspace pointers are DEVICE pointers owned by the caller (e.g. PyTorch
+ *    allocations), except where an entry point says HOST.  The library allocates no device
+ *    memory of its own beyond a few bytes per handle.
+ *  - Calls are asynchronous on the handle's stream unless stated; errors are returned as a
+ *    split3_status (never printed, never aborted).  Argument errors are detected before any
+ *    work is enqueued.  SPLIT3_ERR_CUDA reports a failed launch / CUDA API call.
+ *  - C must not alias A, B or the workspace.  A handle is not thread-safe: use one per stream.
+ *  - Requires an sm_100 device (B200); other devices -> SPLIT3_ERR_ARCH at create time.
+ */
+#ifndef SPLIT3_H
+#define SPLIT3_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct split3_ctx *split3_handle_t;
+
+typedef enum split3_status {
+    SPLIT3_OK = 0,
+    SPLIT3_ERR_INVALID_VALUE = 1,   /* bad dimension, leading dimension, pointer or flag */
+    SPLIT3_ERR_NOT_FINITE = 2,      /* SPLIT3_CHECK_FINITE found a NaN/Inf input entry */
+    SPLIT3_ERR_WORKSPACE = 3,       /* workspace missing or smaller than split3_sgemm_workspace_size */
+    SPLIT3_ERR_CUDA = 4,            /* a CUDA runtime/driver call or a launch failed */
+    SPLIT3_ERR_ARCH = 5,            /* device is not sm_100 */
+    SPLIT3_ERR_NOT_IMPLEMENTED = 6  /* a combination this build does not support */
+} split3_status;
+
+/* flags (bitwise OR) */
+#define SPLIT3_THREE_TERM   0u         /* default: A1B1 + 2^-11 (A1B2 + A2B1) */
+#define SPLIT3_FOUR_TERM    (1u << 0)  /* keep the dropped 2^-22 A2B2 term (Eq. A_2 in full) */
+#define SPLIT3_CHECK_FINITE (1u << 1)  /* synchronise; reject NaN/Inf inputs */
+#define SPLIT3_ONE_TERM     (1u << 2)  /* control: a1b1 * A1B1 only (a scaled plain FP16 GEMM) */
+#define SPLIT3_FLAGS_MASK   (SPLIT3_FOUR_TERM | SPLIT3_CHECK_FINITE | SPLIT3_ONE_TERM)
+
+/* ---- handle ------------------------------------------------------------------------ */
+
+/* Create a handle bound to CUDA device `device` and stream `cuda_stream` (a cudaStream_t;
+ * NULL = the legacy default stream).  Fails with SPLIT3_ERR_ARCH unless the device is sm_100. */
+int split3_sgemm_create(split3_handle_t *h, int device, void *cuda_stream);
+
+/* Rebind the handle to another stream of the same device. */
+int split3_set_stream(split3_handle_t h, void *cuda_stream);
+
+/* Destroy the handle (does not free caller-owned workspace).  NULL is a no-op. */
+int split3_sgemm_destroy(split3_handle_t h);
+
+/* Bytes of device workspace split3_sgemm needs for (M, N, K): the four FP16 planes with
+ * padded leading dimensions (a multiple of 8 elements) plus 256 bytes of scalars. */
+size_t split3_sgemm_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags);
+
+/* Attach caller-owned device workspace (256-byte aligned).  The handle keeps the pointer;
+ * the caller keeps ownership and must keep it alive while calls are in flight. */
+int split3_sgemm_set_workspace(split3_handle_t h, void *dptr, size_t bytes);
+
+/* ---- the whole method --------------------------------------------------------------- */
+
+/* C = A*B emulated by FP16 tensor-core GEMMs.  Enqueues: scalar reset,
+ * max-abs of A and B, split of A and B into FP16 planes (B planes stored transposed,
+ * N x K, K-major), and the tcgen05 GEMM with fused rescaling epilogue.  C is overwritten
+ * (beta = 0).  M == 0 or N == 0: no-op.  K == 0: C is zero-filled.
+ * Non-finite inputs: without SPLIT3_CHECK_FINITE they propagate into the rows/columns of C
+ * that touch them (the max-abs skips them); with it the call synchronises and returns
+ * SPLIT3_ERR_NOT_FINITE, the index then being available from split3_last_bad_index. */
+int split3_sgemm(split3_handle_t h, int64_t M, int64_t N, int64_t K,
+                 const float *A, int64_t lda, const float *B, int64_t ldb,
+                 float *C, int64_t ldc, uint32_t flags);
+
+/* Same computation with HOST buffers (pageable or pinned): copies A and B to the workspace
+ * staging area of the handle's device, runs split3_sgemm, copies C back, and synchronises
+ * the handle's stream before returning.  Device staging for A, B and C is taken from the
+ * workspace, which must hold split3_sgemm_host_workspace_size(M, N, K, flags) bytes.
+ * Host layout is packed row-major (lda = K, ldb = N, ldc = N). */
+size_t split3_sgemm_host_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags);
+int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K,
+                      const float *A_host, const float *B_host, float *C_host, uint32_t flags);
+
+/* After SPLIT3_ERR_NOT_FINITE: first offending linear index (row*cols+col) of A, or
+ * M*K + index within B; -1 if none recorded. */
+int64_t split3_last_bad_index(split3_handle_t h);
+
+const char *split3_status_string(int status);
+
+/* ---- lower level: used by the multi-GPU driver and by the tests -------------------------- */
+
+/* Max-abs over FINITE entries of X (rows x cols, ld), folded into *d_maxabs with an atomic
+ * max on the float's bit pattern (exact and order-independent; non-finite entries are
+ * skipped, DESIGN.md §3 R8).  d_maxabs: device float, caller initialises it to 0.0f.
+ * If d_bad is non-NULL (device int64, caller initialises to INT64_MAX), the smallest
+ * linear index of a non-finite entry is folded into it with an atomic min. */
+int split3_maxabs(split3_handle_t h, int64_t rows, int64_t cols, const float *X, int64_t ldx,
+                  float *d_maxabs, int64_t *d_bad);
+
+/* Split X (rows x cols, ld) with the scale exponent derived on the device from *d_maxabs
+ * (the GLOBAL max when X is a shard; reading R1) into FP16 planes hi/lo (uint16 binary16
+ * bit patterns) per Eq. A_1.  transpose = 0: planes are rows x cols (ldp >= cols);
+ * transpose = 1: planes are cols x rows (ldp >= rows) — the K-major layout the GEMM wants
+ * for B.  ldp must be a multiple of 8 and the plane pointers 16-byte aligned.
+ * If d_sexp is non-NULL the scale exponent s is written to *d_sexp (device int32). */
+int split3_split(split3_handle_t h, int64_t rows, int64_t cols, const float *X, int64_t ldx,
+                 const float *d_maxabs, uint16_t *hi, uint16_t *lo, int64_t ldp, int transpose,
+                 int32_t *d_sexp);
+
+/* GEMM from planes: A1, A2 are M x K (K-major, ldpa), B1t, B2t are N x K (K-major, ldpb),
+ * i.e. the planes of B TRANSPOSED.  *d_sA, *d_sB are the device scale exponents.  Computes
+ * C = (D_hi + 2^-11 D_mid [+ 2^-22 D_lo]) * 2^(sA+sB) (flags as for split3_sgemm; with
+ * SPLIT3_ONE_TERM only A1/B1t are read and A2/B2t may be NULL).  ldpa, ldpb multiples of 8,
+ * plane pointers 16-byte aligned, K >= 1. */
+int split3_gemm_planes(split3_handle_t h, int64_t M, int64_t N, int64_t K,
+                       const uint16_t *A1, const uint16_t *A2, int64_t ldpa, const int32_t *d_sA,
+                       const uint16_t *B1t, const uint16_t *B2t, int64_t ldpb, const int32_t *d_sB,
+                       float *C, int64_t ldc, uint32_t flags);
+
+/* Number of kernels the last split3_sgemm / split3_gemm_planes call launched (for the bench's
+ * gpu_launches count; memsets are not counted). */
+int split3_last_launch_count(split3_handle_t h);
+
+/* ---- measurement hooks (bench.py's roofline; no effect on results) ---------------------- */
+
+/* enable != 0: every following split3_sgemm records CUDA events on the handle's stream around
+ * its split phase (max-abs + split kernels) and its GEMM kernel. */
+int split3_timing_enable(split3_handle_t h, int enable);
+
+/* Synchronise the recorded events and return the summed durations (milliseconds) of the split
+ * phase and of the GEMM kernel since the last read, and the number of calls timed; resets. */
+int split3_timing_read(split3_handle_t h, double *split_ms, double *gemm_ms, int *calls);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPLIT3_H */

@@ -1,0 +1,369 @@
+// capi.cu — the extern "C" boundary declared in include/split3.h.
+//
+// Validation, workspace carving and launch orchestration only: every arithmetic step of the
+// path runs in the kernels of split_kernels.cu (a1, a2) and gemm3.cu (a3, a4).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <new>
+#include <vector>
+
+#include "../../include/split3.h"
+#include "internal.h"
+
+struct split3_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    long long last_bad = -1;
+    int last_launches = 0;
+    // measurement hooks: event triples (start, after split, after gemm) per timed call
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+};
+
+namespace {
+cudaEvent_t next_event(split3_ctx* h) {
+    if (h->ev_used == h->ev_pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        h->ev_pool.push_back(e);
+    }
+    return h->ev_pool[h->ev_used++];
+}
+void record(split3_ctx* h, cudaEvent_t e) {
+    if (e) cudaEventRecord(e, h->stream);
+}
+}  // namespace
+
+namespace {
+
+using split3::plane_ld;
+
+// Scalars block at the start of the workspace (256 B): [0] float maxA, [1] float maxB,
+// [2] int32 sA, [3] int32 sB, [8..9] int64 badA, [10..11] int64 badB.
+constexpr size_t kScalarBytes = 256;
+
+struct Carve {
+    float* maxA;
+    float* maxB;
+    int32_t* sA;
+    int32_t* sB;
+    long long* badA;
+    long long* badB;
+    uint16_t* A1;
+    uint16_t* A2;
+    uint16_t* B1t;
+    uint16_t* B2t;
+    int64_t ldpa, ldpb;
+    size_t end;   // bytes used
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+Carve carve(void* ws, int64_t M, int64_t N, int64_t K) {
+    Carve c;
+    uint8_t* b = static_cast<uint8_t*>(ws);
+    c.maxA = reinterpret_cast<float*>(b);
+    c.maxB = c.maxA + 1;
+    c.sA = reinterpret_cast<int32_t*>(b + 8);
+    c.sB = c.sA + 1;
+    c.badA = reinterpret_cast<long long*>(b + 32);
+    c.badB = c.badA + 1;
+    c.ldpa = plane_ld(K);
+    c.ldpb = plane_ld(K);
+    size_t off = kScalarBytes;
+    const size_t pa = align256((size_t)M * (size_t)c.ldpa * 2);
+    const size_t pb = align256((size_t)N * (size_t)c.ldpb * 2);
+    c.A1 = reinterpret_cast<uint16_t*>(b + off); off += pa;
+    c.A2 = reinterpret_cast<uint16_t*>(b + off); off += pa;
+    c.B1t = reinterpret_cast<uint16_t*>(b + off); off += pb;
+    c.B2t = reinterpret_cast<uint16_t*>(b + off); off += pb;
+    c.end = off;
+    return c;
+}
+
+size_t ws_size(int64_t M, int64_t N, int64_t K) {
+    if (M < 0 || N < 0 || K < 0) return 0;
+    return kScalarBytes + 2 * align256((size_t)M * (size_t)plane_ld(K) * 2) +
+           2 * align256((size_t)N * (size_t)plane_ld(K) * 2);
+}
+
+inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+inline int terms_of(uint32_t flags) {
+    if (flags & SPLIT3_ONE_TERM) return 1;
+    if (flags & SPLIT3_FOUR_TERM) return 4;
+    return 3;
+}
+
+int set_dev(split3_ctx* h) {
+    return cudaSetDevice(h->device) == cudaSuccess ? SPLIT3_OK : SPLIT3_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* split3_status_string(int status) {
+    switch (status) {
+        case SPLIT3_OK: return "SPLIT3_OK";
+        case SPLIT3_ERR_INVALID_VALUE: return "SPLIT3_ERR_INVALID_VALUE";
+        case SPLIT3_ERR_NOT_FINITE: return "SPLIT3_ERR_NOT_FINITE";
+        case SPLIT3_ERR_WORKSPACE: return "SPLIT3_ERR_WORKSPACE";
+        case SPLIT3_ERR_CUDA: return "SPLIT3_ERR_CUDA";
+        case SPLIT3_ERR_ARCH: return "SPLIT3_ERR_ARCH";
+        case SPLIT3_ERR_NOT_IMPLEMENTED: return "SPLIT3_ERR_NOT_IMPLEMENTED";
+        default: return "SPLIT3_ERR_UNKNOWN";
+    }
+}
+
+int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
+    if (!h) return SPLIT3_ERR_INVALID_VALUE;
+    *h = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess) return SPLIT3_ERR_CUDA;
+    if (device < 0 || device >= ndev) return SPLIT3_ERR_INVALID_VALUE;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return SPLIT3_ERR_CUDA;
+    if (prop.major != 10 || prop.minor != 0) return SPLIT3_ERR_ARCH;
+    split3_ctx* c = new (std::nothrow) split3_ctx();
+    if (!c) return SPLIT3_ERR_CUDA;
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+    *h = c;
+    return SPLIT3_OK;
+}
+
+int split3_set_stream(split3_handle_t h, void* cuda_stream) {
+    if (!h) return SPLIT3_ERR_INVALID_VALUE;
+    h->stream = static_cast<cudaStream_t>(cuda_stream);
+    return SPLIT3_OK;
+}
+
+int split3_sgemm_destroy(split3_handle_t h) {
+    if (h)
+        for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+    delete h;
+    return SPLIT3_OK;
+}
+
+size_t split3_sgemm_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags) {
+    (void)flags;
+    return ws_size(M, N, K);
+}
+
+int split3_sgemm_set_workspace(split3_handle_t h, void* dptr, size_t bytes) {
+    if (!h) return SPLIT3_ERR_INVALID_VALUE;
+    if (bytes && (!dptr || !aligned(dptr, 256))) return SPLIT3_ERR_INVALID_VALUE;
+    h->ws = dptr;
+    h->ws_bytes = dptr ? bytes : 0;
+    return SPLIT3_OK;
+}
+
+int64_t split3_last_bad_index(split3_handle_t h) { return h ? h->last_bad : -1; }
+
+int split3_last_launch_count(split3_handle_t h) { return h ? h->last_launches : 0; }
+
+int split3_maxabs(split3_handle_t h, int64_t rows, int64_t cols, const float* X, int64_t ldx,
+                  float* d_maxabs, int64_t* d_bad) {
+    if (!h || rows < 0 || cols < 0 || !d_maxabs) return SPLIT3_ERR_INVALID_VALUE;
+    if (rows == 0 || cols == 0) return SPLIT3_OK;
+    if (!X || ldx < cols || !aligned(d_maxabs, 4)) return SPLIT3_ERR_INVALID_VALUE;
+    if (set_dev(h)) return SPLIT3_ERR_CUDA;
+    int n = split3::launch_maxabs(h->stream, rows, cols, X, ldx, d_maxabs,
+                                  reinterpret_cast<long long*>(d_bad), h->num_sms);
+    if (n < 0) return SPLIT3_ERR_CUDA;
+    h->last_launches = n;
+    return SPLIT3_OK;
+}
+
+int split3_split(split3_handle_t h, int64_t rows, int64_t cols, const float* X, int64_t ldx,
+                 const float* d_maxabs, uint16_t* hi, uint16_t* lo, int64_t ldp, int transpose,
+                 int32_t* d_sexp) {
+    if (!h || rows < 0 || cols < 0 || !d_maxabs) return SPLIT3_ERR_INVALID_VALUE;
+    if (transpose != 0 && transpose != 1) return SPLIT3_ERR_INVALID_VALUE;
+    if (rows == 0 || cols == 0) return SPLIT3_OK;
+    const int64_t need = transpose ? rows : cols;
+    if (!X || !hi || !lo || ldx < cols || ldp < need || ldp % 8 != 0 || !aligned(hi, 16) ||
+        !aligned(lo, 16))
+        return SPLIT3_ERR_INVALID_VALUE;
+    if (set_dev(h)) return SPLIT3_ERR_CUDA;
+    int n = transpose
+                ? split3::launch_split_t(h->stream, rows, cols, X, ldx, d_maxabs, hi, lo, ldp, d_sexp, h->num_sms)
+                : split3::launch_split(h->stream, rows, cols, X, ldx, d_maxabs, hi, lo, ldp, d_sexp, h->num_sms);
+    if (n < 0) return SPLIT3_ERR_CUDA;
+    h->last_launches = n;
+    return SPLIT3_OK;
+}
+
+int split3_gemm_planes(split3_handle_t h, int64_t M, int64_t N, int64_t K, const uint16_t* A1,
+                       const uint16_t* A2, int64_t ldpa, const int32_t* d_sA, const uint16_t* B1t,
+                       const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB, float* C,
+                       int64_t ldc, uint32_t flags) {
+    if (!h || M < 0 || N < 0 || K < 1) return SPLIT3_ERR_INVALID_VALUE;
+    if (flags & ~SPLIT3_FLAGS_MASK) return SPLIT3_ERR_INVALID_VALUE;
+    if ((flags & SPLIT3_ONE_TERM) && (flags & SPLIT3_FOUR_TERM)) return SPLIT3_ERR_INVALID_VALUE;
+    if (M == 0 || N == 0) { h->last_launches = 0; return SPLIT3_OK; }
+    const int terms = terms_of(flags);
+    if (!A1 || !B1t || !C || !d_sA || !d_sB || ldc < N || ldpa < K || ldpb < K || ldpa % 8 ||
+        ldpb % 8 || !aligned(A1, 16) || !aligned(B1t, 16))
+        return SPLIT3_ERR_INVALID_VALUE;
+    if (terms != 1 && (!A2 || !B2t || !aligned(A2, 16) || !aligned(B2t, 16)))
+        return SPLIT3_ERR_INVALID_VALUE;
+    if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return SPLIT3_ERR_NOT_IMPLEMENTED;
+    if (set_dev(h)) return SPLIT3_ERR_CUDA;
+    cudaEvent_t ev0 = nullptr, ev2 = nullptr;
+    if (h->timing && h->ev_used + 3 <= 3 * 4096) {
+        ev0 = next_event(h);
+        cudaEvent_t ev1 = next_event(h);
+        ev2 = next_event(h);
+        if (!ev0 || !ev1 || !ev2) return SPLIT3_ERR_CUDA;
+        record(h, ev0);
+        record(h, ev1);   // empty split phase
+    }
+    int err = 0;
+    int n = split3::launch_gemm3(h->stream, M, N, K, A1, A2, ldpa, d_sA, B1t, B2t, ldpb, d_sB, C,
+                                 ldc, terms, h->num_sms, &err);
+    if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
+    record(h, ev2);
+    h->last_launches = n;
+    return SPLIT3_OK;
+}
+
+int split3_sgemm(split3_handle_t h, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                 const float* B, int64_t ldb, float* C, int64_t ldc, uint32_t flags) {
+    if (!h || M < 0 || N < 0 || K < 0) return SPLIT3_ERR_INVALID_VALUE;
+    if (flags & ~SPLIT3_FLAGS_MASK) return SPLIT3_ERR_INVALID_VALUE;
+    if ((flags & SPLIT3_ONE_TERM) && (flags & SPLIT3_FOUR_TERM)) return SPLIT3_ERR_INVALID_VALUE;
+    h->last_launches = 0;
+    h->last_bad = -1;
+    if (M == 0 || N == 0) return SPLIT3_OK;
+    if (!C || ldc < N) return SPLIT3_ERR_INVALID_VALUE;
+    if (K > 0 && (!A || !B || lda < K || ldb < N)) return SPLIT3_ERR_INVALID_VALUE;
+    if (set_dev(h)) return SPLIT3_ERR_CUDA;
+    if (K == 0) {   // empty sum: C = 0
+        if (cudaMemset2DAsync(C, (size_t)ldc * 4, 0, (size_t)N * 4, (size_t)M, h->stream) != cudaSuccess)
+            return SPLIT3_ERR_CUDA;
+        return SPLIT3_OK;
+    }
+    if (!h->ws || h->ws_bytes < ws_size(M, N, K)) return SPLIT3_ERR_WORKSPACE;
+    Carve w = carve(h->ws, M, N, K);
+    const bool check = (flags & SPLIT3_CHECK_FINITE) != 0;
+    // scalars: maxA = maxB = 0.0f, sA = sB = 0, badA = badB = INT64_MAX
+    if (cudaMemsetAsync(h->ws, 0, 32, h->stream) != cudaSuccess) return SPLIT3_ERR_CUDA;
+    int launches = 0, n;
+    if (check) {
+        // INT64_MAX = 0x7FFF...FF: set the 16 bytes of badA/badB to 0xFF then clear the sign bytes
+        if (cudaMemsetAsync(w.badA, 0xFF, 16, h->stream) != cudaSuccess ||
+            cudaMemsetAsync(reinterpret_cast<uint8_t*>(w.badA) + 7, 0x7F, 1, h->stream) != cudaSuccess ||
+            cudaMemsetAsync(reinterpret_cast<uint8_t*>(w.badB) + 7, 0x7F, 1, h->stream) != cudaSuccess)
+            return SPLIT3_ERR_CUDA;
+    }
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+    if (h->timing && h->ev_used + 3 <= 3 * 4096) {
+        ev0 = next_event(h); ev1 = next_event(h); ev2 = next_event(h);
+        if (!ev0 || !ev1 || !ev2) return SPLIT3_ERR_CUDA;
+        record(h, ev0);
+    }
+    // a1: per-matrix max-abs (reading R1)
+    n = split3::launch_maxabs(h->stream, M, K, A, lda, w.maxA, check ? w.badA : nullptr, h->num_sms);
+    if (n < 0) return SPLIT3_ERR_CUDA;
+    launches += n;
+    n = split3::launch_maxabs(h->stream, K, N, B, ldb, w.maxB, check ? w.badB : nullptr, h->num_sms);
+    if (n < 0) return SPLIT3_ERR_CUDA;
+    launches += n;
+    if (check) {
+        long long bad[2];
+        if (cudaMemcpyAsync(bad, w.badA, 16, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
+            cudaStreamSynchronize(h->stream) != cudaSuccess)
+            return SPLIT3_ERR_CUDA;
+        if (bad[0] != INT64_MAX || bad[1] != INT64_MAX) {
+            h->last_bad = bad[0] != INT64_MAX ? bad[0] : M * K + bad[1];
+            h->last_launches = launches;
+            return SPLIT3_ERR_NOT_FINITE;
+        }
+    }
+    // a2: split A (planes M x K) and B (planes transposed: N x K)
+    n = split3::launch_split(h->stream, M, K, A, lda, w.maxA, w.A1, w.A2, w.ldpa, w.sA, h->num_sms);
+    if (n < 0) return SPLIT3_ERR_CUDA;
+    launches += n;
+    n = split3::launch_split_t(h->stream, K, N, B, ldb, w.maxB, w.B1t, w.B2t, w.ldpb, w.sB, h->num_sms);
+    if (n < 0) return SPLIT3_ERR_CUDA;
+    launches += n;
+    record(h, ev1);
+    // a3 + a4: tensor-core products with the fused epilogue
+    int err = 0;
+    n = split3::launch_gemm3(h->stream, M, N, K, w.A1, w.A2, w.ldpa, w.sA, w.B1t, w.B2t, w.ldpb, w.sB,
+                             C, ldc, terms_of(flags), h->num_sms, &err);
+    if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
+    record(h, ev2);
+    launches += n;
+    h->last_launches = launches;
+    return SPLIT3_OK;
+}
+
+int split3_timing_enable(split3_handle_t h, int enable) {
+    if (!h) return SPLIT3_ERR_INVALID_VALUE;
+    h->timing = enable != 0;
+    return SPLIT3_OK;
+}
+
+int split3_timing_read(split3_handle_t h, double* split_ms, double* gemm_ms, int* calls) {
+    if (!h) return SPLIT3_ERR_INVALID_VALUE;
+    double s = 0.0, g = 0.0;
+    int n = 0;
+    for (size_t i = 0; i + 3 <= h->ev_used; i += 3) {
+        float a = 0.f, b = 0.f;
+        if (cudaEventSynchronize(h->ev_pool[i + 2]) != cudaSuccess ||
+            cudaEventElapsedTime(&a, h->ev_pool[i], h->ev_pool[i + 1]) != cudaSuccess ||
+            cudaEventElapsedTime(&b, h->ev_pool[i + 1], h->ev_pool[i + 2]) != cudaSuccess)
+            return SPLIT3_ERR_CUDA;
+        s += a;
+        g += b;
+        n++;
+    }
+    h->ev_used = 0;
+    if (split_ms) *split_ms = s;
+    if (gemm_ms) *gemm_ms = g;
+    if (calls) *calls = n;
+    return SPLIT3_OK;
+}
+
+size_t split3_sgemm_host_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags) {
+    if (M < 0 || N < 0 || K < 0) return 0;
+    return split3_sgemm_workspace_size(M, N, K, flags) + align256((size_t)M * K * 4) +
+           align256((size_t)K * N * 4) + align256((size_t)M * N * 4);
+}
+
+int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const float* A_host,
+                      const float* B_host, float* C_host, uint32_t flags) {
+    if (!h || M < 0 || N < 0 || K < 0) return SPLIT3_ERR_INVALID_VALUE;
+    if (M == 0 || N == 0) return SPLIT3_OK;
+    if (!C_host || (K > 0 && (!A_host || !B_host))) return SPLIT3_ERR_INVALID_VALUE;
+    if (!h->ws || h->ws_bytes < split3_sgemm_host_workspace_size(M, N, K, flags))
+        return SPLIT3_ERR_WORKSPACE;
+    if (set_dev(h)) return SPLIT3_ERR_CUDA;
+    uint8_t* base = static_cast<uint8_t*>(h->ws) + split3_sgemm_workspace_size(M, N, K, flags);
+    float* dA = reinterpret_cast<float*>(base);
+    float* dB = reinterpret_cast<float*>(base + align256((size_t)M * K * 4));
+    float* dC = reinterpret_cast<float*>(base + align256((size_t)M * K * 4) + align256((size_t)K * N * 4));
+    if (K > 0) {
+        if (cudaMemcpyAsync(dA, A_host, (size_t)M * K * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
+            cudaMemcpyAsync(dB, B_host, (size_t)K * N * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess)
+            return SPLIT3_ERR_CUDA;
+    }
+    int st = split3_sgemm(h, M, N, K, dA, K, dB, N, dC, N, flags);
+    if (st != SPLIT3_OK) return st;
+    if (cudaMemcpyAsync(C_host, dC, (size_t)M * N * 4, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
+        cudaStreamSynchronize(h->stream) != cudaSuccess)
+        return SPLIT3_ERR_CUDA;
+    return SPLIT3_OK;
+}
+
+}  // extern "C"

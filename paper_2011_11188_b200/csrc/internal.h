@@ -1,0 +1,30 @@
+// internal.h — declarations shared by the CUDA translation units of libsplit3.so.
+// Not part of the public ABI (that is include/split3.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace split3 {
+
+// Padded plane leading dimension: a multiple of 8 elements (16 bytes, the TMA stride unit).
+inline int64_t plane_ld(int64_t k) { return ((k + 7) / 8) * 8; }
+
+// ---- split_kernels.cu ------------------------------------------------------------------
+// Each launcher returns the number of kernels it launched (>= 0) or -1 on a launch error.
+int launch_maxabs(cudaStream_t s, int64_t rows, int64_t cols, const float* X, int64_t ld,
+                  float* d_max, long long* d_bad, int num_sms);
+int launch_split(cudaStream_t s, int64_t rows, int64_t cols, const float* X, int64_t ld,
+                 const float* d_max, uint16_t* hi, uint16_t* lo, int64_t ldp, int32_t* d_sexp,
+                 int num_sms);
+int launch_split_t(cudaStream_t s, int64_t rows, int64_t cols, const float* X, int64_t ld,
+                   const float* d_max, uint16_t* hi, uint16_t* lo, int64_t ldp, int32_t* d_sexp,
+                   int num_sms);
+
+// ---- gemm3.cu --------------------------------------------------------------------------
+// terms: 1, 3 or 4.  Returns kernels launched (1) or -1 on error (*err set to a status).
+int launch_gemm3(cudaStream_t s, int64_t M, int64_t N, int64_t K,
+                 const uint16_t* A1, const uint16_t* A2, int64_t ldpa, const int32_t* d_sA,
+                 const uint16_t* B1t, const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB,
+                 float* C, int64_t ldc, int terms, int num_sms, int* err);
+
+}  // namespace split3

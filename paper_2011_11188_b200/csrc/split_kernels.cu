@@ -1,0 +1,295 @@
+// split_kernels.cu — steps a1 (scale: max-abs) and a2 (split/encode) of the hot path.
+//
+// a1: m = max |x| over finite entries (the scale keeps A1/A2 "within the
+//     limited dynamic range of fp16"; reading R1/R8 in DESIGN.md §3).  Order-independent and
+//     exact: an atomicMax on the bit pattern of |x| (non-negative floats order like uints).
+// a2: Eq. A_1: x' = x*2^-s (exact), A1 = RN16(x'), r = x' - A1 (exact in
+//     fp32, DESIGN.md §3 R5), A2 = RN16(2^11 r)  (a2 = 2^-11 a1).
+//     RN16 is cvt.rn.f16.f32 (round-to-nearest-even, subnormals kept: no FTZ in this TU).
+//
+// Both are HBM-bound streaming kernels: 4 B/el read for a1; 4 B/el read + 2x2 B/el written
+// for a2.  float4 loads, grids sized in multiples of the SM count, grid-stride loops.
+#include <cuda_fp16.h>
+#include <climits>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace split3 {
+namespace {
+
+constexpr unsigned kFiniteLimit = 0x7F800000u;   // |x| bits >= this: Inf or NaN
+
+// Block-level reduction of the per-thread max (bits) and min bad index, one atomic each.
+__device__ __forceinline__ void block_fold(unsigned m, long long bad, float* d_max, long long* d_bad) {
+    __shared__ unsigned sm[32];
+    __shared__ long long sb[32];
+    for (int o = 16; o > 0; o >>= 1) {
+        m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        bad = min(bad, (long long)__shfl_xor_sync(0xffffffffu, bad, o));
+    }
+    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { sm[w] = m; sb[w] = bad; }
+    __syncthreads();
+    if (w == 0) {
+        int nw = blockDim.x >> 5;
+        m = l < nw ? sm[l] : 0u;
+        bad = l < nw ? sb[l] : LLONG_MAX;
+        for (int o = 16; o > 0; o >>= 1) {
+            m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+            bad = min(bad, (long long)__shfl_xor_sync(0xffffffffu, bad, o));
+        }
+        if (l == 0) {
+            if (m) atomicMax(reinterpret_cast<unsigned*>(d_max), m);
+            if (d_bad && bad != LLONG_MAX) atomicMin(d_bad, bad);
+        }
+    }
+}
+
+__device__ __forceinline__ void fold1(float x, long long idx, unsigned& m, long long& bad) {
+    unsigned u = __float_as_uint(x) & 0x7FFFFFFFu;
+    if (u < kFiniteLimit) m = max(m, u);
+    else bad = min(bad, idx);
+}
+
+// Contiguous (ld == cols) matrix viewed as n floats; VEC: 16-byte aligned base.
+template <bool VEC>
+__global__ void __launch_bounds__(256) maxabs_1d_kernel(const float* __restrict__ X, int64_t n,
+                                                        float* d_max, long long* d_bad) {
+    unsigned m = 0;
+    long long bad = LLONG_MAX;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    int64_t done = 0;
+    if (VEC) {
+        const int64_t n4 = n / 4;
+        const float4* X4 = reinterpret_cast<const float4*>(X);
+        int64_t i = tid;
+        for (; i + 3 * nthr < n4; i += 4 * nthr) {          // 4 independent 16-B loads in flight
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) v[u] = __ldcs(X4 + i + u * nthr);
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                int64_t b = 4 * (i + u * nthr);
+                fold1(v[u].x, b, m, bad); fold1(v[u].y, b + 1, m, bad);
+                fold1(v[u].z, b + 2, m, bad); fold1(v[u].w, b + 3, m, bad);
+            }
+        }
+        for (; i < n4; i += nthr) {
+            float4 v = __ldcs(X4 + i);
+            int64_t b = 4 * i;
+            fold1(v.x, b, m, bad); fold1(v.y, b + 1, m, bad);
+            fold1(v.z, b + 2, m, bad); fold1(v.w, b + 3, m, bad);
+        }
+        done = n4 * 4;
+    }
+    for (int64_t i = done + tid; i < n; i += nthr) fold1(__ldcs(X + i), i, m, bad);
+    block_fold(m, bad, d_max, d_bad);
+}
+
+// Strided matrix: grid-stride over rows, threads over columns.
+__global__ void __launch_bounds__(256) maxabs_2d_kernel(const float* __restrict__ X, int64_t rows,
+                                                        int64_t cols, int64_t ld, float* d_max,
+                                                        long long* d_bad) {
+    unsigned m = 0;
+    long long bad = LLONG_MAX;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+        for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols;
+             c += (int64_t)gridDim.x * blockDim.x)
+            fold1(X[r * ld + c], r * cols + c, m, bad);
+    block_fold(m, bad, d_max, d_bad);
+}
+
+// Scale exponent from the max-abs (reading R1): s = max(floor(log2 m) - 14, -127), s(0) = 0.
+__device__ __forceinline__ int scale_exp_dev(float m) {
+    unsigned b = __float_as_uint(m);
+    if (b == 0u) return 0;
+    int E = (b >= 0x00800000u) ? (int)(b >> 23) - 127 : (31 - __clz(b)) - 149;
+    int s = E - 14;
+    return s < -127 ? -127 : s;
+}
+
+// 2^-s as an fp32 (s in [-127, 113] -> exponent field 127 - s in [14, 254]: always normal).
+__device__ __forceinline__ float pow2_neg(int s) { return __uint_as_float((unsigned)(127 - s) << 23); }
+
+// Eq. A_1 for one value: returns (A1 bits, A2 bits).  __fmul_rn/__fsub_rn forbid contraction.
+__device__ __forceinline__ void split1(float x, float f, unsigned short& h1, unsigned short& h2) {
+    float xs = __fmul_rn(x, f);                       // exact: power-of-two scaling
+    __half a1 = __float2half_rn(xs);                  // cvt.rn.f16.f32
+    float r = __fsub_rn(xs, __half2float(a1));        // exact (DESIGN.md §3 R5)
+    __half a2 = __float2half_rn(__fmul_rn(r, 2048.0f));
+    h1 = __half_as_ushort(a1);
+    h2 = __half_as_ushort(a2);
+}
+
+// Non-transposed split: planes rows x cols (ldp).  VEC: cols % 4 == 0, ld % 4 == 0, aligned.
+template <bool VEC>
+__global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ X, int64_t rows,
+                                                    int64_t cols, int64_t ld,
+                                                    const float* __restrict__ d_max,
+                                                    uint16_t* __restrict__ hi,
+                                                    uint16_t* __restrict__ lo, int64_t ldp,
+                                                    int32_t* d_sexp) {
+    const int s = scale_exp_dev(*d_max);
+    const float f = pow2_neg(s);
+    if (d_sexp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *d_sexp = s;
+    if (VEC) {
+        const int64_t c4n = cols / 4;
+        for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+            const float4* xr = reinterpret_cast<const float4*>(X + r * ld);
+            uint2* h1r = reinterpret_cast<uint2*>(hi + r * ldp);
+            uint2* h2r = reinterpret_cast<uint2*>(lo + r * ldp);
+            for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < c4n;
+                 c += (int64_t)gridDim.x * blockDim.x) {
+                float4 v = __ldcs(xr + c);
+                unsigned short a[4], b[4];
+                split1(v.x, f, a[0], b[0]); split1(v.y, f, a[1], b[1]);
+                split1(v.z, f, a[2], b[2]); split1(v.w, f, a[3], b[3]);
+                h1r[c] = make_uint2(a[0] | ((unsigned)a[1] << 16), a[2] | ((unsigned)a[3] << 16));
+                h2r[c] = make_uint2(b[0] | ((unsigned)b[1] << 16), b[2] | ((unsigned)b[3] << 16));
+            }
+        }
+    } else {
+        for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+            for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols;
+                 c += (int64_t)gridDim.x * blockDim.x) {
+                unsigned short a, b;
+                split1(X[r * ld + c], f, a, b);
+                hi[r * ldp + c] = a;
+                lo[r * ldp + c] = b;
+            }
+    }
+}
+
+// Transposed split: X is rows x cols (row-major), planes are cols x rows (ldp >= rows), i.e.
+// the K-major layout of B^T the GEMM reads.  64 x 64 tiles through shared memory: coalesced
+// float4 reads along X's rows, coalesced 16-byte writes along the planes' rows.
+constexpr int TT = 64;
+constexpr int TPAD = TT + 2;   // halves per smem row (132 B: 4-B aligned, breaks bank stride)
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) split_t_kernel(const float* __restrict__ X, int64_t rows,
+                                                      int64_t cols, int64_t ld,
+                                                      const float* __restrict__ d_max,
+                                                      uint16_t* __restrict__ hi,
+                                                      uint16_t* __restrict__ lo, int64_t ldp,
+                                                      int32_t* d_sexp) {
+    __shared__ __align__(16) unsigned short s1[TT][TPAD];
+    __shared__ __align__(16) unsigned short s2[TT][TPAD];
+    const int s = scale_exp_dev(*d_max);
+    const float f = pow2_neg(s);
+    if (d_sexp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *d_sexp = s;
+    const int t = threadIdx.x;
+    const int64_t ntr = (rows + TT - 1) / TT, ntc = (cols + TT - 1) / TT;
+    for (int64_t tile = blockIdx.x; tile < ntr * ntc; tile += gridDim.x) {
+        const int64_t r0 = (tile % ntr) * TT;   // consecutive blocks walk down X's rows (K)
+        const int64_t c0 = (tile / ntr) * TT;
+        // load + split: thread t covers X rows r0 + t/16 + 16 i, columns c0 + 4 (t%16) .. +3
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int rr = t / 16 + 16 * i;
+            const int cc = 4 * (t % 16);
+            const int64_t r = r0 + rr, c = c0 + cc;
+            float v[4] = {0.f, 0.f, 0.f, 0.f};
+            if (r < rows) {
+                if (VEC && c + 3 < cols) {
+                    float4 q = __ldcs(reinterpret_cast<const float4*>(X + r * ld + c));
+                    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; j++)
+                        if (c + j < cols) v[j] = X[r * ld + c + j];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                unsigned short a, b;
+                split1(v[j], f, a, b);
+                s1[cc + j][rr] = a;
+                s2[cc + j][rr] = b;
+            }
+        }
+        __syncthreads();
+        // store: plane row n = c0 + t/4 gets K entries r0 + 16 (t%4) .. +15 (two 16-B chunks)
+        {
+            const int nn = t / 4, kk = 16 * (t % 4);
+            const int64_t n = c0 + nn;
+            if (n < cols) {
+                const unsigned* p1 = reinterpret_cast<const unsigned*>(&s1[nn][kk]);
+                const unsigned* p2 = reinterpret_cast<const unsigned*>(&s2[nn][kk]);
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const int64_t k = r0 + kk + 8 * h;
+                    if (k < ldp) {   // chunk lies inside the padded row (ldp % 8 == 0)
+                        uint4 w1 = make_uint4(p1[4 * h], p1[4 * h + 1], p1[4 * h + 2], p1[4 * h + 3]);
+                        uint4 w2 = make_uint4(p2[4 * h], p2[4 * h + 1], p2[4 * h + 2], p2[4 * h + 3]);
+                        *reinterpret_cast<uint4*>(hi + n * ldp + k) = w1;
+                        *reinterpret_cast<uint4*>(lo + n * ldp + k) = w2;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+inline int grid_rows(int64_t rows, int num_sms, int64_t blocks_x) {
+    int64_t want = (int64_t)num_sms * 8 / (blocks_x > 0 ? blocks_x : 1);
+    if (want < 1) want = 1;
+    if (want > rows) want = rows;
+    if (want > 65535) want = 65535;
+    return (int)want;
+}
+
+}  // namespace
+
+int launch_maxabs(cudaStream_t st, int64_t rows, int64_t cols, const float* X, int64_t ld,
+                  float* d_max, long long* d_bad, int num_sms) {
+    if (rows <= 0 || cols <= 0) return 0;
+    if (ld == cols) {
+        int64_t n = rows * cols;
+        int64_t blocks = (n / 4 + 255) / 256;
+        int64_t cap = (int64_t)num_sms * 8;
+        int g = (int)(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+        if (aligned16(X)) maxabs_1d_kernel<true><<<g, 256, 0, st>>>(X, n, d_max, d_bad);
+        else maxabs_1d_kernel<false><<<g, 256, 0, st>>>(X, n, d_max, d_bad);
+    } else {
+        int64_t bx = (cols + 255) / 256;
+        if (bx > 64) bx = 64;
+        dim3 grid((unsigned)bx, (unsigned)grid_rows(rows, num_sms, bx));
+        maxabs_2d_kernel<<<grid, 256, 0, st>>>(X, rows, cols, ld, d_max, d_bad);
+    }
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_split(cudaStream_t st, int64_t rows, int64_t cols, const float* X, int64_t ld,
+                 const float* d_max, uint16_t* hi, uint16_t* lo, int64_t ldp, int32_t* d_sexp,
+                 int num_sms) {
+    if (rows <= 0 || cols <= 0) return 0;
+    const bool vec = (cols % 4 == 0) && (ld % 4 == 0) && aligned16(X);
+    const int64_t units = vec ? cols / 4 : cols;
+    int64_t bx = (units + 255) / 256;
+    if (bx > 64) bx = 64;
+    dim3 grid((unsigned)bx, (unsigned)grid_rows(rows, num_sms, bx));
+    if (vec) split_kernel<true><<<grid, 256, 0, st>>>(X, rows, cols, ld, d_max, hi, lo, ldp, d_sexp);
+    else split_kernel<false><<<grid, 256, 0, st>>>(X, rows, cols, ld, d_max, hi, lo, ldp, d_sexp);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_split_t(cudaStream_t st, int64_t rows, int64_t cols, const float* X, int64_t ld,
+                   const float* d_max, uint16_t* hi, uint16_t* lo, int64_t ldp, int32_t* d_sexp,
+                   int num_sms) {
+    if (rows <= 0 || cols <= 0) return 0;
+    const bool vec = (ld % 4 == 0) && aligned16(X);
+    int64_t tiles = ((rows + TT - 1) / TT) * ((cols + TT - 1) / TT);
+    int64_t cap = (int64_t)num_sms * 8;
+    int g = (int)(tiles < cap ? tiles : cap);
+    if (vec) split_t_kernel<true><<<g, 256, 0, st>>>(X, rows, cols, ld, d_max, hi, lo, ldp, d_sexp);
+    else split_t_kernel<false><<<g, 256, 0, st>>>(X, rows, cols, ld, d_max, hi, lo, ldp, d_sexp);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+}  // namespace split3

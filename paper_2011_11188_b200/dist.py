@@ -1,0 +1,176 @@
+"""2-D C-tile partitioner over the GPUs of one box.
+
+C = A*B with A (M x K) and B (K x N) sharded over P ranks arranged as a pr x pc grid;
+rank r = i*pc + j owns the C tile rows [i*m, (i+1)*m) x cols [j*n, (j+1)*n), m = M/pr, n = N/pc.
+
+Input ownership (inputs start sharded):
+  * A is cut into P row blocks of M/P rows; block r is owned by rank r, so the row panel i of
+    A (the rows tile (i, *) needs) is owned by the ROW GROUP {(i, 0..pc-1)}.
+  * B is cut into P column blocks of N/P columns; block c = j*pr + i is owned by rank (i, j),
+    so the column panel j is owned by the COLUMN GROUP {(0..pr-1, j)}.
+
+One step (the only exchanges are 2 floats and the plane panels; there is no reduction over K):
+  1. a1 local max-abs of the owned A block and B block;
+  2. all_reduce(MAX) of [maxA, maxB] over all ranks: the global per-matrix scale (reading R1;
+     max is exact and order-free, so every rank derives the same sA, sB as one GPU would);
+  3. a2 local split of the owned blocks with the global scale (B's block transposed: N/P x K);
+  4. all_gather of the FP16 planes: A planes over the row group -> an m x K panel; B^T planes
+     over the column group -> an n x K panel (B's column blocks are row blocks of B^T, so the
+     gather concatenates contiguously);
+  5. a3+a4 the local tcgen05 GEMM on the m x n tile.
+With m and n multiples of the GEMM tile (128), every C element is computed by the same kernel
+over the same K order as on one GPU: the P-GPU C equals the 1-GPU C bitwise.
+
+The local ops are injectable (``ops``) so the exchange logic is tested on CPU with the gloo
+backend (tests/test_dist_gloo.py); the default ops are the CUDA library's.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+import torch.distributed as dist
+
+
+def grid_for(world: int) -> tuple[int, int]:
+    """pr x pc process grid: pr = the largest divisor of world that is <= sqrt(world)."""
+    if world < 1:
+        raise ValueError("world size must be >= 1")
+    pr = 1
+    for d in range(1, int(math.isqrt(world)) + 1):
+        if world % d == 0:
+            pr = d
+    return pr, world // pr
+
+
+def coords(rank: int, world: int) -> tuple[int, int]:
+    pr, pc = grid_for(world)
+    return rank // pc, rank % pc
+
+
+def a_block_rows(M: int, world: int, rank: int) -> tuple[int, int]:
+    """Rows [r0, r1) of A owned by `rank`."""
+    if M % world:
+        raise ValueError("M must be divisible by the world size")
+    b = M // world
+    return rank * b, (rank + 1) * b
+
+
+def b_block_cols(N: int, world: int, rank: int) -> tuple[int, int]:
+    """Columns [c0, c1) of B owned by `rank` (block index j*pr + i)."""
+    if N % world:
+        raise ValueError("N must be divisible by the world size")
+    pr, pc = grid_for(world)
+    i, j = coords(rank, world)
+    b = N // world
+    c = j * pr + i
+    return c * b, (c + 1) * b
+
+
+def c_tile(M: int, N: int, world: int, rank: int) -> tuple[int, int, int, int]:
+    """(r0, r1, c0, c1) of the C tile computed by `rank`."""
+    pr, pc = grid_for(world)
+    i, j = coords(rank, world)
+    m, n = M // pr, N // pc
+    return i * m, (i + 1) * m, j * n, (j + 1) * n
+
+
+def make_groups(world: int):
+    """Row groups and column groups (every rank must call this, in the same order)."""
+    pr, pc = grid_for(world)
+    rows = [dist.new_group([i * pc + j for j in range(pc)]) for i in range(pr)]
+    cols = [dist.new_group([i * pc + j for i in range(pr)]) for j in range(pc)]
+    return rows, cols
+
+
+def _gather_rows(t: torch.Tensor, group, group_size: int) -> torch.Tensor:
+    """Concatenate each group member's `t` along dim 0 (group order = member rank order)."""
+    if group_size == 1:
+        return t
+    out = torch.empty((group_size * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+    else:
+        parts = list(out.chunk(group_size, 0))
+        dist.all_gather(parts, t.contiguous(), group=group)
+    return out
+
+
+class CudaOps:
+    """The product's local steps: the CUDA library through its binding."""
+
+    def __init__(self, h):
+        self.h = h
+
+    def maxabs_into(self, X, d_max1):
+        self.h.maxabs(X, d_max1)
+
+    def split(self, X, d_max1, transpose):
+        hi, lo, sexp = self.h.split(X, d_max1, transpose=transpose)
+        return hi, lo, sexp
+
+    def gemm(self, m, n, K, A1, A2, sA, B1t, B2t, sB, out, four_term, one_term):
+        return self.h.gemm_planes(m, n, K, A1, A2, sA, B1t, B2t, sB, out=out,
+                                  four_term=four_term, one_term=one_term)
+
+
+def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, groups=None,
+             out: torch.Tensor | None = None, four_term=False, one_term=False):
+    """One rank's share of C = A*B.  A_blk: its (M/P) x K block of A; B_blk: its K x (N/P)
+    block of B.  Returns the rank's m x n C tile (see the module docstring)."""
+    world = dist.get_world_size()
+    rank = dist.get_rank()
+    pr, pc = grid_for(world)
+    i, j = coords(rank, world)
+    K = A_blk.shape[1]
+    if groups is None:
+        groups = make_groups(world)
+    row_groups, col_groups = groups
+    dev = A_blk.device
+    # 1-2: global max-abs of A and B (exact, order-free)
+    mx = torch.zeros(2, dtype=torch.float32, device=dev)
+    ops.maxabs_into(A_blk, mx[0:1])
+    ops.maxabs_into(B_blk, mx[1:2])
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    # 3: local split with the global scale
+    a_hi, a_lo, sA = ops.split(A_blk, mx[0:1], False)
+    b_hi, b_lo, sB = ops.split(B_blk, mx[1:2], True)
+    # 4: plane panels
+    A1 = _gather_rows(a_hi, row_groups[i], pc)
+    B1t = _gather_rows(b_hi, col_groups[j], pr)
+    if one_term:
+        A2, B2t = A1, B1t
+    else:
+        A2 = _gather_rows(a_lo, row_groups[i], pc)
+        B2t = _gather_rows(b_lo, col_groups[j], pr)
+    m, n = M // pr, N // pc
+    # 5: local GEMM on the C tile
+    return ops.gemm(m, n, K, A1, A2, sA, B1t, B2t, sB, out, four_term, one_term)
+
+
+class TileGemm:
+    """bench.py's multi-GPU step: each rank owns an n x n C tile of a (pr*n) x (pc*n) x n
+    problem (weak scaling), inputs sharded as above, generated on device from seeds."""
+
+    def __init__(self, h, n: int, world: int, rank: int, four_term=False, one_term=False, seed=0):
+        from workloads import torch_matrix
+
+        self.pr, self.pc = grid_for(world)
+        self.M, self.N, self.K = self.pr * n, self.pc * n, n
+        self.h = h
+        self.ops = CudaOps(h)
+        self.groups = make_groups(world)
+        r0, r1 = a_block_rows(self.M, world, rank)
+        c0, c1 = b_block_cols(self.N, world, rank)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.A_blk = torch_matrix("uniform", r1 - r0, self.K, seed=seed * 1000 + 2 * rank, device=dev)
+        self.B_blk = torch_matrix("uniform", self.K, c1 - c0, seed=seed * 1000 + 2 * rank + 1, device=dev)
+        self.C = torch.empty((n, n), dtype=torch.float32, device=dev)
+        self.four, self.one = four_term, one_term
+
+    def run(self):
+        return sgemm_2d(self.A_blk, self.B_blk, self.M, self.N, self.ops, self.groups, out=self.C,
+                        four_term=self.four, one_term=self.one)
+
+    def launches_per_step(self) -> int:
+        return 5   # 2 max-abs + 2 split + 1 GEMM (NCCL kernels not counted)

@@ -1,0 +1,305 @@
+"""Thin Python binding of libsplit3.so (include/split3.h).
+
+Argument marshalling only: tensors are passed as device pointers, torch's current
+stream as the handle's stream and a torch uint8 tensor as the caller-owned
+workspace.  Every step of the hot path runs in the library's CUDA kernels; there
+is no CPU or PyTorch fallback — a missing library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+from . import _build
+
+LIB_PATH = _build.LIB
+
+OK = 0
+ERR_INVALID_VALUE = 1
+ERR_NOT_FINITE = 2
+ERR_WORKSPACE = 3
+ERR_CUDA = 4
+ERR_ARCH = 5
+ERR_NOT_IMPLEMENTED = 6
+
+THREE_TERM = 0
+FOUR_TERM = 1 << 0
+CHECK_FINITE = 1 << 1
+ONE_TERM = 1 << 2
+
+# every symbol include/split3.h declares (checked by tests/test_capi.py)
+EXPORTS = (
+    "split3_sgemm_create", "split3_set_stream", "split3_sgemm_destroy",
+    "split3_sgemm_workspace_size", "split3_sgemm_set_workspace", "split3_sgemm",
+    "split3_sgemm_host_workspace_size", "split3_sgemm_host", "split3_last_bad_index",
+    "split3_status_string", "split3_maxabs", "split3_split", "split3_gemm_planes",
+    "split3_last_launch_count", "split3_timing_enable", "split3_timing_read",
+)
+
+_lib = None
+_lock = threading.Lock()
+_i64 = ctypes.c_int64
+_p = ctypes.c_void_p
+
+
+class Split3Error(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {status_string(status)} ({status})")
+
+
+class NotFiniteError(Split3Error):
+    def __init__(self, status: int, what: str, index: int):
+        self.index = index
+        super().__init__(status, f"{what} (first non-finite index {index})")
+
+
+def load() -> ctypes.CDLL:
+    """Load libsplit3.so (raises if it was not built; never falls back)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                "(no CPU fallback exists)")
+        lib = ctypes.CDLL(LIB_PATH)
+        lib.split3_sgemm_create.argtypes = [ctypes.POINTER(_p), ctypes.c_int, _p]
+        lib.split3_set_stream.argtypes = [_p, _p]
+        lib.split3_sgemm_destroy.argtypes = [_p]
+        lib.split3_sgemm_workspace_size.restype = ctypes.c_size_t
+        lib.split3_sgemm_workspace_size.argtypes = [_i64, _i64, _i64, ctypes.c_uint32]
+        lib.split3_sgemm_host_workspace_size.restype = ctypes.c_size_t
+        lib.split3_sgemm_host_workspace_size.argtypes = [_i64, _i64, _i64, ctypes.c_uint32]
+        lib.split3_sgemm_set_workspace.argtypes = [_p, _p, ctypes.c_size_t]
+        lib.split3_sgemm.argtypes = [_p, _i64, _i64, _i64, _p, _i64, _p, _i64, _p, _i64, ctypes.c_uint32]
+        lib.split3_sgemm_host.argtypes = [_p, _i64, _i64, _i64, _p, _p, _p, ctypes.c_uint32]
+        lib.split3_last_bad_index.restype = _i64
+        lib.split3_last_bad_index.argtypes = [_p]
+        lib.split3_last_launch_count.argtypes = [_p]
+        lib.split3_timing_enable.argtypes = [_p, ctypes.c_int]
+        lib.split3_timing_read.argtypes = [_p, ctypes.POINTER(ctypes.c_double),
+                                           ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]
+        lib.split3_status_string.restype = ctypes.c_char_p
+        lib.split3_status_string.argtypes = [ctypes.c_int]
+        lib.split3_maxabs.argtypes = [_p, _i64, _i64, _p, _i64, _p, _p]
+        lib.split3_split.argtypes = [_p, _i64, _i64, _p, _i64, _p, _p, _p, _i64, ctypes.c_int, _p]
+        lib.split3_gemm_planes.argtypes = [_p, _i64, _i64, _i64, _p, _p, _i64, _p, _p, _p, _i64, _p,
+                                           _p, _i64, ctypes.c_uint32]
+        _lib = lib
+        return lib
+
+
+def status_string(status: int) -> str:
+    return load().split3_status_string(int(status)).decode()
+
+
+def plane_ld(k: int) -> int:
+    """Padded plane leading dimension (multiple of 8 elements), as the library uses."""
+    return (k + 7) // 8 * 8
+
+
+def _flags(four_term: bool, one_term: bool, check_finite: bool) -> int:
+    f = 0
+    if four_term:
+        f |= FOUR_TERM
+    if one_term:
+        f |= ONE_TERM
+    if check_finite:
+        f |= CHECK_FINITE
+    return f
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+class Handle:
+    """One split3 handle bound to a CUDA device; uses torch's current stream per call."""
+
+    def __init__(self, device=None):
+        lib = load()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", torch.device("cuda", device).index
+                                   if not isinstance(device, int) else device)
+        self._h = _p()
+        st = lib.split3_sgemm_create(ctypes.byref(self._h), self.device.index, None)
+        if st != OK:
+            raise Split3Error(st, "split3_sgemm_create")
+        self._ws = None
+        self._lib = lib
+
+    def close(self):
+        if self._h:
+            self._lib.split3_sgemm_destroy(self._h)
+            self._h = _p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- plumbing ---------------------------------------------------------------
+    def _bind_stream(self):
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        self._lib.split3_set_stream(self._h, s)
+
+    def _ensure_ws(self, nbytes: int):
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            st = self._lib.split3_sgemm_set_workspace(self._h, self._ws.data_ptr(), self._ws.numel())
+            if st != OK:
+                raise Split3Error(st, "split3_sgemm_set_workspace")
+
+    def workspace_size(self, M, N, K, flags=0) -> int:
+        return int(self._lib.split3_sgemm_workspace_size(M, N, K, flags))
+
+    def timing_enable(self, enable: bool = True):
+        self._lib.split3_timing_enable(self._h, int(enable))
+
+    def timing_read(self):
+        """(split_ms_total, gemm_ms_total, calls) since the last read (synchronises)."""
+        s, g, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+        st = self._lib.split3_timing_read(self._h, ctypes.byref(s), ctypes.byref(g), ctypes.byref(n))
+        if st != OK:
+            raise Split3Error(st, "split3_timing_read")
+        return s.value, g.value, n.value
+
+    def last_launch_count(self) -> int:
+        return int(self._lib.split3_last_launch_count(self._h))
+
+    # -- the whole method ---------------------------------------------------------
+    def sgemm(self, A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None,
+              four_term: bool = False, one_term: bool = False, check_finite: bool = False):
+        """C = A @ B (fp32, row-major; leading-dimension strides allowed)."""
+        _check_mat(A, "A")
+        _check_mat(B, "B")
+        M, K = A.shape
+        K2, N = B.shape
+        if K != K2:
+            raise ValueError(f"inner dimensions differ: {K} vs {K2}")
+        if out is None:
+            out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+        _check_mat(out, "C")
+        flags = _flags(four_term, one_term, check_finite)
+        self._ensure_ws(self.workspace_size(M, N, K, flags))
+        self._bind_stream()
+        st = self._lib.split3_sgemm(self._h, M, N, K, _ptr(A), _ld(A), _ptr(B), _ld(B),
+                                    _ptr(out), _ld(out), flags)
+        if st == ERR_NOT_FINITE:
+            raise NotFiniteError(st, "split3_sgemm", int(self._lib.split3_last_bad_index(self._h)))
+        if st != OK:
+            raise Split3Error(st, "split3_sgemm")
+        return out
+
+    def sgemm_host(self, A, B, out=None, four_term=False, one_term=False):
+        """C = A @ B with HOST (numpy / CPU torch) buffers: copies inside the C-ABI call."""
+        import numpy as np
+
+        A = np.ascontiguousarray(A, dtype=np.float32)
+        B = np.ascontiguousarray(B, dtype=np.float32)
+        M, K = A.shape
+        K2, N = B.shape
+        if K != K2:
+            raise ValueError("inner dimensions differ")
+        if out is None:
+            out = np.empty((M, N), np.float32)
+        flags = _flags(four_term, one_term, False)
+        self._ensure_ws(int(self._lib.split3_sgemm_host_workspace_size(M, N, K, flags)))
+        self._bind_stream()
+        st = self._lib.split3_sgemm_host(self._h, M, N, K, A.ctypes.data, B.ctypes.data,
+                                         out.ctypes.data, flags)
+        if st != OK:
+            raise Split3Error(st, "split3_sgemm_host")
+        return out
+
+    def sgemm_host_ptr(self, M, N, K, a_ptr, b_ptr, c_ptr, flags=0):
+        """Raw-pointer variant of sgemm_host (pinned torch tensors in the bench)."""
+        self._ensure_ws(int(self._lib.split3_sgemm_host_workspace_size(M, N, K, flags)))
+        self._bind_stream()
+        st = self._lib.split3_sgemm_host(self._h, M, N, K, a_ptr, b_ptr, c_ptr, flags)
+        if st != OK:
+            raise Split3Error(st, "split3_sgemm_host")
+
+    # -- lower level --------------------------------------------------------------
+    def maxabs(self, X: torch.Tensor, d_max: torch.Tensor, d_bad: torch.Tensor | None = None):
+        """Fold max|X| over finite entries into d_max (float32[1], caller-initialised)."""
+        _check_mat(X, "X")
+        self._bind_stream()
+        st = self._lib.split3_maxabs(self._h, X.shape[0], X.shape[1], _ptr(X), _ld(X),
+                                     _ptr(d_max), _ptr(d_bad))
+        if st != OK:
+            raise Split3Error(st, "split3_maxabs")
+
+    def split(self, X: torch.Tensor, d_max: torch.Tensor, transpose: bool = False,
+              hi=None, lo=None, d_sexp=None):
+        """Eq. A_1 planes of X (int16 tensors holding binary16 bits) with padded ld."""
+        _check_mat(X, "X")
+        rows, cols = X.shape
+        prow, pcol = (cols, rows) if transpose else (rows, cols)
+        ldp = plane_ld(pcol)
+        if hi is None:
+            hi = torch.empty((prow, ldp), dtype=torch.int16, device=X.device)
+        if lo is None:
+            lo = torch.empty((prow, ldp), dtype=torch.int16, device=X.device)
+        if d_sexp is None:
+            d_sexp = torch.zeros(1, dtype=torch.int32, device=X.device)
+        self._bind_stream()
+        st = self._lib.split3_split(self._h, rows, cols, _ptr(X), _ld(X), _ptr(d_max), _ptr(hi),
+                                    _ptr(lo), hi.stride(0), int(transpose), _ptr(d_sexp))
+        if st != OK:
+            raise Split3Error(st, "split3_split")
+        return hi, lo, d_sexp
+
+    def gemm_planes(self, M, N, K, A1, A2, d_sA, B1t, B2t, d_sB, out=None,
+                    four_term=False, one_term=False):
+        """C from planes: A1/A2 M x ldp, B1t/B2t N x ldp (K-major), device scale exponents."""
+        if out is None:
+            out = torch.empty((M, N), dtype=torch.float32, device=A1.device)
+        flags = _flags(four_term, one_term, False)
+        self._bind_stream()
+        st = self._lib.split3_gemm_planes(self._h, M, N, K, _ptr(A1), _ptr(A2), A1.stride(0), _ptr(d_sA),
+                                          _ptr(B1t), _ptr(B2t), B1t.stride(0), _ptr(d_sB),
+                                          _ptr(out), _ld(out), flags)
+        if st != OK:
+            raise Split3Error(st, "split3_gemm_planes")
+        return out
+
+
+def _check_mat(t, name):
+    if not isinstance(t, torch.Tensor) or t.dim() != 2:
+        raise ValueError(f"{name} must be a 2-D torch tensor")
+    if t.dtype != torch.float32:
+        raise ValueError(f"{name} must be float32, got {t.dtype}")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (use Handle.sgemm_host for host buffers)")
+    if t.stride(1) != 1 or (t.shape[0] > 1 and t.stride(0) < t.shape[1]):
+        raise ValueError(f"{name} must be row-major with unit column stride")
+
+
+def _ld(t) -> int:
+    return max(t.stride(0), t.shape[1], 1) if t.shape[0] > 1 else max(t.shape[1], 1)
+
+
+_handles: dict[int, Handle] = {}
+
+
+def handle(device=None) -> Handle:
+    idx = torch.cuda.current_device() if device is None else torch.device(device).index
+    h = _handles.get(idx)
+    if h is None:
+        h = Handle(idx)
+        _handles[idx] = h
+    return h
+
+
+def sgemm(A, B, out=None, four_term=False, one_term=False, check_finite=False):
+    """C = A @ B emulated with FP16 tensor-core GEMMs (arXiv 2011.11188, Appendix A)."""
+    return handle(A.device).sgemm(A, B, out=out, four_term=four_term, one_term=one_term,
+                                  check_finite=check_finite)

@@ -1,0 +1,329 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle, element by element.
+
+Bars (BASELINE.json north_star):
+  * planes: bit-exact vs oracle/;  max-abs and scale exponent: exact;
+  * C: ||C - C_split||_F / ||C_split||_F <= 1e-6  (C_split: oracle's fp64 split emulation)
+       ||C - C64||_F / (||A||_F ||B||_F) <= 2e-6  (C64: oracle's fp64 GEMM)
+  * integer inputs {-2..2}: C == exact product, bitwise.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from workloads import numpy_matrix, torch_matrix
+
+pytestmark = pytest.mark.gpu
+
+E_OR_TOL = 1e-6
+E64_TOL = 2e-6
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+
+
+@pytest.fixture(scope="module")
+def h():
+    import paper_2011_11188_b200 as s3
+
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    return s3.Handle(0)
+
+
+def _planes_np(t, rows, cols):
+    return t[:rows, :cols].cpu().numpy().view(np.uint16)
+
+
+def _gpu_split(h, X, transpose):
+    d_max = torch.zeros(1, dtype=torch.float32, device="cuda")
+    h.maxabs(X, d_max)
+    hi, lo, sexp = h.split(X, d_max, transpose=transpose)
+    torch.cuda.synchronize()
+    return hi, lo, int(sexp.item()), float(d_max.item())
+
+
+def _metrics(C, Csplit, C64, A, B):
+    C = C.astype(np.float64)
+    e_or = np.linalg.norm(C - Csplit) / max(np.linalg.norm(Csplit), 1e-300)
+    e64 = np.linalg.norm(C - C64) / max(np.linalg.norm(A.astype(np.float64)) * np.linalg.norm(B.astype(np.float64)), 1e-300)
+    e64rel = np.linalg.norm(C - C64) / max(np.linalg.norm(C64), 1e-300)
+    return e_or, e64, e64rel
+
+
+# ----------------------------------------------------------- a1 + a2: planes -----
+
+SPLIT_SHAPES = [(1, 1), (3, 5), (64, 64), (65, 129), (200, 333), (256, 1000), (1000, 72)]
+
+
+@pytest.mark.parametrize("kind", ["uniform", "loguni", "glorot", "int2", "fp16"])
+@pytest.mark.parametrize("shape", SPLIT_SHAPES)
+def test_planes_bit_exact(h, orc, kind, shape):
+    rows, cols = shape
+    X = numpy_matrix(kind, rows, cols, seed=rows * 7 + cols)
+    hi_o, lo_o, s_o = orc.split(X)
+    Xd = torch.from_numpy(X).cuda()
+    for transpose in (False, True):
+        hi, lo, s, m = _gpu_split(h, Xd, transpose)
+        assert m == float(np.max(np.abs(X)))
+        assert s == s_o
+        if transpose:
+            assert np.array_equal(_planes_np(hi, cols, rows), hi_o.T)
+            assert np.array_equal(_planes_np(lo, cols, rows), lo_o.T)
+        else:
+            assert np.array_equal(_planes_np(hi, rows, cols), hi_o)
+            assert np.array_equal(_planes_np(lo, rows, cols), lo_o)
+
+
+@pytest.mark.parametrize("scale", [2.0 ** -20, 1.0, 2.0 ** 14, 2.0 ** -126, 2.0 ** 100])
+def test_planes_scale_family(h, orc, scale):
+    X = (numpy_matrix("uniform", 97, 131, seed=3) * np.float32(scale)).astype(np.float32)
+    hi_o, lo_o, s_o = orc.split(X)
+    for transpose in (False, True):
+        hi, lo, s, _ = _gpu_split(h, torch.from_numpy(X).cuda(), transpose)
+        assert s == s_o
+        got_hi = _planes_np(hi, 131, 97).T if transpose else _planes_np(hi, 97, 131)
+        got_lo = _planes_np(lo, 131, 97).T if transpose else _planes_np(lo, 97, 131)
+        assert np.array_equal(got_hi, hi_o) and np.array_equal(got_lo, lo_o)
+
+
+def test_planes_strided_and_unaligned(h, orc):
+    """Leading dimension > cols and a misaligned base: scalar paths, same bits."""
+    big = numpy_matrix("loguni", 70, 103, seed=9)
+    Xd = torch.from_numpy(big).cuda()
+    sub = Xd[:, 1:100]            # ld = 103, base offset 4 bytes (not 16-B aligned)
+    X = big[:, 1:100].copy()
+    hi_o, lo_o, s_o = orc.split(X)
+    for transpose in (False, True):
+        hi, lo, s, _ = _gpu_split(h, sub, transpose)
+        assert s == s_o
+        got = _planes_np(hi, 99, 70).T if transpose else _planes_np(hi, 70, 99)
+        assert np.array_equal(got, hi_o)
+        got = _planes_np(lo, 99, 70).T if transpose else _planes_np(lo, 70, 99)
+        assert np.array_equal(got, lo_o)
+
+
+def test_maxabs_skips_nonfinite_and_reports_index(h):
+    X = numpy_matrix("uniform", 50, 60, seed=1)
+    X[7, 9] = np.nan
+    X[30, 2] = np.inf
+    Xd = torch.from_numpy(X).cuda()
+    d_max = torch.zeros(1, dtype=torch.float32, device="cuda")
+    d_bad = torch.full((1,), np.iinfo(np.int64).max, dtype=torch.int64, device="cuda")
+    h.maxabs(Xd, d_max, d_bad)
+    fin = np.isfinite(X)
+    assert float(d_max.item()) == float(np.max(np.abs(X[fin])))
+    assert int(d_bad.item()) == 7 * 60 + 9
+
+
+# ------------------------------------------------------- a3 + a4: the product -----
+
+GEMM_SHAPES = [(1, 1, 1), (64, 64, 64), (128, 128, 64), (200, 300, 100), (257, 129, 1000),
+               (130, 390, 77), (512, 512, 512), (1024, 1024, 1024), (33, 1000, 2000)]
+
+
+@pytest.mark.parametrize("terms", [3, 4, 1])
+@pytest.mark.parametrize("shape", GEMM_SHAPES)
+def test_sgemm_vs_oracle(h, orc, shape, terms):
+    M, N, K = shape
+    A = numpy_matrix("uniform", M, K, seed=M + 1)
+    B = numpy_matrix("uniform", K, N, seed=N + 2)
+    C = h.sgemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(),
+                four_term=terms == 4, one_term=terms == 1).cpu().numpy()
+    Cs = orc.sgemm(A, B, terms=terms)
+    C64 = orc.gemm64(A, B)
+    e_or, e64, e64rel = _metrics(C, Cs, C64, A, B)
+    assert e_or <= E_OR_TOL, (e_or, e64, e64rel)
+    if terms != 1:
+        assert e64 <= E64_TOL and e64rel <= 1e-6, (e_or, e64, e64rel)
+
+
+@pytest.mark.parametrize("kind", ["loguni", "glorot", "fp16"])
+def test_sgemm_distributions(h, orc, kind):
+    M, N, K = 192, 160, 700
+    A = numpy_matrix(kind, M, K, seed=5)
+    B = numpy_matrix(kind, K, N, seed=6)
+    C = h.sgemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+    Cs = orc.sgemm(A, B, terms=3)
+    e_or, _, _ = _metrics(C, Cs, orc.gemm64(A, B), A, B)
+    assert e_or <= E_OR_TOL
+
+
+@pytest.mark.parametrize("M,N,K", [(64, 64, 64), (300, 200, 4096), (256, 256, 16384)])
+def test_integer_inputs_bit_exact(h, M, N, K):
+    """Entries in {-2..2}: A2 = B2 = 0, every partial sum is an integer < 2^24: exact."""
+    A = numpy_matrix("int2", M, K, seed=1)
+    B = numpy_matrix("int2", K, N, seed=2)
+    exact = (A.astype(np.int64) @ B.astype(np.int64)).astype(np.float32)
+    for terms in (3, 4, 1):
+        C = h.sgemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(),
+                    four_term=terms == 4, one_term=terms == 1).cpu().numpy()
+        assert np.array_equal(C, exact)
+
+
+def test_three_term_equals_one_term_when_residual_zero(h):
+    """fp16-representable inputs: D_mid == 0, so 3-term C == 1-term C bitwise."""
+    A = numpy_matrix("fp16", 200, 512, seed=1) * np.float32(2.0 ** -10)
+    B = numpy_matrix("fp16", 512, 150, seed=2) * np.float32(2.0 ** -10)
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    c3 = h.sgemm(Ad, Bd).cpu().numpy()
+    c1 = h.sgemm(Ad, Bd, one_term=True).cpu().numpy()
+    assert np.array_equal(c3.view(np.uint32), c1.view(np.uint32))
+
+
+def test_strided_operands_and_output(h, orc):
+    M, N, K = 100, 90, 130
+    Abig = torch.from_numpy(numpy_matrix("uniform", M, K + 6, seed=1)).cuda()
+    Bbig = torch.from_numpy(numpy_matrix("uniform", K, N + 3, seed=2)).cuda()
+    A, B = Abig[:, 2:2 + K], Bbig[:, :N]
+    Cbig = torch.full((M, N + 5), 7.0, device="cuda")
+    C = Cbig[:, 1:1 + N]
+    h.sgemm(A, B, out=C)
+    Cs = orc.sgemm(A.cpu().numpy(), B.cpu().numpy(), terms=3)
+    e_or = np.linalg.norm(C.cpu().numpy() - Cs) / np.linalg.norm(Cs)
+    assert e_or <= E_OR_TOL
+    cb = Cbig.cpu().numpy()
+    assert np.all(cb[:, 0] == 7.0) and np.all(cb[:, N + 1:] == 7.0)
+
+
+def test_edge_cases(h):
+    import paper_2011_11188_b200 as s3
+
+    A = torch.ones((3, 0), device="cuda")
+    B = torch.ones((0, 4), device="cuda")
+    C = torch.full((3, 4), 5.0, device="cuda")
+    h.sgemm(A, B, out=C)                                    # K == 0: zero-fill
+    assert torch.all(C == 0)
+    h.sgemm(torch.ones((0, 5), device="cuda"), torch.ones((5, 4), device="cuda"))   # M == 0
+    z = h.sgemm(torch.zeros((70, 33), device="cuda"), torch.zeros((33, 20), device="cuda"))
+    assert torch.all(z == 0)
+    with pytest.raises(ValueError):
+        h.sgemm(torch.ones((3, 4), device="cuda"), torch.ones((5, 4), device="cuda"))
+    # check-finite: first offending index
+    A = torch.ones((10, 10), device="cuda")
+    A[3, 4] = float("nan")
+    with pytest.raises(s3.NotFiniteError) as ei:
+        h.sgemm(A, torch.ones((10, 6), device="cuda"), check_finite=True)
+    assert ei.value.index == 34
+    B = torch.ones((10, 6), device="cuda")
+    B[2, 5] = float("inf")
+    with pytest.raises(s3.NotFiniteError) as ei:
+        h.sgemm(torch.ones((10, 10), device="cuda"), B, check_finite=True)
+    assert ei.value.index == 100 + 17
+    # without the flag, non-finite values propagate only to the rows/cols that touch them
+    A = torch.ones((130, 64), device="cuda")
+    A[5, 3] = float("inf")
+    C = h.sgemm(A, torch.ones((64, 140), device="cuda")).cpu().numpy()
+    assert not np.all(np.isfinite(C[5])) and np.all(np.isfinite(np.delete(C, 5, axis=0)))
+    assert np.all(np.delete(C, 5, axis=0) == 64.0)
+
+
+def test_capi_error_codes(h):
+    import ctypes
+
+    import paper_2011_11188_b200.split3 as s3
+
+    lib = s3.load()
+    hd = h._h
+    assert lib.split3_sgemm(hd, 4, 4, 4, 1, 3, 1, 4, 1, 4, 0) == s3.ERR_INVALID_VALUE   # lda < K
+    assert lib.split3_sgemm(hd, 4, 4, 4, 1, 4, 1, 4, 1, 4, 1 << 7) == s3.ERR_INVALID_VALUE   # flag
+    assert lib.split3_sgemm(hd, -1, 4, 4, 1, 4, 1, 4, 1, 4, 0) == s3.ERR_INVALID_VALUE
+    assert lib.split3_sgemm(hd, 4, 4, 4, None, 4, 1, 4, 1, 4, 0) == s3.ERR_INVALID_VALUE
+    h2 = s3.Handle(0)
+    A = torch.ones((64, 64), device="cuda")
+    st = lib.split3_sgemm(h2._h, 64, 64, 64, A.data_ptr(), 64, A.data_ptr(), 64, A.data_ptr(), 64, 0)
+    assert st == s3.ERR_WORKSPACE
+    assert lib.split3_sgemm_set_workspace(h2._h, ctypes.c_void_p(A.data_ptr() + 4), 1024) == s3.ERR_INVALID_VALUE
+
+
+def test_host_buffers_roundtrip(h, orc):
+    A = numpy_matrix("uniform", 300, 200, seed=1)
+    B = numpy_matrix("uniform", 200, 100, seed=2)
+    C = h.sgemm_host(A, B)
+    Cs = orc.sgemm(A, B)
+    assert np.linalg.norm(C - Cs) / np.linalg.norm(Cs) <= E_OR_TOL
+
+
+# ------------------------------------------------ tensor-core numerics probe -----
+
+def _probe(h, a_vals, b_vals, K=64):
+    """D_hi[0,0] for A1 row 0 = a_vals, B1 column 0 = b_vals (1-term, scales 2^0)."""
+    M = N = 128
+    A1 = np.zeros((M, K), np.float16)
+    B1t = np.zeros((N, K), np.float16)
+    A1[0, :len(a_vals)] = a_vals
+    B1t[0, :len(b_vals)] = b_vals
+    A1d = torch.from_numpy(A1.view(np.int16)).cuda()
+    B1d = torch.from_numpy(B1t.view(np.int16)).cuda()
+    z = torch.zeros(1, dtype=torch.int32, device="cuda")
+    C = h.gemm_planes(M, N, K, A1d, A1d, z, B1d, B1d, z, one_term=True)
+    return float(C[0, 0].item())
+
+
+def test_tc_accumulation_probe(h):
+    """Records how tcgen05 kind::f16 rounds its FP32 accumulation (DESIGN.md §3 R9).
+
+    Values are (D - 1)/ulp(1).  Written to gpurun_out/tc_probe.json; asserts only what every
+    plausible model agrees on (exact products, subnormal fp16 inputs not flushed).
+    """
+    u = 2.0 ** -23
+    t = 2.0 ** -12
+    res = {}
+    res["P1_0.75ulp"] = (_probe(h, [1, t], [1, 1.5 * t]) - 1) / u
+    res["P1n"] = (_probe(h, [-1, -t], [1, 1.5 * t]) + 1) / u
+    res["P2_tie"] = (_probe(h, [1, t], [1, t]) - 1) / u
+    q = 2.0 ** -13
+    res["P3_1.875ulp"] = (_probe(h, [1] + [q] * 15, [1] + [q] * 15) - 1) / u
+    res["P4_two_halves"] = (_probe(h, [1, t, t], [1, t, t]) - 1) / u
+    a = [1] + [0] * 15 + [t]
+    b = [1] + [0] * 15 + [1.5 * t]
+    res["P5_cross_mma_0.75ulp"] = (_probe(h, a, b) - 1) / u
+    a = [1] + [0] * 63 + [t]
+    b = [1] + [0] * 63 + [1.5 * t]
+    res["P5b_cross_stage_0.75ulp"] = (_probe(h, a, b, K=128) - 1) / u
+    sub = _probe(h, [2.0 ** -24], [2.0 ** -24])
+    res["P6_subnormal_product"] = sub
+    # alignment width: 1 + 2^-(23+j) * 1.5 for j = 1..8 -> does the addend survive?
+    for j in range(0, 9):
+        small = 1.5 * 2.0 ** -(23 + j)
+        # split small into two fp16 factors
+        res[f"P7_align_j{j}"] = (_probe(h, [1, 2.0 ** -12], [1, small * 2 ** 12]) - 1) / u
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, "tc_probe.json"), "w") as f:
+        json.dump(res, f, indent=1)
+    print(json.dumps(res, indent=1))
+    assert sub == 2.0 ** -48
+    assert res["P2_tie"] == 0.0
+
+
+# --------------------------------------------- full size (bench configuration) -----
+
+@pytest.mark.parametrize("N,terms", [(4096, 3), (4096, 4), (16384, 3)])
+def test_full_size_sampled_parity(h, orc, N, terms):
+    """configs[1] sizes, launched exactly as bench.py does; oracle on sampled outputs."""
+    A = torch_matrix("uniform", N, N, seed=11, device="cuda")
+    B = torch_matrix("uniform", N, N, seed=12, device="cuda")
+    C = h.sgemm(A, B, four_term=terms == 4)
+    torch.cuda.synchronize()
+    rng = np.random.Generator(np.random.PCG64(N))
+    R = 48
+    rows = np.sort(rng.choice(N, R, replace=False))
+    cols = np.sort(rng.choice(N, R, replace=False))
+    An = A.cpu().numpy()
+    Bn = B.cpu().numpy()
+    Cs, sA, sB = orc.sgemm_sampled(An, Bn, rows, cols, terms=terms)
+    Cg = C[torch.from_numpy(rows).cuda()][:, torch.from_numpy(cols).cuda()].cpu().numpy().astype(np.float64)
+    # fp64 reference on the sample
+    C64 = An[rows].astype(np.float64) @ Bn[:, cols].astype(np.float64)
+    e_or = np.linalg.norm(Cg - Cs) / np.linalg.norm(Cs)
+    e64rel = np.linalg.norm(Cg - C64) / np.linalg.norm(C64)
+    # E64 over the sample, normalised as the full metric would be (unbiased Frobenius estimate)
+    scale = (N * N) / (R * R)
+    e64 = np.sqrt(scale) * np.linalg.norm(Cg - C64) / (np.linalg.norm(An.astype(np.float64)) *
+                                                      np.linalg.norm(Bn.astype(np.float64)))
+    rec = {"N": N, "terms": terms, "E_or": e_or, "E64": e64, "E64rel": e64rel, "sA": sA, "sB": sB}
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, f"parity_N{N}_t{terms}.json"), "w") as f:
+        json.dump(rec, f)
+    print(rec)
+    assert e_or <= E_OR_TOL, rec
+    assert e64 <= E64_TOL, rec

@@ -99,6 +99,7 @@ def test_encode_fp64_vs_numpy(orc):
 
 
 @pytest.mark.slow
+@pytest.mark.skipif(not os.environ.get("SPLIT3_SLOW"), reason="set SPLIT3_SLOW=1 (minutes)")
 def test_encode_vs_numpy_fp32_exhaustive(orc):
     """All 2^32 fp32 patterns (minutes; run with -m slow)."""
     for start in range(0, 1 << 32, 1 << 26):
