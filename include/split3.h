@@ -135,6 +135,14 @@ int split3_gemm_planes(split3_handle_t h, int64_t M, int64_t N, int64_t K,
  * gpu_launches count; memsets are not counted). */
 int split3_last_launch_count(split3_handle_t h);
 
+/* ---- numerics knob ------------------------------------------------------------------- */
+
+/* D_hi promotion period (DESIGN.md §3 R9): the tcgen05 FP32 accumulator truncates, so the
+ * A1*B1 product is accumulated in TMEM for at most `kblocks` 64-wide k-blocks (4*kblocks
+ * MMAs) and then added with round-to-nearest into an FP32 master.  0 = library default (2).
+ * Smaller = more accurate, more epilogue work.  Range 0..1024. */
+int split3_set_promotion(split3_handle_t h, int kblocks);
+
 /* ---- measurement hooks (bench.py's roofline; no effect on results) ---------------------- */
 
 /* enable != 0: every following split3_sgemm records CUDA events on the handle's stream around

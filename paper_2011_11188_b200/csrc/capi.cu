@@ -20,6 +20,7 @@ struct split3_ctx {
     size_t ws_bytes = 0;
     long long last_bad = -1;
     int last_launches = 0;
+    int promo_kb = 0;   // 0 = library default
     // measurement hooks: event triples (start, after split, after gemm) per timed call
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -229,7 +230,7 @@ int split3_gemm_planes(split3_handle_t h, int64_t M, int64_t N, int64_t K, const
     }
     int err = 0;
     int n = split3::launch_gemm3(h->stream, M, N, K, A1, A2, ldpa, d_sA, B1t, B2t, ldpb, d_sB, C,
-                                 ldc, terms, h->num_sms, &err);
+                                 ldc, terms, h->num_sms, h->promo_kb, &err);
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
     h->last_launches = n;
@@ -300,11 +301,17 @@ int split3_sgemm(split3_handle_t h, int64_t M, int64_t N, int64_t K, const float
     // a3 + a4: tensor-core products with the fused epilogue
     int err = 0;
     n = split3::launch_gemm3(h->stream, M, N, K, w.A1, w.A2, w.ldpa, w.sA, w.B1t, w.B2t, w.ldpb, w.sB,
-                             C, ldc, terms_of(flags), h->num_sms, &err);
+                             C, ldc, terms_of(flags), h->num_sms, h->promo_kb, &err);
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
     launches += n;
     h->last_launches = launches;
+    return SPLIT3_OK;
+}
+
+int split3_set_promotion(split3_handle_t h, int kblocks) {
+    if (!h || kblocks < 0 || kblocks > 1024) return SPLIT3_ERR_INVALID_VALUE;
+    h->promo_kb = kblocks;
     return SPLIT3_OK;
 }
 

@@ -7,17 +7,23 @@
 //     C     = (D_hi + 2^-11 D_mid [+ 2^-22 D_lo]) * 2^(sA+sB)      (DESIGN.md §3 R7)
 // FP16 inputs, FP32 accumulation -> tcgen05.mma kind::f16, D in TMEM.
 //
+// FP32 accumulation on sm_100 tcgen05 TRUNCATES (measured: tests/test_gpu_parity.py
+// ::test_tc_accumulation_probe, DESIGN.md §3 R9).  D_hi therefore accumulates in TMEM for at
+// most `promo_kb` k-blocks (4*promo_kb MMAs), after which the epilogue warps add the chunk,
+// with one round-to-nearest FP32 add, into a master copy held in registers ("promotion").
+// D_mid (weight 2^-11) and D_lo (2^-22) accumulate over the whole K in TMEM.
+//
 // sm_100a design:
-//  * persistent, one CTA per SM, static tile schedule with grouped rasterisation;
-//  * warp 0 = TMA producer (one lane): A1/A2 (128 x 64) and B1t/B2t (128 x 64) boxes per
-//    stage, 128-byte swizzle, into a STAGES-deep shared-memory ring guarded by mbarriers;
-//  * warp 1 = MMA issuer (one lane): per 16-wide k step, 3 tcgen05.mma (4 with D_lo) of
-//    M=128, N=128, K=16 into TMEM; tcgen05.commit releases the smem stage / signals the
-//    epilogue; it also owns the TMEM allocation;
-//  * warps 2..5 = epilogue: tcgen05.ld 32 columns of D_hi/D_mid(/D_lo) per step, one fma,
-//    the exact power-of-two rescale, masked float4 stores.  The accumulators are double
-//    buffered in TMEM (2 x 256 of 512 columns) so the epilogue of tile i overlaps the
-//    mainloop of tile i+1 (3-term and 1-term; 4-term uses a single 384-column buffer).
+//  * CTA pairs (cluster of 2, tcgen05 cta_group::2): one 256 x 128 C tile per pair; CTA r of
+//    the pair loads A rows [m0 + 128 r, +128) and B^T rows [n0 + 64 r, +64); the leader's
+//    single thread issues M=256, N=128, K=16 MMAs that read both CTAs' shared memory, and
+//    each CTA's TMEM holds its 128 rows of the accumulators;
+//  * persistent: gridDim.x/2 pairs walk the tiles with a static, grouped raster;
+//  * warp 0 = TMA producer, warp 1 = MMA issuer (leader CTA) + TMEM owner, warps 2..5 =
+//    epilogue (promotion + final combine + masked stores);
+//  * TMEM (512 columns per CTA): D_hi ping-pong chunk buffers [0,128) and [128,256);
+//    D_mid double-buffered across tiles at [256,384) and [384,512) (3-term).  4-term: one
+//    D_mid buffer at 256 and D_lo at 384.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -27,20 +33,31 @@
 namespace split3 {
 namespace {
 
-constexpr int BM = 128;
-constexpr int BN = 128;
+constexpr int BM = 128;                             // rows per CTA (pair: 256)
+constexpr int BN = 128;                             // columns per pair tile
+constexpr int BNH = BN / 2;                         // B^T rows loaded per CTA
 constexpr int BK = 64;                              // 64 fp16 = 128 B = one swizzle row
-constexpr int STAGES = 3;
+constexpr int STAGES = 4;
 constexpr int TILE_A_BYTES = BM * BK * 2;           // 16 KB
-constexpr int TILE_B_BYTES = BN * BK * 2;           // 16 KB
-constexpr int STAGE_BYTES = 2 * TILE_A_BYTES + 2 * TILE_B_BYTES;   // 64 KB
+constexpr int TILE_B_BYTES = BNH * BK * 2;          // 8 KB
+constexpr int STAGE_BYTES = 2 * TILE_A_BYTES + 2 * TILE_B_BYTES;   // 48 KB
 constexpr int NUM_THREADS = 192;                    // 6 warps
-constexpr int GROUP_M = 16;                         // rasterisation group (m-blocks)
+constexpr int GROUP_M = 8;                          // rasterisation group (pair m-blocks)
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;         // shared::cluster address of the leader CTA
 
 // ------------------------------------------------------------------ PTX wrappers -------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
@@ -49,8 +66,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+// arrive on the barrier at this offset in the LEADER CTA (own CTA when called by the leader)
+__device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar & PEER_MASK) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     uint32_t done;
@@ -64,12 +82,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             : "memory");
     } while (!done);
 }
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
-                                            int32_t x, int32_t y) {
+// 2-SM TMA: data lands in this CTA's smem, the transaction bytes on the leader's barrier.
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                                 int32_t x, int32_t y) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & PEER_MASK), "r"(x), "r"(y)
         : "memory");
 }
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
@@ -81,19 +100,22 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16, FP32 accumulation.
-__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
-                                        uint32_t idesc, uint32_t accumulate) {
+// D[tmem] (+)= A[smem] * B[smem]^T over the CTA pair, kind::f16, FP32 accumulation.
+__device__ __forceinline__ void mma_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
+// arrive (once) on the barrier at this offset in BOTH CTAs of the pair when the MMAs complete
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+        "h"((uint16_t)3)
+        : "memory");
 }
 // 32 lanes x 32 consecutive 32-bit columns -> 32 registers per thread.
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
@@ -145,39 +167,50 @@ __device__ __forceinline__ void tile_coords(int64_t tile, int64_t num_m, int64_t
     nb = r / gsize;
 }
 
-// Exact 2^e scaling with a single rounding (only the result can round: underflow/overflow).
-__device__ __forceinline__ float scale_pow2(float v, int e, float f, bool fast) {
-    return fast ? v * f : ldexpf(v, e);
+// Add 32 TMEM columns (one row per thread) into master[off .. off+32).
+template <int OFF>
+__device__ __forceinline__ void promote32(uint32_t taddr, float (&master)[BN]) {
+    uint32_t v[32];
+    tmem_ld32(taddr + OFF, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 32; j++) master[OFF + j] = __fadd_rn(master[OFF + j], __uint_as_float(v[j]));
 }
 
 template <int TERMS>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapA2,
              const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
-             int M, int N, int K, const int32_t* __restrict__ d_sA,
+             int M, int N, int K, int promo_kb, const int32_t* __restrict__ d_sA,
              const int32_t* __restrict__ d_sB, float* __restrict__ C, int64_t ldc) {
-    constexpr int NACC = TERMS == 1 ? 1 : (TERMS == 3 ? 2 : 3);    // accumulators per tile
-    constexpr int ACC_STAGES = (NACC * BN * 2 <= 512) ? 2 : 1;
-    constexpr uint32_t TMEM_COLS = 512;
     constexpr bool LOAD_LO = TERMS != 1;
-    constexpr uint32_t TX_BYTES = LOAD_LO ? STAGE_BYTES : TILE_A_BYTES + TILE_B_BYTES;
-    constexpr uint32_t IDESC = make_idesc(BM, BN);
+    constexpr int MID_BUFS = TERMS == 3 ? 2 : 1;      // D_mid buffers (cross-tile overlap)
+    constexpr uint32_t TX_BYTES = 2u * (LOAD_LO ? STAGE_BYTES : TILE_A_BYTES + TILE_B_BYTES);
+    constexpr uint32_t IDESC = make_idesc(2 * BM, BN);
+    constexpr uint32_t COL_HI = 0;                    // + 128 * hb
+    constexpr uint32_t COL_MID = 256;                 // + 128 * mb (3-term)
+    constexpr uint32_t COL_LO = 384;                  // 4-term
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* full_bar = bars;                       // [STAGES]
-    uint64_t* empty_bar = bars + STAGES;             // [STAGES]
-    uint64_t* tfull_bar = bars + 2 * STAGES;         // [ACC_STAGES]
-    uint64_t* tempty_bar = bars + 2 * STAGES + 2;    // [ACC_STAGES]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+    uint64_t* full_bar = bars;                        // [STAGES]   leader: TMA bytes landed
+    uint64_t* empty_bar = bars + STAGES;              // [STAGES]   both: stage consumed
+    uint64_t* hfull_bar = bars + 2 * STAGES;          // [2]        both: D_hi chunk ready
+    uint64_t* hempty_bar = bars + 2 * STAGES + 2;     // [2]        leader: D_hi chunk drained
+    uint64_t* mfull_bar = bars + 2 * STAGES + 4;      // [2]        both: D_mid (D_lo) ready
+    uint64_t* mempty_bar = bars + 2 * STAGES + 6;     // [2]        leader: D_mid drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 8);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int64_t num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+    const uint32_t crank = cluster_rank();
+    const bool leader = crank == 0;
+    const int64_t num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + BN - 1) / BN;
     const int64_t num_tiles = num_m * num_n;
     const int num_kb = (K + BK - 1) / BK;
+    const int64_t pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&mapA1); tma_prefetch(&mapB1);
@@ -186,122 +219,166 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             mbar_init(smem_u32(&full_bar[i]), 1);
             mbar_init(smem_u32(&empty_bar[i]), 1);
         }
-        for (int i = 0; i < ACC_STAGES; i++) {
-            mbar_init(smem_u32(&tfull_bar[i]), 1);
-            mbar_init(smem_u32(&tempty_bar[i]), 4);      // one arrive per epilogue warp
+        for (int i = 0; i < 2; i++) {
+            mbar_init(smem_u32(&hfull_bar[i]), 1);
+            mbar_init(smem_u32(&hempty_bar[i]), 8);      // 4 epilogue warps x 2 CTAs
+            mbar_init(smem_u32(&mfull_bar[i]), 1);
+            mbar_init(smem_u32(&mempty_bar[i]), 8);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
                      "r"(TMEM_COLS)
                      : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
     }
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ===================== TMA producer =====================
+        // ===================== TMA producer (both CTAs) =====================
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int64_t tile = pair; tile < num_tiles; tile += num_pairs) {
                 int64_t mb, nb;
                 tile_coords(tile, num_m, num_n, mb, nb);
-                const int32_t y_a = (int32_t)(mb * BM), y_b = (int32_t)(nb * BN);
+                const int32_t y_a = (int32_t)(mb * 2 * BM + crank * BM);
+                const int32_t y_b = (int32_t)(nb * BN + crank * BNH);
                 for (int kb = 0; kb < num_kb; kb++) {
                     mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
                     const uint32_t fb = smem_u32(&full_bar[stage]);
-                    mbar_expect_tx(fb, TX_BYTES);
+                    if (leader) mbar_expect_tx(fb, TX_BYTES);
                     uint8_t* st = smem + stage * STAGE_BYTES;
                     const int32_t x = kb * BK;
-                    tma_load_2d(smem_u32(st), &mapA1, fb, x, y_a);
-                    tma_load_2d(smem_u32(st + 2 * TILE_A_BYTES), &mapB1, fb, x, y_b);
+                    tma_load_2d_pair(smem_u32(st), &mapA1, fb, x, y_a);
+                    tma_load_2d_pair(smem_u32(st + 2 * TILE_A_BYTES), &mapB1, fb, x, y_b);
                     if (LOAD_LO) {
-                        tma_load_2d(smem_u32(st + TILE_A_BYTES), &mapA2, fb, x, y_a);
-                        tma_load_2d(smem_u32(st + 2 * TILE_A_BYTES + TILE_B_BYTES), &mapB2, fb, x, y_b);
+                        tma_load_2d_pair(smem_u32(st + TILE_A_BYTES), &mapA2, fb, x, y_a);
+                        tma_load_2d_pair(smem_u32(st + 2 * TILE_A_BYTES + TILE_B_BYTES), &mapB2, fb, x, y_b);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ===================== MMA issuer =====================
-        if (lane == 0) {
+        // ===================== MMA issuer (leader CTA, one thread) =====================
+        if (leader && lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            int as = 0;
-            uint32_t aphase = 0;
-            for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                mbar_wait(smem_u32(&tempty_bar[as]), aphase ^ 1);
-                tc_fence_after();
-                const uint32_t t_hi = tmem_base + (uint32_t)(as * NACC * BN);
-                const uint32_t t_mid = t_hi + BN;
-                const uint32_t t_lo = t_hi + 2 * BN;
-                for (int kb = 0; kb < num_kb; kb++) {
-                    mbar_wait(smem_u32(&full_bar[stage]), phase);
+            uint32_t cc = 0;       // global D_hi chunk counter
+            uint32_t tc = 0;       // tile counter
+            for (int64_t tile = pair; tile < num_tiles; tile += num_pairs, tc++) {
+                const uint32_t mbuf = MID_BUFS == 2 ? (tc & 1) : 0;
+                const uint32_t mphase = MID_BUFS == 2 ? ((tc >> 1) & 1) : (tc & 1);
+                if (TERMS != 1) {
+                    mbar_wait(smem_u32(&mempty_bar[mbuf]), mphase ^ 1);
                     tc_fence_after();
-                    uint8_t* st = smem + stage * STAGE_BYTES;
-                    const uint64_t a1 = sdesc_sw128(smem_u32(st));
-                    const uint64_t a2 = sdesc_sw128(smem_u32(st + TILE_A_BYTES));
-                    const uint64_t b1 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES));
-                    const uint64_t b2 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES + TILE_B_BYTES));
-#pragma unroll
-                    for (int k = 0; k < BK / 16; k++) {
-                        const uint64_t dk = (uint64_t)(2 * k);   // +32 B along K per 16 elements
-                        const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-                        mma_f16(t_hi, a1 + dk, b1 + dk, IDESC, acc);
-                        if (TERMS >= 3) {
-                            mma_f16(t_mid, a1 + dk, b2 + dk, IDESC, acc);
-                            mma_f16(t_mid, a2 + dk, b1 + dk, IDESC, 1u);
-                        }
-                        if (TERMS == 4) mma_f16(t_lo, a2 + dk, b2 + dk, IDESC, acc);
-                    }
-                    mma_commit(smem_u32(&empty_bar[stage]));      // smem stage free when done
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                mma_commit(smem_u32(&tfull_bar[as]));             // accumulators ready
-                if (++as == ACC_STAGES) { as = 0; aphase ^= 1; }
+                const uint32_t t_mid = tmem_base + COL_MID + (TERMS == 3 ? 128 * mbuf : 0);
+                const uint32_t t_lo = tmem_base + COL_LO;
+                for (int kb0 = 0; kb0 < num_kb; kb0 += promo_kb, cc++) {
+                    const uint32_t hb = cc & 1, hphase = (cc >> 1) & 1;
+                    mbar_wait(smem_u32(&hempty_bar[hb]), hphase ^ 1);
+                    tc_fence_after();
+                    const uint32_t t_hi = tmem_base + COL_HI + 128 * hb;
+                    const int kb1 = kb0 + promo_kb < num_kb ? kb0 + promo_kb : num_kb;
+                    for (int kb = kb0; kb < kb1; kb++) {
+                        mbar_wait(smem_u32(&full_bar[stage]), phase);
+                        tc_fence_after();
+                        uint8_t* st = smem + stage * STAGE_BYTES;
+                        const uint64_t a1 = sdesc_sw128(smem_u32(st));
+                        const uint64_t a2 = sdesc_sw128(smem_u32(st + TILE_A_BYTES));
+                        const uint64_t b1 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES));
+                        const uint64_t b2 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES + TILE_B_BYTES));
+#pragma unroll
+                        for (int k = 0; k < BK / 16; k++) {
+                            const uint64_t dk = (uint64_t)(2 * k);   // +32 B along K per 16 elements
+                            const uint32_t acc_hi = (kb > kb0 || k > 0) ? 1u : 0u;
+                            const uint32_t acc_md = (kb > 0 || k > 0) ? 1u : 0u;
+                            mma_pair(t_hi, a1 + dk, b1 + dk, IDESC, acc_hi);
+                            if (TERMS >= 3) {
+                                mma_pair(t_mid, a1 + dk, b2 + dk, IDESC, acc_md);
+                                mma_pair(t_mid, a2 + dk, b1 + dk, IDESC, 1u);
+                            }
+                            if (TERMS == 4) mma_pair(t_lo, a2 + dk, b2 + dk, IDESC, acc_md);
+                        }
+                        mma_commit_pair(smem_u32(&empty_bar[stage]));   // stage free in both CTAs
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    mma_commit_pair(smem_u32(&hfull_bar[hb]));          // D_hi chunk ready
+                }
+                if (TERMS != 1) mma_commit_pair(smem_u32(&mfull_bar[mbuf]));   // D_mid ready
             }
         }
     } else {
-        // ===================== epilogue (warps 2..5) =====================
+        // ===================== epilogue (warps 2..5, both CTAs) =====================
         const int quad = warp & 3;                       // TMEM lane quadrant of this warp
         const int sAB = *d_sA + *d_sB;
         const bool fast = sAB >= -126 && sAB <= 127;
         const float fscale = fast ? __uint_as_float((unsigned)(sAB + 127) << 23) : 1.0f;
         const bool vec_ok = (ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(C) & 15u) == 0);
-        int as = 0;
-        uint32_t aphase = 0;
-        for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16);
+        uint32_t cc = 0, tc = 0;
+        for (int64_t tile = pair; tile < num_tiles; tile += num_pairs, tc++) {
             int64_t mb, nb;
             tile_coords(tile, num_m, num_n, mb, nb);
-            mbar_wait(smem_u32(&tfull_bar[as]), aphase);
-            tc_fence_after();
-            const int64_t row = mb * BM + quad * 32 + lane;
-            const uint32_t t_row = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(as * NACC * BN);
-            float* crow = C + row * ldc;
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; c++) {
-                uint32_t hi[32], mid[32], lo[32];
-                tmem_ld32(t_row + c * 32, hi);
-                if (TERMS >= 3) tmem_ld32(t_row + BN + c * 32, mid);
-                if (TERMS == 4) tmem_ld32(t_row + 2 * BN + c * 32, lo);
-                tmem_ld_wait();
-                float out[32];
+            float master[BN];
 #pragma unroll
-                for (int j = 0; j < 32; j++) {
-                    float v = __uint_as_float(hi[j]);
-                    if (TERMS == 3) v = __fmaf_rn(__uint_as_float(mid[j]), 0x1p-11f, v);
-                    if (TERMS == 4)
-                        v = __fmaf_rn(__fmaf_rn(__uint_as_float(lo[j]), 0x1p-11f, __uint_as_float(mid[j])),
-                                      0x1p-11f, v);
-                    out[j] = scale_pow2(v, sAB, fscale, fast);
+            for (int j = 0; j < BN; j++) master[j] = 0.0f;
+            for (int kb0 = 0; kb0 < num_kb; kb0 += promo_kb, cc++) {
+                const uint32_t hb = cc & 1, hphase = (cc >> 1) & 1;
+                mbar_wait(smem_u32(&hfull_bar[hb]), hphase);
+                tc_fence_after();
+                const uint32_t t_hi = lane_base + COL_HI + 128 * hb;
+                promote32<0>(t_hi, master);
+                promote32<32>(t_hi, master);
+                promote32<64>(t_hi, master);
+                promote32<96>(t_hi, master);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_leader(smem_u32(&hempty_bar[hb]));
+            }
+            const uint32_t mbuf = MID_BUFS == 2 ? (tc & 1) : 0;
+            const uint32_t mphase = MID_BUFS == 2 ? ((tc >> 1) & 1) : (tc & 1);
+            if (TERMS != 1) {
+                mbar_wait(smem_u32(&mfull_bar[mbuf]), mphase);
+                tc_fence_after();
+            }
+            const int64_t row = mb * 2 * BM + crank * BM + quad * 32 + lane;
+            float* crow = C + row * ldc;
+            const uint32_t t_mid = lane_base + COL_MID + (TERMS == 3 ? 128 * mbuf : 0);
+            const uint32_t t_lo = lane_base + COL_LO;
+#pragma unroll
+            for (int c = 0; c < BN / 32; c++) {
+                float out[32];
+                if (TERMS == 1) {
+#pragma unroll
+                    for (int j = 0; j < 32; j++) out[j] = master[c * 32 + j];
+                } else {
+                    uint32_t mid[32];
+                    tmem_ld32(t_mid + c * 32, mid);
+                    if (TERMS == 4) {
+                        uint32_t lo[32];
+                        tmem_ld32(t_lo + c * 32, lo);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 32; j++)
+                            out[j] = __fmaf_rn(__fmaf_rn(__uint_as_float(lo[j]), 0x1p-11f, __uint_as_float(mid[j])),
+                                               0x1p-11f, master[c * 32 + j]);
+                    } else {
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 32; j++)
+                            out[j] = __fmaf_rn(__uint_as_float(mid[j]), 0x1p-11f, master[c * 32 + j]);
+                    }
                 }
+#pragma unroll
+                for (int j = 0; j < 32; j++) out[j] = fast ? out[j] * fscale : ldexpf(out[j], sAB);
                 const int64_t col0 = nb * BN + c * 32;
                 if (row < M) {
                     if (vec_ok && col0 + 32 <= N) {
@@ -316,18 +393,19 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     }
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[as]));
-            if (++as == ACC_STAGES) { as = 0; aphase ^= 1; }
+            if (TERMS != 1) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_leader(smem_u32(&mempty_bar[mbuf]));
+            }
         }
     }
 
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                      "r"(TMEM_COLS)
                      : "memory");
     }
@@ -369,7 +447,8 @@ bool make_plane_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K,
 template <int TERMS>
 int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap& a1,
              const CUtensorMap& a2, const CUtensorMap& b1, const CUtensorMap& b2,
-             const int32_t* d_sA, const int32_t* d_sB, float* C, int64_t ldc, int num_sms) {
+             const int32_t* d_sA, const int32_t* d_sB, float* C, int64_t ldc, int num_sms,
+             int promo_kb) {
     static bool attr_set = false;
     if (!attr_set) {
         if (cudaFuncSetAttribute(gemm3_kernel<TERMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -377,10 +456,11 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
             return -1;
         attr_set = true;
     }
-    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-    const int grid = (int)(tiles < num_sms ? tiles : num_sms);
+    const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
+    const int64_t pairs = num_sms / 2;
+    const int grid = 2 * (int)(tiles < pairs ? tiles : pairs);
     gemm3_kernel<TERMS><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(a1, a2, b1, b2, (int)M, (int)N, (int)K,
-                                                               d_sA, d_sB, C, ldc);
+                                                               promo_kb, d_sA, d_sB, C, ldc);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -389,19 +469,20 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
 int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_t* A1,
                  const uint16_t* A2, int64_t ldpa, const int32_t* d_sA, const uint16_t* B1t,
                  const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB, float* C, int64_t ldc,
-                 int terms, int num_sms, int* err) {
+                 int terms, int num_sms, int promo_kb, int* err) {
     CUtensorMap ma1, ma2, mb1, mb2;
     const uint16_t* A2e = terms == 1 ? A1 : A2;
     const uint16_t* B2e = terms == 1 ? B1t : B2t;
     if (!make_plane_map(&ma1, A1, M, K, ldpa, BM) || !make_plane_map(&ma2, A2e, M, K, ldpa, BM) ||
-        !make_plane_map(&mb1, B1t, N, K, ldpb, BN) || !make_plane_map(&mb2, B2e, N, K, ldpb, BN)) {
+        !make_plane_map(&mb1, B1t, N, K, ldpb, BNH) || !make_plane_map(&mb2, B2e, N, K, ldpb, BNH)) {
         *err = 4;   // SPLIT3_ERR_CUDA
         return -1;
     }
+    const int promo = promo_kb > 0 ? promo_kb : kDefaultPromoKb;
     int r;
-    if (terms == 1) r = launch_t<1>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms);
-    else if (terms == 4) r = launch_t<4>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms);
-    else r = launch_t<3>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms);
+    if (terms == 1) r = launch_t<1>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo);
+    else if (terms == 4) r = launch_t<4>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo);
+    else r = launch_t<3>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo);
     if (r < 0) *err = 4;
     return r;
 }

@@ -21,10 +21,14 @@ int launch_split_t(cudaStream_t s, int64_t rows, int64_t cols, const float* X, i
                    int num_sms);
 
 // ---- gemm3.cu --------------------------------------------------------------------------
+// D_hi promotion period in 64-wide k-blocks (4 MMAs each) when the handle sets none
+// (DESIGN.md §3 R9: measured truncating accumulation, promote every 8 MMAs).
+constexpr int kDefaultPromoKb = 2;
+
 // terms: 1, 3 or 4.  Returns kernels launched (1) or -1 on error (*err set to a status).
 int launch_gemm3(cudaStream_t s, int64_t M, int64_t N, int64_t K,
                  const uint16_t* A1, const uint16_t* A2, int64_t ldpa, const int32_t* d_sA,
                  const uint16_t* B1t, const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB,
-                 float* C, int64_t ldc, int terms, int num_sms, int* err);
+                 float* C, int64_t ldc, int terms, int num_sms, int promo_kb, int* err);
 
 }  // namespace split3

@@ -37,6 +37,7 @@ EXPORTS = (
     "split3_sgemm_host_workspace_size", "split3_sgemm_host", "split3_last_bad_index",
     "split3_status_string", "split3_maxabs", "split3_split", "split3_gemm_planes",
     "split3_last_launch_count", "split3_timing_enable", "split3_timing_read",
+    "split3_set_promotion",
 )
 
 _lib = None
@@ -82,6 +83,7 @@ def load() -> ctypes.CDLL:
         lib.split3_last_bad_index.argtypes = [_p]
         lib.split3_last_launch_count.argtypes = [_p]
         lib.split3_timing_enable.argtypes = [_p, ctypes.c_int]
+        lib.split3_set_promotion.argtypes = [_p, ctypes.c_int]
         lib.split3_timing_read.argtypes = [_p, ctypes.POINTER(ctypes.c_double),
                                            ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]
         lib.split3_status_string.restype = ctypes.c_char_p
@@ -159,6 +161,12 @@ class Handle:
 
     def workspace_size(self, M, N, K, flags=0) -> int:
         return int(self._lib.split3_sgemm_workspace_size(M, N, K, flags))
+
+    def set_promotion(self, kblocks: int):
+        """D_hi promotion period in 64-wide k-blocks (0 = library default)."""
+        st = self._lib.split3_set_promotion(self._h, int(kblocks))
+        if st != OK:
+            raise Split3Error(st, "split3_set_promotion")
 
     def timing_enable(self, enable: bool = True):
         self._lib.split3_timing_enable(self._h, int(enable))

@@ -327,3 +327,32 @@ def test_full_size_sampled_parity(h, orc, N, terms):
     print(rec)
     assert e_or <= E_OR_TOL, rec
     assert e64 <= E64_TOL, rec
+
+
+def test_promotion_sweep(h, orc):
+    """E_or vs the D_hi promotion period at K = 8192 (records gpurun_out/promo_sweep.json).
+
+    The default period must meet the 1e-6 bar; longer periods must not be more accurate
+    than shorter ones by more than noise (the truncation error grows with the chain length).
+    """
+    M, N, K = 256, 256, 8192
+    A = numpy_matrix("uniform", M, K, seed=31)
+    B = numpy_matrix("uniform", K, N, seed=32)
+    Cs = orc.sgemm(A, B, terms=3)
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    res = {}
+    try:
+        for p in (1, 2, 4, 8, 16, 1024):
+            h.set_promotion(p)
+            C = h.sgemm(Ad, Bd).cpu().numpy()
+            res[p] = float(np.linalg.norm(C - Cs) / np.linalg.norm(Cs))
+    finally:
+        h.set_promotion(0)
+    C = h.sgemm(Ad, Bd).cpu().numpy()
+    res["default"] = float(np.linalg.norm(C - Cs) / np.linalg.norm(Cs))
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, "promo_sweep.json"), "w") as f:
+        json.dump(res, f, indent=1)
+    print(res)
+    assert res["default"] <= E_OR_TOL
+    assert res[1] <= res[1024]
