@@ -56,6 +56,16 @@ __device__ __forceinline__ uint32_t cluster_rank() {
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return r;
 }
+// one lane of a converged warp (returns true on exactly one lane)
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -240,8 +250,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ===================== TMA producer (both CTAs) =====================
-        if (lane == 0) {
+        // ===================== TMA producer (both CTAs; warp-uniform, one elected lane) =====
+        {
             int stage = 0;
             uint32_t phase = 0;
             for (int64_t tile = pair; tile < num_tiles; tile += num_pairs) {
@@ -252,22 +262,25 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                 for (int kb = 0; kb < num_kb; kb++) {
                     mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
                     const uint32_t fb = smem_u32(&full_bar[stage]);
-                    if (leader) mbar_expect_tx(fb, TX_BYTES);
                     uint8_t* st = smem + stage * STAGE_BYTES;
                     const int32_t x = kb * BK;
-                    tma_load_2d_pair(smem_u32(st), &mapA1, fb, x, y_a);
-                    tma_load_2d_pair(smem_u32(st + 2 * TILE_A_BYTES), &mapB1, fb, x, y_b);
-                    if (LOAD_LO) {
-                        tma_load_2d_pair(smem_u32(st + TILE_A_BYTES), &mapA2, fb, x, y_a);
-                        tma_load_2d_pair(smem_u32(st + 2 * TILE_A_BYTES + TILE_B_BYTES), &mapB2, fb, x, y_b);
+                    if (elect_one()) {
+                        if (leader) mbar_expect_tx(fb, TX_BYTES);
+                        tma_load_2d_pair(smem_u32(st), &mapA1, fb, x, y_a);
+                        tma_load_2d_pair(smem_u32(st + 2 * TILE_A_BYTES), &mapB1, fb, x, y_b);
+                        if (LOAD_LO) {
+                            tma_load_2d_pair(smem_u32(st + TILE_A_BYTES), &mapA2, fb, x, y_a);
+                            tma_load_2d_pair(smem_u32(st + 2 * TILE_A_BYTES + TILE_B_BYTES), &mapB2, fb, x, y_b);
+                        }
                     }
+                    __syncwarp();
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ===================== MMA issuer (leader CTA, one thread) =====================
-        if (leader && lane == 0) {
+        // ===================== MMA issuer (leader CTA; warp-uniform, one elected lane) ======
+        if (leader) {
             int stage = 0;
             uint32_t phase = 0;
             uint32_t cc = 0;       // global D_hi chunk counter
@@ -295,24 +308,31 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                         const uint64_t a2 = sdesc_sw128(smem_u32(st + TILE_A_BYTES));
                         const uint64_t b1 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES));
                         const uint64_t b2 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES + TILE_B_BYTES));
+                        if (elect_one()) {
 #pragma unroll
-                        for (int k = 0; k < BK / 16; k++) {
-                            const uint64_t dk = (uint64_t)(2 * k);   // +32 B along K per 16 elements
-                            const uint32_t acc_hi = (kb > kb0 || k > 0) ? 1u : 0u;
-                            const uint32_t acc_md = (kb > 0 || k > 0) ? 1u : 0u;
-                            mma_pair(t_hi, a1 + dk, b1 + dk, IDESC, acc_hi);
-                            if (TERMS >= 3) {
-                                mma_pair(t_mid, a1 + dk, b2 + dk, IDESC, acc_md);
-                                mma_pair(t_mid, a2 + dk, b1 + dk, IDESC, 1u);
+                            for (int k = 0; k < BK / 16; k++) {
+                                const uint64_t dk = (uint64_t)(2 * k);   // +32 B along K per 16 elements
+                                const uint32_t acc_hi = (kb > kb0 || k > 0) ? 1u : 0u;
+                                const uint32_t acc_md = (kb > 0 || k > 0) ? 1u : 0u;
+                                mma_pair(t_hi, a1 + dk, b1 + dk, IDESC, acc_hi);
+                                if (TERMS >= 3) {
+                                    mma_pair(t_mid, a1 + dk, b2 + dk, IDESC, acc_md);
+                                    mma_pair(t_mid, a2 + dk, b1 + dk, IDESC, 1u);
+                                }
+                                if (TERMS == 4) mma_pair(t_lo, a2 + dk, b2 + dk, IDESC, acc_md);
                             }
-                            if (TERMS == 4) mma_pair(t_lo, a2 + dk, b2 + dk, IDESC, acc_md);
+                            mma_commit_pair(smem_u32(&empty_bar[stage]));   // stage free in both CTAs
                         }
-                        mma_commit_pair(smem_u32(&empty_bar[stage]));   // stage free in both CTAs
+                        __syncwarp();
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
-                    mma_commit_pair(smem_u32(&hfull_bar[hb]));          // D_hi chunk ready
+                    if (elect_one()) mma_commit_pair(smem_u32(&hfull_bar[hb]));   // D_hi chunk ready
+                    __syncwarp();
                 }
-                if (TERMS != 1) mma_commit_pair(smem_u32(&mfull_bar[mbuf]));   // D_mid ready
+                if (TERMS != 1) {
+                    if (elect_one()) mma_commit_pair(smem_u32(&mfull_bar[mbuf]));   // D_mid ready
+                    __syncwarp();
+                }
             }
         }
     } else {

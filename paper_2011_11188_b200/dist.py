@@ -90,9 +90,10 @@ def _gather_rows(t: torch.Tensor, group, group_size: int) -> torch.Tensor:
     out = torch.empty((group_size * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, t.contiguous(), group=group)
-    else:
-        parts = list(out.chunk(group_size, 0))
-        dist.all_gather(parts, t.contiguous(), group=group)
+    else:   # gloo (CPU tests): no 16-bit integer support, move the bytes
+        src = t.contiguous().view(torch.uint8)
+        parts = list(out.view(torch.uint8).chunk(group_size, 0))
+        dist.all_gather(parts, src, group=group)
     return out
 
 
