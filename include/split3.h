@@ -143,6 +143,16 @@ int split3_last_launch_count(split3_handle_t h);
  * Smaller = more accurate, more epilogue work.  Range 0..1024. */
 int split3_set_promotion(split3_handle_t h, int kblocks);
 
+/* GEMM wave lockstep (default on): the persistent GEMM's producers wait — bounded, at most
+ * 0.2 ms — for all CTA pairs at each tile boundary so that concurrent tiles share their K-window
+ * in L2 (DRAM traffic).  A scheduling hint only: results are identical either way. */
+int split3_set_wave_sync(split3_handle_t h, int enable);
+
+/* GEMM tile schedule: raster group height in 256-row tile pairs (0 = default 8) and the L2
+ * eviction policy of the A-plane and B-plane TMA loads (0 normal, 1 evict_first, 2 evict_last).
+ * Scheduling only: results are identical for every setting. */
+int split3_set_schedule(split3_handle_t h, int group_m, int l2_policy_a, int l2_policy_b);
+
 /* ---- measurement hooks (bench.py's roofline; no effect on results) ---------------------- */
 
 /* enable != 0: every following split3_sgemm records CUDA events on the handle's stream around

@@ -21,6 +21,9 @@ struct split3_ctx {
     long long last_bad = -1;
     int last_launches = 0;
     int promo_kb = 0;   // 0 = library default
+    int wave_sync = 1;  // GEMM wave lockstep hint (L2 locality)
+    split3::GemmTuneIn tune;
+    unsigned* d_counters = nullptr;   // 256 B of device scratch owned by the handle
     // measurement hooks: event triples (start, after split, after gemm) per timed call
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -137,6 +140,10 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
     c->stream = static_cast<cudaStream_t>(cuda_stream);
+    if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(&c->d_counters, 256) != cudaSuccess) {
+        delete c;
+        return SPLIT3_ERR_CUDA;
+    }
     *h = c;
     return SPLIT3_OK;
 }
@@ -148,8 +155,10 @@ int split3_set_stream(split3_handle_t h, void* cuda_stream) {
 }
 
 int split3_sgemm_destroy(split3_handle_t h) {
-    if (h)
+    if (h) {
         for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+        if (h->d_counters) cudaFree(h->d_counters);
+    }
     delete h;
     return SPLIT3_OK;
 }
@@ -230,7 +239,8 @@ int split3_gemm_planes(split3_handle_t h, int64_t M, int64_t N, int64_t K, const
     }
     int err = 0;
     int n = split3::launch_gemm3(h->stream, M, N, K, A1, A2, ldpa, d_sA, B1t, B2t, ldpb, d_sB, C,
-                                 ldc, terms, h->num_sms, h->promo_kb, &err);
+                                 ldc, terms, h->num_sms, h->promo_kb,
+                                 h->wave_sync ? h->d_counters : nullptr, h->tune, &err);
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
     h->last_launches = n;
@@ -301,11 +311,28 @@ int split3_sgemm(split3_handle_t h, int64_t M, int64_t N, int64_t K, const float
     // a3 + a4: tensor-core products with the fused epilogue
     int err = 0;
     n = split3::launch_gemm3(h->stream, M, N, K, w.A1, w.A2, w.ldpa, w.sA, w.B1t, w.B2t, w.ldpb, w.sB,
-                             C, ldc, terms_of(flags), h->num_sms, h->promo_kb, &err);
+                             C, ldc, terms_of(flags), h->num_sms, h->promo_kb,
+                             h->wave_sync ? h->d_counters : nullptr, h->tune, &err);
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
     launches += n;
     h->last_launches = launches;
+    return SPLIT3_OK;
+}
+
+int split3_set_schedule(split3_handle_t h, int group_m, int l2_policy_a, int l2_policy_b) {
+    if (!h || group_m < 0 || group_m > 4096 || l2_policy_a < 0 || l2_policy_a > 2 || l2_policy_b < 0 ||
+        l2_policy_b > 2)
+        return SPLIT3_ERR_INVALID_VALUE;
+    h->tune.group_m = group_m;
+    h->tune.pol_a = l2_policy_a;
+    h->tune.pol_b = l2_policy_b;
+    return SPLIT3_OK;
+}
+
+int split3_set_wave_sync(split3_handle_t h, int enable) {
+    if (!h) return SPLIT3_ERR_INVALID_VALUE;
+    h->wave_sync = enable != 0;
     return SPLIT3_OK;
 }
 

@@ -34,18 +34,17 @@ namespace split3 {
 namespace {
 
 constexpr int BM = 128;                             // rows per CTA (pair: 256)
-constexpr int BN = 128;                             // columns per pair tile
-constexpr int BNH = BN / 2;                         // B^T rows loaded per CTA
 constexpr int BK = 64;                              // 64 fp16 = 128 B = one swizzle row
-constexpr int STAGES = 4;
 constexpr int TILE_A_BYTES = BM * BK * 2;           // 16 KB
-constexpr int TILE_B_BYTES = BNH * BK * 2;          // 8 KB
-constexpr int STAGE_BYTES = 2 * TILE_A_BYTES + 2 * TILE_B_BYTES;   // 48 KB
-constexpr int NUM_THREADS = 192;                    // 6 warps
-constexpr int GROUP_M = 8;                          // rasterisation group (pair m-blocks)
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+constexpr int NUM_EPI_WARPS = 8;                    // 2 per TMEM lane quadrant
+constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;   // TMA warp, MMA warp, epilogue warps
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;         // shared::cluster address of the leader CTA
+
+// L2 cache-policy encodings for the .L2::cache_hint operand (as CUTLASS's CacheHintSm90).
+constexpr uint64_t kPolicyNormal = 0x1000000000000000ull;
+constexpr uint64_t kPolicyFirst = 0x12F0000000000000ull;
+constexpr uint64_t kPolicyLast = 0x14F0000000000000ull;
 
 // ------------------------------------------------------------------ PTX wrappers -------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -65,6 +64,25 @@ __device__ __forceinline__ bool elect_one() {
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(pred));
     return pred != 0;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Wave lockstep (L2 locality): every CTA's producer announces that it starts its
+// i-th tile, then waits — at most kWaveWaitNs — until all CTAs that have an i-th tile did.  A
+// performance hint only: the bounded wait can never deadlock (e.g. if not all CTAs are resident).
+constexpr uint64_t kWaveWaitNs = 200000;
+__device__ __forceinline__ void wave_sync(unsigned* counter, unsigned target) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
+    const uint64_t t0 = globaltimer_ns();
+    unsigned v;
+    do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+        if (v >= target) break;
+        __nanosleep(64);
+    } while (globaltimer_ns() - t0 < kWaveWaitNs);
 }
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -94,11 +112,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 // 2-SM TMA: data lands in this CTA's smem, the transaction bytes on the leader's barrier.
 __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar,
-                                                 int32_t x, int32_t y) {
+                                                 int32_t x, int32_t y, uint64_t policy) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & PEER_MASK), "r"(x), "r"(y)
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & PEER_MASK), "r"(x), "r"(y), "l"(policy)
         : "memory");
 }
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
@@ -141,6 +159,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
           "=r"(v[31])
         : "r"(taddr));
 }
+// 32 lanes x 16 consecutive 32-bit columns -> 16 registers per thread.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld_wait() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -165,41 +193,65 @@ __host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
          | ((uint32_t)(m >> 4) << 24);            // M >> 4
 }
 
-__device__ __forceinline__ void tile_coords(int64_t tile, int64_t num_m, int64_t num_n,
+__device__ __forceinline__ void tile_coords(int64_t tile, int64_t num_m, int64_t num_n, int group_m,
                                             int64_t& mb, int64_t& nb) {
-    const int64_t per_group = (int64_t)GROUP_M * num_n;
+    const int64_t per_group = (int64_t)group_m * num_n;
     const int64_t g = tile / per_group;
-    const int64_t first_m = g * GROUP_M;
+    const int64_t first_m = g * group_m;
     int64_t gsize = num_m - first_m;
-    if (gsize > GROUP_M) gsize = GROUP_M;
+    if (gsize > group_m) gsize = group_m;
     const int64_t r = tile - g * per_group;
     mb = first_m + r % gsize;
     nb = r / gsize;
 }
 
-// Add 32 TMEM columns (one row per thread) into master[off .. off+32).
-template <int OFF>
-__device__ __forceinline__ void promote32(uint32_t taddr, float (&master)[BN]) {
-    uint32_t v[32];
-    tmem_ld32(taddr + OFF, v);
-    tmem_ld_wait();
+
+// Tile geometry per instantiation: BN_ = 256 (3-term, 1-term) or 128 (4-term: D_lo needs TMEM).
+template <int BN_>
+struct Geo {
+    static constexpr int BNH = BN_ / 2;                               // B^T rows loaded per CTA
+    static constexpr int TILE_B_BYTES = BNH * BK * 2;
+    static constexpr int STAGE_BYTES = 2 * TILE_A_BYTES + 2 * TILE_B_BYTES;
+    static constexpr int STAGES = (220 * 1024) / STAGE_BYTES > 6 ? 6 : (220 * 1024) / STAGE_BYTES;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+// Add this thread's row of NCOL TMEM columns into master[], 16 columns per tcgen05.ld.
+template <int NCOL>
+__device__ __forceinline__ void promote_all(uint32_t taddr, float (&master)[NCOL]) {
 #pragma unroll
-    for (int j = 0; j < 32; j++) master[OFF + j] = __fadd_rn(master[OFF + j], __uint_as_float(v[j]));
+    for (int c = 0; c < NCOL / 16; c++) {
+        uint32_t v[16];
+        tmem_ld16(taddr + c * 16, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; j++) master[c * 16 + j] = __fadd_rn(master[c * 16 + j], __uint_as_float(v[j]));
+    }
 }
 
-template <int TERMS>
+template <int TERMS, int BN_>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapA2,
              const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
              int M, int N, int K, int promo_kb, const int32_t* __restrict__ d_sA,
-             const int32_t* __restrict__ d_sB, float* __restrict__ C, int64_t ldc) {
+             const int32_t* __restrict__ d_sB, float* __restrict__ C, int64_t ldc,
+             unsigned* __restrict__ wave_counter, const GemmTune tune) {
+    using G = Geo<BN_>;
+    constexpr int STAGES = G::STAGES;
+    constexpr int STAGE_BYTES = G::STAGE_BYTES;
+    constexpr int TILE_B_BYTES = G::TILE_B_BYTES;
+    constexpr int BNH = G::BNH;
     constexpr bool LOAD_LO = TERMS != 1;
-    constexpr int MID_BUFS = TERMS == 3 ? 2 : 1;      // D_mid buffers (cross-tile overlap)
+    constexpr bool HAS_MID = TERMS != 1;
+    // TMEM columns per CTA: 512.  D_hi chunk buffers (HB of them), then D_mid (+ D_lo).
+    constexpr int HB = (TERMS == 1 || BN_ == 128) ? 2 : 1;
+    constexpr uint32_t COL_MID = HB * BN_;
+    constexpr uint32_t COL_LO = COL_MID + BN_;
+    static_assert(HB * BN_ + (HAS_MID ? BN_ : 0) + (TERMS == 4 ? BN_ : 0) <= 512, "TMEM budget");
     constexpr uint32_t TX_BYTES = 2u * (LOAD_LO ? STAGE_BYTES : TILE_A_BYTES + TILE_B_BYTES);
-    constexpr uint32_t IDESC = make_idesc(2 * BM, BN);
-    constexpr uint32_t COL_HI = 0;                    // + 128 * hb
-    constexpr uint32_t COL_MID = 256;                 // + 128 * mb (3-term)
-    constexpr uint32_t COL_LO = 384;                  // 4-term
+    constexpr uint32_t IDESC = make_idesc(2 * BM, BN_);
+    constexpr int NCOL = BN_ / 2;                    // columns per epilogue warp (2 warps per quadrant)
+    constexpr uint32_t EPI_ARRIVALS = 2 * NUM_EPI_WARPS;
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -209,15 +261,15 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     uint64_t* empty_bar = bars + STAGES;              // [STAGES]   both: stage consumed
     uint64_t* hfull_bar = bars + 2 * STAGES;          // [2]        both: D_hi chunk ready
     uint64_t* hempty_bar = bars + 2 * STAGES + 2;     // [2]        leader: D_hi chunk drained
-    uint64_t* mfull_bar = bars + 2 * STAGES + 4;      // [2]        both: D_mid (D_lo) ready
-    uint64_t* mempty_bar = bars + 2 * STAGES + 6;     // [2]        leader: D_mid drained
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 8);
+    uint64_t* mfull_bar = bars + 2 * STAGES + 4;      // [1]        both: D_mid (D_lo) ready
+    uint64_t* mempty_bar = bars + 2 * STAGES + 5;     // [1]        leader: D_mid drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 6);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t crank = cluster_rank();
     const bool leader = crank == 0;
-    const int64_t num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + BN - 1) / BN;
+    const int64_t num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + BN_ - 1) / BN_;
     const int64_t num_tiles = num_m * num_n;
     const int num_kb = (K + BK - 1) / BK;
     const int64_t pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
@@ -231,10 +283,10 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         }
         for (int i = 0; i < 2; i++) {
             mbar_init(smem_u32(&hfull_bar[i]), 1);
-            mbar_init(smem_u32(&hempty_bar[i]), 8);      // 4 epilogue warps x 2 CTAs
-            mbar_init(smem_u32(&mfull_bar[i]), 1);
-            mbar_init(smem_u32(&mempty_bar[i]), 8);
+            mbar_init(smem_u32(&hempty_bar[i]), EPI_ARRIVALS);
         }
+        mbar_init(smem_u32(&mfull_bar[0]), 1);
+        mbar_init(smem_u32(&mempty_bar[0]), EPI_ARRIVALS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -251,172 +303,191 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs; warp-uniform, one elected lane) =====
-        {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int64_t tile = pair; tile < num_tiles; tile += num_pairs) {
-                int64_t mb, nb;
-                tile_coords(tile, num_m, num_n, mb, nb);
-                const int32_t y_a = (int32_t)(mb * 2 * BM + crank * BM);
-                const int32_t y_b = (int32_t)(nb * BN + crank * BNH);
-                for (int kb = 0; kb < num_kb; kb++) {
-                    mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
-                    const uint32_t fb = smem_u32(&full_bar[stage]);
-                    uint8_t* st = smem + stage * STAGE_BYTES;
-                    const int32_t x = kb * BK;
-                    if (elect_one()) {
-                        if (leader) mbar_expect_tx(fb, TX_BYTES);
-                        tma_load_2d_pair(smem_u32(st), &mapA1, fb, x, y_a);
-                        tma_load_2d_pair(smem_u32(st + 2 * TILE_A_BYTES), &mapB1, fb, x, y_b);
-                        if (LOAD_LO) {
-                            tma_load_2d_pair(smem_u32(st + TILE_A_BYTES), &mapA2, fb, x, y_a);
-                            tma_load_2d_pair(smem_u32(st + 2 * TILE_A_BYTES + TILE_B_BYTES), &mapB2, fb, x, y_b);
-                        }
+        int stage = 0;
+        uint32_t phase = 0;
+        unsigned wave_target = 0;   // cumulative arrivals expected up to this tile index
+        int64_t idx = 0;
+        for (int64_t tile = pair; tile < num_tiles; tile += num_pairs, idx++) {
+            if (wave_counter && idx > 0) {
+                int64_t active = num_tiles - idx * num_pairs;   // pairs with an idx-th tile
+                if (active > num_pairs) active = num_pairs;
+                wave_target += 2u * (unsigned)active;
+                if (elect_one()) wave_sync(wave_counter, wave_target);
+                __syncwarp();
+            }
+            int64_t mb, nb;
+            tile_coords(tile, num_m, num_n, tune.group_m, mb, nb);
+            const int32_t y_a = (int32_t)(mb * 2 * BM + crank * BM);
+            const int32_t y_b = (int32_t)(nb * BN_ + crank * BNH);
+            for (int kb = 0; kb < num_kb; kb++) {
+                mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+                const uint32_t fb = smem_u32(&full_bar[stage]);
+                uint8_t* st = smem + stage * STAGE_BYTES;
+                const int32_t x = kb * BK;
+                if (elect_one()) {
+                    if (leader) mbar_expect_tx(fb, TX_BYTES);
+                    tma_load_2d_pair(smem_u32(st), &mapA1, fb, x, y_a, tune.pol_a);
+                    tma_load_2d_pair(smem_u32(st + 2 * TILE_A_BYTES), &mapB1, fb, x, y_b, tune.pol_b);
+                    if (LOAD_LO) {
+                        tma_load_2d_pair(smem_u32(st + TILE_A_BYTES), &mapA2, fb, x, y_a, tune.pol_a);
+                        tma_load_2d_pair(smem_u32(st + 2 * TILE_A_BYTES + TILE_B_BYTES), &mapB2, fb, x, y_b,
+                                         tune.pol_b);
                     }
-                    __syncwarp();
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
+                __syncwarp();
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA; warp-uniform, one elected lane) ======
+        // Per k-block the D_mid (and D_lo) MMAs are issued BEFORE waiting for the D_hi buffer, so
+        // a promotion drain overlaps ~8 queued MMAs; at a tile start D_hi goes first (the
+        // epilogue drains D_hi before D_mid).
         if (leader) {
             int stage = 0;
             uint32_t phase = 0;
             uint32_t cc = 0;       // global D_hi chunk counter
             uint32_t tc = 0;       // tile counter
             for (int64_t tile = pair; tile < num_tiles; tile += num_pairs, tc++) {
-                const uint32_t mbuf = MID_BUFS == 2 ? (tc & 1) : 0;
-                const uint32_t mphase = MID_BUFS == 2 ? ((tc >> 1) & 1) : (tc & 1);
-                if (TERMS != 1) {
-                    mbar_wait(smem_u32(&mempty_bar[mbuf]), mphase ^ 1);
-                    tc_fence_after();
-                }
-                const uint32_t t_mid = tmem_base + COL_MID + (TERMS == 3 ? 128 * mbuf : 0);
+                const uint32_t t_mid = tmem_base + COL_MID;
                 const uint32_t t_lo = tmem_base + COL_LO;
-                for (int kb0 = 0; kb0 < num_kb; kb0 += promo_kb, cc++) {
-                    const uint32_t hb = cc & 1, hphase = (cc >> 1) & 1;
-                    mbar_wait(smem_u32(&hempty_bar[hb]), hphase ^ 1);
+                bool mid_ready = false;
+                for (int kb = 0; kb < num_kb; kb++) {
+                    const bool chunk_start = (kb % promo_kb) == 0;
+                    if (chunk_start && kb > 0) cc++;
+                    const uint32_t hb = HB == 2 ? (cc & 1) : 0;
+                    const uint32_t hphase = HB == 2 ? ((cc >> 1) & 1) : (cc & 1);
+                    const uint32_t t_hi = tmem_base + hb * BN_;
+                    mbar_wait(smem_u32(&full_bar[stage]), phase);
                     tc_fence_after();
-                    const uint32_t t_hi = tmem_base + COL_HI + 128 * hb;
-                    const int kb1 = kb0 + promo_kb < num_kb ? kb0 + promo_kb : num_kb;
-                    for (int kb = kb0; kb < kb1; kb++) {
-                        mbar_wait(smem_u32(&full_bar[stage]), phase);
-                        tc_fence_after();
-                        uint8_t* st = smem + stage * STAGE_BYTES;
-                        const uint64_t a1 = sdesc_sw128(smem_u32(st));
-                        const uint64_t a2 = sdesc_sw128(smem_u32(st + TILE_A_BYTES));
-                        const uint64_t b1 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES));
-                        const uint64_t b2 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES + TILE_B_BYTES));
+                    uint8_t* st = smem + stage * STAGE_BYTES;
+                    const uint64_t a1 = sdesc_sw128(smem_u32(st));
+                    const uint64_t a2 = sdesc_sw128(smem_u32(st + TILE_A_BYTES));
+                    const uint64_t b1 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES));
+                    const uint64_t b2 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES + TILE_B_BYTES));
+                    const bool hi_first = kb == 0;
+                    auto issue_mid = [&]() {
+                        if (!HAS_MID) return;
+                        if (!mid_ready) {
+                            mbar_wait(smem_u32(&mempty_bar[0]), (tc & 1) ^ 1);
+                            tc_fence_after();
+                            mid_ready = true;
+                        }
                         if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < BK / 16; k++) {
-                                const uint64_t dk = (uint64_t)(2 * k);   // +32 B along K per 16 elements
-                                const uint32_t acc_hi = (kb > kb0 || k > 0) ? 1u : 0u;
-                                const uint32_t acc_md = (kb > 0 || k > 0) ? 1u : 0u;
-                                mma_pair(t_hi, a1 + dk, b1 + dk, IDESC, acc_hi);
-                                if (TERMS >= 3) {
-                                    mma_pair(t_mid, a1 + dk, b2 + dk, IDESC, acc_md);
-                                    mma_pair(t_mid, a2 + dk, b1 + dk, IDESC, 1u);
-                                }
-                                if (TERMS == 4) mma_pair(t_lo, a2 + dk, b2 + dk, IDESC, acc_md);
+                                const uint64_t dk = (uint64_t)(2 * k);
+                                const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+                                mma_pair(t_mid, a1 + dk, b2 + dk, IDESC, acc);
+                                mma_pair(t_mid, a2 + dk, b1 + dk, IDESC, 1u);
+                                if (TERMS == 4) mma_pair(t_lo, a2 + dk, b2 + dk, IDESC, acc);
                             }
-                            mma_commit_pair(smem_u32(&empty_bar[stage]));   // stage free in both CTAs
                         }
                         __syncwarp();
-                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    };
+                    auto issue_hi = [&]() {
+                        if (chunk_start) {
+                            mbar_wait(smem_u32(&hempty_bar[hb]), hphase ^ 1);
+                            tc_fence_after();
+                        }
+                        if (elect_one()) {
+#pragma unroll
+                            for (int k = 0; k < BK / 16; k++) {
+                                const uint64_t dk = (uint64_t)(2 * k);
+                                mma_pair(t_hi, a1 + dk, b1 + dk, IDESC, (!chunk_start || k > 0) ? 1u : 0u);
+                            }
+                        }
+                        __syncwarp();
+                    };
+                    if (hi_first) { issue_hi(); issue_mid(); } else { issue_mid(); issue_hi(); }
+                    if (elect_one()) {
+                        mma_commit_pair(smem_u32(&empty_bar[stage]));        // stage free in both CTAs
+                        const bool chunk_end = ((kb + 1) % promo_kb) == 0 || kb + 1 == num_kb;
+                        if (chunk_end) mma_commit_pair(smem_u32(&hfull_bar[hb]));   // D_hi chunk ready
+                        if (HAS_MID && kb + 1 == num_kb) mma_commit_pair(smem_u32(&mfull_bar[0]));
                     }
-                    if (elect_one()) mma_commit_pair(smem_u32(&hfull_bar[hb]));   // D_hi chunk ready
                     __syncwarp();
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                if (TERMS != 1) {
-                    if (elect_one()) mma_commit_pair(smem_u32(&mfull_bar[mbuf]));   // D_mid ready
-                    __syncwarp();
-                }
+                cc++;
             }
         }
     } else {
-        // ===================== epilogue (warps 2..5, both CTAs) =====================
-        const int quad = warp & 3;                       // TMEM lane quadrant of this warp
+        // ===================== epilogue (warps 2..9, both CTAs) =====================
+        // warp w reads TMEM lane quadrant (w % 4) and columns [NCOL * half, + NCOL).
+        const int quad = warp & 3;
+        const int half = (warp - 2) >> 2;
         const int sAB = *d_sA + *d_sB;
         const bool fast = sAB >= -126 && sAB <= 127;
         const float fscale = fast ? __uint_as_float((unsigned)(sAB + 127) << 23) : 1.0f;
         const bool vec_ok = (ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(C) & 15u) == 0);
-        const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16);
+        const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * NCOL);
         uint32_t cc = 0, tc = 0;
         for (int64_t tile = pair; tile < num_tiles; tile += num_pairs, tc++) {
             int64_t mb, nb;
-            tile_coords(tile, num_m, num_n, mb, nb);
-            float master[BN];
+            tile_coords(tile, num_m, num_n, tune.group_m, mb, nb);
+            float master[NCOL];
 #pragma unroll
-            for (int j = 0; j < BN; j++) master[j] = 0.0f;
+            for (int j = 0; j < NCOL; j++) master[j] = 0.0f;
             for (int kb0 = 0; kb0 < num_kb; kb0 += promo_kb, cc++) {
-                const uint32_t hb = cc & 1, hphase = (cc >> 1) & 1;
+                const uint32_t hb = HB == 2 ? (cc & 1) : 0;
+                const uint32_t hphase = HB == 2 ? ((cc >> 1) & 1) : (cc & 1);
                 mbar_wait(smem_u32(&hfull_bar[hb]), hphase);
                 tc_fence_after();
-                const uint32_t t_hi = lane_base + COL_HI + 128 * hb;
-                promote32<0>(t_hi, master);
-                promote32<32>(t_hi, master);
-                promote32<64>(t_hi, master);
-                promote32<96>(t_hi, master);
+                promote_all<NCOL>(lane_base + hb * BN_, master);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_leader(smem_u32(&hempty_bar[hb]));
             }
-            const uint32_t mbuf = MID_BUFS == 2 ? (tc & 1) : 0;
-            const uint32_t mphase = MID_BUFS == 2 ? ((tc >> 1) & 1) : (tc & 1);
-            if (TERMS != 1) {
-                mbar_wait(smem_u32(&mfull_bar[mbuf]), mphase);
+            if (HAS_MID) {
+                mbar_wait(smem_u32(&mfull_bar[0]), tc & 1);
                 tc_fence_after();
-            }
-            const int64_t row = mb * 2 * BM + crank * BM + quad * 32 + lane;
-            float* crow = C + row * ldc;
-            const uint32_t t_mid = lane_base + COL_MID + (TERMS == 3 ? 128 * mbuf : 0);
-            const uint32_t t_lo = lane_base + COL_LO;
 #pragma unroll
-            for (int c = 0; c < BN / 32; c++) {
-                float out[32];
-                if (TERMS == 1) {
-#pragma unroll
-                    for (int j = 0; j < 32; j++) out[j] = master[c * 32 + j];
-                } else {
-                    uint32_t mid[32];
-                    tmem_ld32(t_mid + c * 32, mid);
+                for (int c = 0; c < NCOL / 16; c++) {
+                    uint32_t mid[16];
+                    tmem_ld16(lane_base + COL_MID + c * 16, mid);
                     if (TERMS == 4) {
-                        uint32_t lo[32];
-                        tmem_ld32(t_lo + c * 32, lo);
+                        uint32_t lo[16];
+                        tmem_ld16(lane_base + COL_LO + c * 16, lo);
                         tmem_ld_wait();
 #pragma unroll
-                        for (int j = 0; j < 32; j++)
-                            out[j] = __fmaf_rn(__fmaf_rn(__uint_as_float(lo[j]), 0x1p-11f, __uint_as_float(mid[j])),
-                                               0x1p-11f, master[c * 32 + j]);
+                        for (int j = 0; j < 16; j++)
+                            master[c * 16 + j] = __fmaf_rn(
+                                __fmaf_rn(__uint_as_float(lo[j]), 0x1p-11f, __uint_as_float(mid[j])), 0x1p-11f,
+                                master[c * 16 + j]);
                     } else {
                         tmem_ld_wait();
 #pragma unroll
-                        for (int j = 0; j < 32; j++)
-                            out[j] = __fmaf_rn(__uint_as_float(mid[j]), 0x1p-11f, master[c * 32 + j]);
+                        for (int j = 0; j < 16; j++)
+                            master[c * 16 + j] = __fmaf_rn(__uint_as_float(mid[j]), 0x1p-11f, master[c * 16 + j]);
                     }
                 }
-#pragma unroll
-                for (int j = 0; j < 32; j++) out[j] = fast ? out[j] * fscale : ldexpf(out[j], sAB);
-                const int64_t col0 = nb * BN + c * 32;
-                if (row < M) {
-                    if (vec_ok && col0 + 32 <= N) {
-                        float4* dst = reinterpret_cast<float4*>(crow + col0);
-#pragma unroll
-                        for (int j = 0; j < 8; j++)
-                            dst[j] = make_float4(out[4 * j], out[4 * j + 1], out[4 * j + 2], out[4 * j + 3]);
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 32; j++)
-                            if (col0 + j < N) crow[col0 + j] = out[j];
-                    }
-                }
-            }
-            if (TERMS != 1) {
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive_leader(smem_u32(&mempty_bar[mbuf]));
+                if (lane == 0) mbar_arrive_leader(smem_u32(&mempty_bar[0]));   // D_mid free early
+            }
+            if (fast) {                                  // warp-uniform branch
+#pragma unroll
+                for (int j = 0; j < NCOL; j++) master[j] = master[j] * fscale;
+            } else {                                     // 2^sAB outside the fp32 normal range:
+                const double fd = __longlong_as_double((long long)(sAB + 1023) << 52);   // exact in fp64,
+#pragma unroll                                               // then one rounding to fp32
+                for (int j = 0; j < NCOL; j++) master[j] = __double2float_rn(__dmul_rn((double)master[j], fd));
+            }
+            const int64_t row = mb * 2 * BM + crank * BM + quad * 32 + lane;
+            const int64_t col0 = nb * BN_ + half * NCOL;
+            if (row < M) {
+                float* crow = C + row * ldc + col0;
+                if (vec_ok && col0 + NCOL <= N) {
+#pragma unroll
+                    for (int j = 0; j < NCOL / 4; j++)
+                        reinterpret_cast<float4*>(crow)[j] =
+                            make_float4(master[4 * j], master[4 * j + 1], master[4 * j + 2], master[4 * j + 3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < NCOL; j++)
+                        if (col0 + j < N) crow[j] = master[j];
+                }
             }
         }
     }
@@ -464,23 +535,26 @@ bool make_plane_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K,
     return r == CUDA_SUCCESS;
 }
 
-template <int TERMS>
+template <int TERMS, int BN_>
 int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap& a1,
              const CUtensorMap& a2, const CUtensorMap& b1, const CUtensorMap& b2,
              const int32_t* d_sA, const int32_t* d_sB, float* C, int64_t ldc, int num_sms,
-             int promo_kb) {
+             int promo_kb, unsigned* wave_counter, const GemmTune& tune) {
+    constexpr int SMEM_BYTES = Geo<BN_>::SMEM;
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(gemm3_kernel<TERMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(gemm3_kernel<TERMS, BN_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  SMEM_BYTES) != cudaSuccess)
             return -1;
         attr_set = true;
     }
-    const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
+    const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN_ - 1) / BN_);
     const int64_t pairs = num_sms / 2;
     const int grid = 2 * (int)(tiles < pairs ? tiles : pairs);
-    gemm3_kernel<TERMS><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(a1, a2, b1, b2, (int)M, (int)N, (int)K,
-                                                               promo_kb, d_sA, d_sB, C, ldc);
+    if (wave_counter && cudaMemsetAsync(wave_counter, 0, sizeof(unsigned), st) != cudaSuccess) return -1;
+    gemm3_kernel<TERMS, BN_><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(a1, a2, b1, b2, (int)M, (int)N, (int)K,
+                                                               promo_kb, d_sA, d_sB, C, ldc, wave_counter,
+                                                               tune);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -489,20 +563,27 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
 int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_t* A1,
                  const uint16_t* A2, int64_t ldpa, const int32_t* d_sA, const uint16_t* B1t,
                  const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB, float* C, int64_t ldc,
-                 int terms, int num_sms, int promo_kb, int* err) {
+                 int terms, int num_sms, int promo_kb, unsigned* wave_counter, const GemmTuneIn& tin,
+                 int* err) {
     CUtensorMap ma1, ma2, mb1, mb2;
     const uint16_t* A2e = terms == 1 ? A1 : A2;
     const uint16_t* B2e = terms == 1 ? B1t : B2t;
+    const int bnh = (terms == 4 ? 128 : 256) / 2;
     if (!make_plane_map(&ma1, A1, M, K, ldpa, BM) || !make_plane_map(&ma2, A2e, M, K, ldpa, BM) ||
-        !make_plane_map(&mb1, B1t, N, K, ldpb, BNH) || !make_plane_map(&mb2, B2e, N, K, ldpb, BNH)) {
+        !make_plane_map(&mb1, B1t, N, K, ldpb, bnh) || !make_plane_map(&mb2, B2e, N, K, ldpb, bnh)) {
         *err = 4;   // SPLIT3_ERR_CUDA
         return -1;
     }
     const int promo = promo_kb > 0 ? promo_kb : kDefaultPromoKb;
+    GemmTune tune;
+    tune.group_m = tin.group_m > 0 ? tin.group_m : kDefaultGroupM;
+    auto pol = [](int p) { return p == 1 ? kPolicyFirst : (p == 2 ? kPolicyLast : kPolicyNormal); };
+    tune.pol_a = pol(tin.pol_a);
+    tune.pol_b = pol(tin.pol_b);
     int r;
-    if (terms == 1) r = launch_t<1>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo);
-    else if (terms == 4) r = launch_t<4>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo);
-    else r = launch_t<3>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo);
+    if (terms == 1) r = launch_t<1, 256>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune);
+    else if (terms == 4) r = launch_t<4, 128>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune);
+    else r = launch_t<3, 256>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune);
     if (r < 0) *err = 4;
     return r;
 }

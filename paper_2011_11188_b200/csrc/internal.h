@@ -25,10 +25,22 @@ int launch_split_t(cudaStream_t s, int64_t rows, int64_t cols, const float* X, i
 // (DESIGN.md §3 R9: measured truncating accumulation, promote every 8 MMAs).
 constexpr int kDefaultPromoKb = 2;
 
+// GEMM scheduling knobs (results never depend on them).
+constexpr int kDefaultGroupM = 8;     // raster group, in pair m-blocks
+struct GemmTuneIn {
+    int group_m = 0;                  // 0 = default
+    int pol_a = 0, pol_b = 0;         // L2 policy for A / B plane loads: 0 normal, 1 evict_first, 2 evict_last
+};
+struct GemmTune {
+    int group_m;
+    uint64_t pol_a, pol_b;
+};
+
 // terms: 1, 3 or 4.  Returns kernels launched (1) or -1 on error (*err set to a status).
 int launch_gemm3(cudaStream_t s, int64_t M, int64_t N, int64_t K,
                  const uint16_t* A1, const uint16_t* A2, int64_t ldpa, const int32_t* d_sA,
                  const uint16_t* B1t, const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB,
-                 float* C, int64_t ldc, int terms, int num_sms, int promo_kb, int* err);
+                 float* C, int64_t ldc, int terms, int num_sms, int promo_kb,
+                 unsigned* wave_counter, const GemmTuneIn& tune, int* err);
 
 }  // namespace split3

@@ -37,7 +37,7 @@ EXPORTS = (
     "split3_sgemm_host_workspace_size", "split3_sgemm_host", "split3_last_bad_index",
     "split3_status_string", "split3_maxabs", "split3_split", "split3_gemm_planes",
     "split3_last_launch_count", "split3_timing_enable", "split3_timing_read",
-    "split3_set_promotion",
+    "split3_set_promotion", "split3_set_wave_sync", "split3_set_schedule",
 )
 
 _lib = None
@@ -84,6 +84,8 @@ def load() -> ctypes.CDLL:
         lib.split3_last_launch_count.argtypes = [_p]
         lib.split3_timing_enable.argtypes = [_p, ctypes.c_int]
         lib.split3_set_promotion.argtypes = [_p, ctypes.c_int]
+        lib.split3_set_wave_sync.argtypes = [_p, ctypes.c_int]
+        lib.split3_set_schedule.argtypes = [_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         lib.split3_timing_read.argtypes = [_p, ctypes.POINTER(ctypes.c_double),
                                            ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]
         lib.split3_status_string.restype = ctypes.c_char_p
@@ -167,6 +169,16 @@ class Handle:
         st = self._lib.split3_set_promotion(self._h, int(kblocks))
         if st != OK:
             raise Split3Error(st, "split3_set_promotion")
+
+    def set_wave_sync(self, enable: bool):
+        st = self._lib.split3_set_wave_sync(self._h, int(enable))
+        if st != OK:
+            raise Split3Error(st, "split3_set_wave_sync")
+
+    def set_schedule(self, group_m: int = 0, l2_policy_a: int = 0, l2_policy_b: int = 0):
+        st = self._lib.split3_set_schedule(self._h, group_m, l2_policy_a, l2_policy_b)
+        if st != OK:
+            raise Split3Error(st, "split3_set_schedule")
 
     def timing_enable(self, enable: bool = True):
         self._lib.split3_timing_enable(self._h, int(enable))

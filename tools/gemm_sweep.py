@@ -16,6 +16,8 @@ p.add_argument("--promos", default="1,2,4,8,1024")
 p.add_argument("--terms", default="3,1")
 p.add_argument("--reps", type=int, default=10)
 p.add_argument("--secs", type=float, default=0.6)
+p.add_argument("--wave", default="1")
+p.add_argument("--sched", default="0:0:0", help="comma list of group_m:polA:polB")
 a = p.parse_args()
 
 import threading  # noqa: E402
@@ -57,8 +59,11 @@ for n in [int(x) for x in a.sizes.split(",")]:
     del A, B
     C = torch.empty((n, n), device="cuda")
     for terms in [int(x) for x in a.terms.split(",")]:
-        for pr in [int(x) for x in a.promos.split(",")]:
+        for pr, wv, sc in [(int(x), int(w), c) for x in a.promos.split(",") for w in a.wave.split(",")
+                           for c in a.sched.split(",")]:
             h.set_promotion(pr)
+            h.set_wave_sync(bool(wv))
+            h.set_schedule(*[int(v) for v in sc.split(":")])
             for _ in range(2):
                 h.gemm_planes(n, n, n, A1, A2, sA, B1, B2, sB, out=C, four_term=terms == 4, one_term=terms == 1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -76,7 +81,7 @@ for n in [int(x) for x in a.sizes.split(",")]:
             ms = e0.elapsed_time(e1) / reps
             tf = terms * 2.0 * n ** 3 / (ms / 1e3) / 1e12
             mhz = float(sorted(ck.v)[len(ck.v) // 2]) if ck.v else float("nan")
-            r = {"n": n, "terms": terms, "promo": pr, "ms": round(ms, 3), "fp16_tflops": round(tf, 1),
+            r = {"n": n, "terms": terms, "promo": pr, "wave": wv, "sched": sc, "ms": round(ms, 3), "fp16_tflops": round(tf, 1),
                  "eff_tflops": round(2.0 * n ** 3 / (ms / 1e3) / 1e12, 1), "sm_mhz": mhz,
                  "watts": round(max(ck.p), 0) if ck.p else None,
                  "per_clock_eff": round(tf * 1e12 / (148 * 8192 * mhz * 1e6), 3)}
