@@ -192,6 +192,7 @@ def workload_config(args, world):
     return {"workload": f"square N={args.n} FP32 uniform[-1,1], {name} split-FP16 GEMM"
                         + (f", 2-D tiles {pr}x{pc}" if world > 1 else ""),
             "M": args.n * pr, "N": args.n * pc, "K": args.n, "terms": args.terms,
+            "inputs": "fp32", "tensor_core": "fp16 x fp16 -> fp32 accumulate (tcgen05 kind::f16)",
             "parallelism": f"2d-tile {pr}x{pc}" if world > 1 else "single",
             "l2": "inputs 1 GiB/matrix > 126 MB L2: no flush needed"}
 
@@ -293,7 +294,7 @@ def main():
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get(str(n), {}).get(str(args.terms))
+                traffic = json.load(f)["bytes_per_launch"].get(str(n), {}).get(str(args.terms))
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "kernel": "gemm3_kernel", "achieved": achieved,
@@ -342,8 +343,7 @@ def main():
             "metric": "split-FP16 SGEMM effective TFLOPS (2MNK/t)",
             "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f16x3->f32" if args.terms == 3 else
-            ("f16x4->f32" if args.terms == 4 else "f16->f32"),
+            "scaling": "weak", "vs_baseline": None, "dtype": "f16",
             "data": "synthetic", "config": workload_config(args, world),
             "frac_of_peak_over_3": value / world / (pk["tc_burst"] / n_prod),
             "gpu_launches": launches_per_step * args.steps,

@@ -34,7 +34,7 @@ def launches(csv_path, out_path):
         name = r["Kernel Name"].split("(")[0]
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "")
-        ms = v / 1e6 if unit == "nsecond" else (v / 1e3 if unit == "usecond" else v)
+        ms = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}.get(unit, 1.0) * v
         per[name][0] += 1
         per[name][1] += ms
     tot = sum(v[1] for v in per.values())
