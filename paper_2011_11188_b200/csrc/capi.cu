@@ -24,6 +24,10 @@ struct split3_ctx {
     int wave_sync = 1;  // GEMM wave lockstep hint (L2 locality)
     split3::GemmTuneIn tune;
     unsigned* d_counters = nullptr;   // 256 B of device scratch owned by the handle
+    // host-buffer entry: copy-in / copy-out streams and events, created on first use
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_done = nullptr;
+    cudaEvent_t ev_rows[8] = {};
     // measurement hooks: event triples (start, after split, after gemm) per timed call
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -158,6 +162,12 @@ int split3_sgemm_destroy(split3_handle_t h) {
     if (h) {
         for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
         if (h->d_counters) cudaFree(h->d_counters);
+        if (h->s_in) cudaStreamDestroy(h->s_in);
+        if (h->s_out) cudaStreamDestroy(h->s_out);
+        for (cudaEvent_t e : {h->ev_a, h->ev_b, h->ev_done})
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : h->ev_rows)
+            if (e) cudaEventDestroy(e);
     }
     delete h;
     return SPLIT3_OK;
@@ -378,6 +388,8 @@ size_t split3_sgemm_host_workspace_size(int64_t M, int64_t N, int64_t K, uint32_
 int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const float* A_host,
                       const float* B_host, float* C_host, uint32_t flags) {
     if (!h || M < 0 || N < 0 || K < 0) return SPLIT3_ERR_INVALID_VALUE;
+    if (flags & ~SPLIT3_FLAGS_MASK) return SPLIT3_ERR_INVALID_VALUE;
+    if ((flags & SPLIT3_ONE_TERM) && (flags & SPLIT3_FOUR_TERM)) return SPLIT3_ERR_INVALID_VALUE;
     if (M == 0 || N == 0) return SPLIT3_OK;
     if (!C_host || (K > 0 && (!A_host || !B_host))) return SPLIT3_ERR_INVALID_VALUE;
     if (!h->ws || h->ws_bytes < split3_sgemm_host_workspace_size(M, N, K, flags))
@@ -387,16 +399,75 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
     float* dA = reinterpret_cast<float*>(base);
     float* dB = reinterpret_cast<float*>(base + align256((size_t)M * K * 4));
     float* dC = reinterpret_cast<float*>(base + align256((size_t)M * K * 4) + align256((size_t)K * N * 4));
-    if (K > 0) {
-        if (cudaMemcpyAsync(dA, A_host, (size_t)M * K * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
-            cudaMemcpyAsync(dB, B_host, (size_t)K * N * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess)
+    if (K == 0 || (flags & SPLIT3_CHECK_FINITE)) {   // serial path
+        if (K > 0 &&
+            (cudaMemcpyAsync(dA, A_host, (size_t)M * K * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
+             cudaMemcpyAsync(dB, B_host, (size_t)K * N * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess))
+            return SPLIT3_ERR_CUDA;
+        int st = split3_sgemm(h, M, N, K, dA, K, dB, N, dC, N, flags);
+        if (st != SPLIT3_OK) return st;
+        if (cudaMemcpyAsync(C_host, dC, (size_t)M * N * 4, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
+            cudaStreamSynchronize(h->stream) != cudaSuccess)
+            return SPLIT3_ERR_CUDA;
+        return SPLIT3_OK;
+    }
+    // Pipelined path.  The per-matrix scale needs all of A (B) on the device before its split,
+    // so the overlap available is: split of A under the copy of B, and the copy-out of C row
+    // blocks under the GEMM of the following row blocks (copy engines run both directions).
+    if (!h->s_in) {
+        if (cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming) != cudaSuccess)
+            return SPLIT3_ERR_CUDA;
+        for (cudaEvent_t& e : h->ev_rows)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return SPLIT3_ERR_CUDA;
+    }
+    cudaStream_t s0 = h->stream;
+    // copy-in must not overwrite the staging buffers while an earlier call on s0 still reads them
+    if (cudaEventRecord(h->ev_done, s0) != cudaSuccess || cudaStreamWaitEvent(h->s_in, h->ev_done, 0) != cudaSuccess)
+        return SPLIT3_ERR_CUDA;
+    if (cudaMemcpyAsync(dA, A_host, (size_t)M * K * 4, cudaMemcpyHostToDevice, h->s_in) != cudaSuccess ||
+        cudaEventRecord(h->ev_a, h->s_in) != cudaSuccess ||
+        cudaMemcpyAsync(dB, B_host, (size_t)K * N * 4, cudaMemcpyHostToDevice, h->s_in) != cudaSuccess ||
+        cudaEventRecord(h->ev_b, h->s_in) != cudaSuccess)
+        return SPLIT3_ERR_CUDA;
+    Carve w = carve(h->ws, M, N, K);
+    int launches = 0, n;
+    if (cudaMemsetAsync(h->ws, 0, 32, s0) != cudaSuccess || cudaStreamWaitEvent(s0, h->ev_a, 0) != cudaSuccess)
+        return SPLIT3_ERR_CUDA;
+    if ((n = split3::launch_maxabs(s0, M, K, dA, K, w.maxA, nullptr, h->num_sms)) < 0) return SPLIT3_ERR_CUDA;
+    launches += n;
+    if ((n = split3::launch_split(s0, M, K, dA, K, w.maxA, w.A1, w.A2, w.ldpa, w.sA, h->num_sms)) < 0)
+        return SPLIT3_ERR_CUDA;
+    launches += n;
+    if (cudaStreamWaitEvent(s0, h->ev_b, 0) != cudaSuccess) return SPLIT3_ERR_CUDA;
+    if ((n = split3::launch_maxabs(s0, K, N, dB, N, w.maxB, nullptr, h->num_sms)) < 0) return SPLIT3_ERR_CUDA;
+    launches += n;
+    if ((n = split3::launch_split_t(s0, K, N, dB, N, w.maxB, w.B1t, w.B2t, w.ldpb, w.sB, h->num_sms)) < 0)
+        return SPLIT3_ERR_CUDA;
+    launches += n;
+    // GEMM in row blocks (multiples of the 256-row pair tile); copy each block out as it completes
+    int nblk = M >= 8 * 1024 ? 4 : (M >= 2048 ? 2 : 1);
+    int64_t rows_per = ((M + nblk - 1) / nblk + 255) / 256 * 256;
+    for (int b = 0; b < nblk; b++) {
+        const int64_t r0 = b * rows_per;
+        if (r0 >= M) break;
+        const int64_t mr = (M - r0 < rows_per) ? M - r0 : rows_per;
+        int err = 0;
+        n = split3::launch_gemm3(s0, mr, N, K, w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa, w.ldpa, w.sA, w.B1t, w.B2t,
+                                 w.ldpb, w.sB, dC + r0 * N, N, terms_of(flags), h->num_sms, h->promo_kb,
+                                 h->wave_sync ? h->d_counters : nullptr, h->tune, &err);
+        if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
+        launches += n;
+        if (cudaEventRecord(h->ev_rows[b], s0) != cudaSuccess || cudaStreamWaitEvent(h->s_out, h->ev_rows[b], 0) != cudaSuccess ||
+            cudaMemcpyAsync(C_host + r0 * N, dC + r0 * N, (size_t)mr * N * 4, cudaMemcpyDeviceToHost, h->s_out) != cudaSuccess)
             return SPLIT3_ERR_CUDA;
     }
-    int st = split3_sgemm(h, M, N, K, dA, K, dB, N, dC, N, flags);
-    if (st != SPLIT3_OK) return st;
-    if (cudaMemcpyAsync(C_host, dC, (size_t)M * N * 4, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
-        cudaStreamSynchronize(h->stream) != cudaSuccess)
+    if (cudaStreamSynchronize(h->s_out) != cudaSuccess || cudaStreamSynchronize(s0) != cudaSuccess)
         return SPLIT3_ERR_CUDA;
+    h->last_launches = launches;
     return SPLIT3_OK;
 }
 

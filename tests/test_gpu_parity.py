@@ -382,3 +382,18 @@ def test_repeatable_bitwise(h):
     c1 = h.sgemm(A, B).clone()
     c2 = h.sgemm(A, B)
     assert torch.equal(c1.view(torch.int32), c2.view(torch.int32))
+
+
+@pytest.mark.parametrize("M", [2048 + 77, 9000])
+def test_host_pipeline_bitwise_equals_device(h, M):
+    """split3_sgemm_host (copy streams, row-block GEMMs, overlapped copy-out) == split3_sgemm."""
+    N, K = 1000, 700
+    A = torch_matrix("uniform", M, K, seed=M, device="cuda")
+    B = torch_matrix("loguni", K, N, seed=M + 1, device="cuda")
+    ref = h.sgemm(A, B).cpu()
+    Ah = A.cpu().pin_memory()
+    Bh = B.cpu().pin_memory()
+    Ch = torch.empty((M, N), dtype=torch.float32).pin_memory()
+    for flags in (0, 0):   # twice: reuse of the handle's streams/events
+        h.sgemm_host_ptr(M, N, K, Ah.data_ptr(), Bh.data_ptr(), Ch.data_ptr(), flags)
+        assert torch.equal(Ch.view(torch.int32), ref.view(torch.int32))
