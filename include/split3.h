@@ -65,8 +65,10 @@ int split3_set_stream(split3_handle_t h, void *cuda_stream);
 /* Destroy the handle (does not free caller-owned workspace).  NULL is a no-op. */
 int split3_sgemm_destroy(split3_handle_t h);
 
-/* Bytes of device workspace split3_sgemm needs for (M, N, K): the four FP16 planes with
- * padded leading dimensions (a multiple of 8 elements) plus 256 bytes of scalars. */
+/* Bytes of device workspace split3_sgemm / split3_sgemm_ex need for (M, N, K): 256 bytes of
+ * scalars, the four FP16 planes with padded leading dimensions (a multiple of 8 elements) and,
+ * when the problem has fewer 256-wide C tiles than CTA pairs, S*M*N floats of split-K partials
+ * (S <= 16 slices of K, reduced in a fixed order: results are deterministic). */
 size_t split3_sgemm_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags);
 
 /* Attach caller-owned device workspace (256-byte aligned).  The handle keeps the pointer;
@@ -100,6 +102,39 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K,
 int64_t split3_last_bad_index(split3_handle_t h);
 
 const char *split3_status_string(int status);
+
+/* ---- operand descriptors: transposes and pre-split reuse --------------- */
+
+/* One GEMM operand.  op(X) = X (trans = 0) or X^T (trans = 1), with X row-major fp32 in device
+ * memory (`data`, leading dimension `ld` of the STORED matrix) — or, when `hi` is non-NULL, the
+ * operand is given pre-split (planes written by split3_presplit for the same role): `hi`, `lo`
+ * FP16 planes (K-major, ldp elements per row, 16-byte aligned) and its device scale exponent.
+ * Pre-split planes are immutable inputs and may be reused across calls. */
+typedef struct split3_matrix {
+    const float *data;
+    int64_t ld;
+    int trans;
+    const uint16_t *hi;
+    const uint16_t *lo;
+    int64_t ldp;
+    const int32_t *d_sexp;
+} split3_matrix;
+
+/* C = op(A) * op(B), op(A) M x K, op(B) K x N (PAPER.md:2-24 with the transposes a dense layer's
+ * forward X*W, backward dY*W^T and X^T*dY need).  Operands given as fp32 are max-abs'ed and split
+ * in this call (their planes go to the workspace); pre-split ones are used as they are.  Flags,
+ * K == 0 and error behaviour as split3_sgemm; with SPLIT3_CHECK_FINITE the reported index is the
+ * linear index in the STORED fp32 matrix (A first, then M*K + index in B). */
+int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const split3_matrix *A,
+                    const split3_matrix *B, float *C, int64_t ldc, uint32_t flags);
+
+/* Split an operand once for reuse (a1 + a2 on one matrix, Eq. A_1, scale rule R1).  role 0: op(X)
+ * is an A operand, rows x cols = M x K, planes M x K; role 1: op(X) is a B operand, rows x cols =
+ * K x N, planes N x K (= op(X)^T, K-major).  X stored row-major (rows x cols if trans == 0, else
+ * cols x rows), leading dimension ldx.  ldp >= K, multiple of 8; d_sexp receives the exponent.
+ * Uses a few bytes of handle-owned scratch; asynchronous on the handle's stream. */
+int split3_presplit(split3_handle_t h, int role, int64_t rows, int64_t cols, const float *X, int64_t ldx,
+                    int trans, uint16_t *hi, uint16_t *lo, int64_t ldp, int32_t *d_sexp);
 
 /* ---- lower level: used by the multi-GPU driver and by the tests -------------------------- */
 

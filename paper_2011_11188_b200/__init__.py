@@ -5,8 +5,8 @@ A ~= a1*A1 + a2*A2, B ~= b1*B1 + b2*B2 (a2 = 2^-11 a1), C ~= a1b1 (A1B1 + 2^-11 
 The product path is libsplit3.so (csrc/, include/split3.h); this package is its binding
 (split3.py) and the multi-GPU 2-D tile driver (dist.py).
 """
-from .split3 import (CHECK_FINITE, FOUR_TERM, ONE_TERM, THREE_TERM, Handle, NotFiniteError,
+from .split3 import (CHECK_FINITE, FOUR_TERM, ONE_TERM, THREE_TERM, Handle, NotFiniteError, Planes,
                      Split3Error, handle, load, plane_ld, sgemm)
 
-__all__ = ["sgemm", "handle", "Handle", "load", "plane_ld", "Split3Error", "NotFiniteError",
+__all__ = ["sgemm", "handle", "Handle", "Planes", "load", "plane_ld", "Split3Error", "NotFiniteError",
            "THREE_TERM", "FOUR_TERM", "ONE_TERM", "CHECK_FINITE"]

@@ -95,11 +95,19 @@ Carve carve(void* ws, int64_t M, int64_t N, int64_t K) {
     return c;
 }
 
-size_t ws_size(int64_t M, int64_t N, int64_t K) {
+size_t ws_bytes_for(int64_t M, int64_t N, int64_t K, bool planesA, bool planesB, int terms_for_partials) {
     if (M < 0 || N < 0 || K < 0) return 0;
-    return kScalarBytes + 2 * align256((size_t)M * (size_t)plane_ld(K) * 2) +
-           2 * align256((size_t)N * (size_t)plane_ld(K) * 2);
+    (void)planesA; (void)planesB;   // plane regions are always carved (fixed layout)
+    size_t b = kScalarBytes + 2 * align256((size_t)M * (size_t)plane_ld(K) * 2) +
+               2 * align256((size_t)N * (size_t)plane_ld(K) * 2);
+    if (terms_for_partials) {
+        const int S = split3::gemm3_k_slices(M, N, K, terms_for_partials, 148, 0);
+        if (S > 1) b += align256((size_t)S * M * N * 4);
+    }
+    return b;
 }
+
+size_t ws_size(int64_t M, int64_t N, int64_t K) { return ws_bytes_for(M, N, K, true, true, 3); }
 
 inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
@@ -174,8 +182,7 @@ int split3_sgemm_destroy(split3_handle_t h) {
 }
 
 size_t split3_sgemm_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags) {
-    (void)flags;
-    return ws_size(M, N, K);
+    return ws_bytes_for(M, N, K, true, true, terms_of(flags));
 }
 
 int split3_sgemm_set_workspace(split3_handle_t h, void* dptr, size_t bytes) {
@@ -250,37 +257,69 @@ int split3_gemm_planes(split3_handle_t h, int64_t M, int64_t N, int64_t K, const
     int err = 0;
     int n = split3::launch_gemm3(h->stream, M, N, K, A1, A2, ldpa, d_sA, B1t, B2t, ldpb, d_sB, C,
                                  ldc, terms, h->num_sms, h->promo_kb,
-                                 h->wave_sync ? h->d_counters : nullptr, h->tune, &err);
+                                 h->wave_sync ? h->d_counters : nullptr, h->tune, nullptr, 0, &err);
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
     h->last_launches = n;
     return SPLIT3_OK;
 }
 
-int split3_sgemm(split3_handle_t h, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
-                 const float* B, int64_t ldb, float* C, int64_t ldc, uint32_t flags) {
-    if (!h || M < 0 || N < 0 || K < 0) return SPLIT3_ERR_INVALID_VALUE;
+// op(X) of a split3_matrix is X (trans = 0) or X^T (trans = 1).  The GEMM consumes K-major planes:
+// A as M x K, B as N x K (= op(B)^T).  The split kernel that produces them directly: for A the
+// transposing one iff trans; for B the transposing one iff !trans (B^T planes from row-major B).
+static int split_operand(split3_ctx* h, int role, int64_t opr, int64_t opc, const split3_matrix* X,
+                         float* d_max, uint16_t* hi, uint16_t* lo, int64_t ldp, int32_t* d_sexp, int* launches) {
+    const bool tr = role == 0 ? X->trans != 0 : X->trans == 0;
+    // stored matrix: rows x cols with ld
+    const int64_t rows = X->trans ? opc : opr, cols = X->trans ? opr : opc;
+    int n = tr ? split3::launch_split_t(h->stream, rows, cols, X->data, X->ld, d_max, hi, lo, ldp, d_sexp, h->num_sms)
+               : split3::launch_split(h->stream, rows, cols, X->data, X->ld, d_max, hi, lo, ldp, d_sexp, h->num_sms);
+    if (n < 0) return SPLIT3_ERR_CUDA;
+    *launches += n;
+    return SPLIT3_OK;
+}
+
+static bool operand_ok(const split3_matrix* X, int64_t opr, int64_t opc, int role, int terms) {
+    if (!X || (X->trans != 0 && X->trans != 1)) return false;
+    if (X->hi) {   // pre-split planes: K-major, rows = M (A) or N (B), K columns
+        const int64_t prow_k = role == 0 ? opc : opr;
+        if (!X->d_sexp || X->ldp < prow_k || X->ldp % 8 || !aligned(X->hi, 16)) return false;
+        if (terms != 1 && (!X->lo || !aligned(X->lo, 16))) return false;
+        return true;
+    }
+    if (!X->data) return false;
+    const int64_t stored_cols = X->trans ? opr : opc;
+    return X->ld >= (stored_cols > 1 ? stored_cols : 1);
+}
+
+int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const split3_matrix* A,
+                    const split3_matrix* B, float* C, int64_t ldc, uint32_t flags) {
+    if (!h || M < 0 || N < 0 || K < 0 || !A || !B) return SPLIT3_ERR_INVALID_VALUE;
     if (flags & ~SPLIT3_FLAGS_MASK) return SPLIT3_ERR_INVALID_VALUE;
     if ((flags & SPLIT3_ONE_TERM) && (flags & SPLIT3_FOUR_TERM)) return SPLIT3_ERR_INVALID_VALUE;
     h->last_launches = 0;
     h->last_bad = -1;
     if (M == 0 || N == 0) return SPLIT3_OK;
     if (!C || ldc < N) return SPLIT3_ERR_INVALID_VALUE;
-    if (K > 0 && (!A || !B || lda < K || ldb < N)) return SPLIT3_ERR_INVALID_VALUE;
+    const int terms = terms_of(flags);
+    if (K > 0 && (!operand_ok(A, M, K, 0, terms) || !operand_ok(B, K, N, 1, terms))) return SPLIT3_ERR_INVALID_VALUE;
+    if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return SPLIT3_ERR_NOT_IMPLEMENTED;
     if (set_dev(h)) return SPLIT3_ERR_CUDA;
     if (K == 0) {   // empty sum: C = 0
         if (cudaMemset2DAsync(C, (size_t)ldc * 4, 0, (size_t)N * 4, (size_t)M, h->stream) != cudaSuccess)
             return SPLIT3_ERR_CUDA;
         return SPLIT3_OK;
     }
-    if (!h->ws || h->ws_bytes < ws_size(M, N, K)) return SPLIT3_ERR_WORKSPACE;
+    if (!h->ws || h->ws_bytes < kScalarBytes) return SPLIT3_ERR_WORKSPACE;
+    const bool needA = A->hi == nullptr, needB = B->hi == nullptr;
+    const size_t need = ws_bytes_for(M, N, K, needA, needB, 0);
+    if (h->ws_bytes < need) return SPLIT3_ERR_WORKSPACE;
     Carve w = carve(h->ws, M, N, K);
     const bool check = (flags & SPLIT3_CHECK_FINITE) != 0;
     // scalars: maxA = maxB = 0.0f, sA = sB = 0, badA = badB = INT64_MAX
     if (cudaMemsetAsync(h->ws, 0, 32, h->stream) != cudaSuccess) return SPLIT3_ERR_CUDA;
     int launches = 0, n;
     if (check) {
-        // INT64_MAX = 0x7FFF...FF: set the 16 bytes of badA/badB to 0xFF then clear the sign bytes
         if (cudaMemsetAsync(w.badA, 0xFF, 16, h->stream) != cudaSuccess ||
             cudaMemsetAsync(reinterpret_cast<uint8_t*>(w.badA) + 7, 0x7F, 1, h->stream) != cudaSuccess ||
             cudaMemsetAsync(reinterpret_cast<uint8_t*>(w.badB) + 7, 0x7F, 1, h->stream) != cudaSuccess)
@@ -292,40 +331,94 @@ int split3_sgemm(split3_handle_t h, int64_t M, int64_t N, int64_t K, const float
         if (!ev0 || !ev1 || !ev2) return SPLIT3_ERR_CUDA;
         record(h, ev0);
     }
-    // a1: per-matrix max-abs (reading R1)
-    n = split3::launch_maxabs(h->stream, M, K, A, lda, w.maxA, check ? w.badA : nullptr, h->num_sms);
-    if (n < 0) return SPLIT3_ERR_CUDA;
-    launches += n;
-    n = split3::launch_maxabs(h->stream, K, N, B, ldb, w.maxB, check ? w.badB : nullptr, h->num_sms);
-    if (n < 0) return SPLIT3_ERR_CUDA;
-    launches += n;
+    // a1: per-matrix max-abs (reading R1) of the fp32 operands (max|op(X)| = max|X|)
+    if (needA) {
+        const int64_t r = A->trans ? K : M, c = A->trans ? M : K;
+        if ((n = split3::launch_maxabs(h->stream, r, c, A->data, A->ld, w.maxA, check ? w.badA : nullptr, h->num_sms)) < 0)
+            return SPLIT3_ERR_CUDA;
+        launches += n;
+    }
+    if (needB) {
+        const int64_t r = B->trans ? N : K, c = B->trans ? K : N;
+        if ((n = split3::launch_maxabs(h->stream, r, c, B->data, B->ld, w.maxB, check ? w.badB : nullptr, h->num_sms)) < 0)
+            return SPLIT3_ERR_CUDA;
+        launches += n;
+    }
     if (check) {
         long long bad[2];
         if (cudaMemcpyAsync(bad, w.badA, 16, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
             cudaStreamSynchronize(h->stream) != cudaSuccess)
             return SPLIT3_ERR_CUDA;
-        if (bad[0] != INT64_MAX || bad[1] != INT64_MAX) {
+        if (bad[0] != INT64_MAX || bad[1] != INT64_MAX) {   // linear index in the STORED matrix
             h->last_bad = bad[0] != INT64_MAX ? bad[0] : M * K + bad[1];
             h->last_launches = launches;
             return SPLIT3_ERR_NOT_FINITE;
         }
     }
-    // a2: split A (planes M x K) and B (planes transposed: N x K)
-    n = split3::launch_split(h->stream, M, K, A, lda, w.maxA, w.A1, w.A2, w.ldpa, w.sA, h->num_sms);
-    if (n < 0) return SPLIT3_ERR_CUDA;
-    launches += n;
-    n = split3::launch_split_t(h->stream, K, N, B, ldb, w.maxB, w.B1t, w.B2t, w.ldpb, w.sB, h->num_sms);
-    if (n < 0) return SPLIT3_ERR_CUDA;
-    launches += n;
+    // a2: split into K-major planes (A: M x K, B: N x K)
+    const uint16_t *A1 = A->hi, *A2 = A->lo, *B1t = B->hi, *B2t = B->lo;
+    const int32_t *sA = A->d_sexp, *sB = B->d_sexp;
+    int64_t ldpa = A->ldp, ldpb = B->ldp;
+    if (needA) {
+        int st = split_operand(h, 0, M, K, A, w.maxA, w.A1, w.A2, w.ldpa, w.sA, &launches);
+        if (st) return st;
+        A1 = w.A1; A2 = w.A2; sA = w.sA; ldpa = w.ldpa;
+    }
+    if (needB) {
+        int st = split_operand(h, 1, K, N, B, w.maxB, w.B1t, w.B2t, w.ldpb, w.sB, &launches);
+        if (st) return st;
+        B1t = w.B1t; B2t = w.B2t; sB = w.sB; ldpb = w.ldpb;
+    }
     record(h, ev1);
-    // a3 + a4: tensor-core products with the fused epilogue
+    // a3 + a4: tensor-core products with the fused epilogue (split-K partials after the planes)
+    // split-K partials: only the region split3_sgemm_workspace_size reserves for them (whatever
+    // follows it in the workspace may be staging buffers of split3_sgemm_host)
+    float* partial = reinterpret_cast<float*>(static_cast<uint8_t*>(h->ws) + w.end);
+    size_t reserved = ws_bytes_for(M, N, K, true, true, terms) - w.end;
+    if (reserved > h->ws_bytes - w.end) reserved = h->ws_bytes - w.end;
+    const int64_t partial_elems = (int64_t)(reserved / 4);
     int err = 0;
-    n = split3::launch_gemm3(h->stream, M, N, K, w.A1, w.A2, w.ldpa, w.sA, w.B1t, w.B2t, w.ldpb, w.sB,
-                             C, ldc, terms_of(flags), h->num_sms, h->promo_kb,
-                             h->wave_sync ? h->d_counters : nullptr, h->tune, &err);
+    n = split3::launch_gemm3(h->stream, M, N, K, A1, A2, ldpa, sA, B1t, B2t, ldpb, sB, C, ldc, terms,
+                             h->num_sms, h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune, partial,
+                             partial_elems, &err);
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
     launches += n;
+    h->last_launches = launches;
+    return SPLIT3_OK;
+}
+
+int split3_sgemm(split3_handle_t h, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                 const float* B, int64_t ldb, float* C, int64_t ldc, uint32_t flags) {
+    if (!h) return SPLIT3_ERR_INVALID_VALUE;
+    if (K > 0 && M > 0 && N > 0 && (!A || !B)) return SPLIT3_ERR_INVALID_VALUE;
+    split3_matrix a = {A, lda, 0, nullptr, nullptr, 0, nullptr};
+    split3_matrix b = {B, ldb, 0, nullptr, nullptr, 0, nullptr};
+    return split3_sgemm_ex(h, M, N, K, &a, &b, C, ldc, flags);
+}
+
+int split3_presplit(split3_handle_t h, int role, int64_t rows, int64_t cols, const float* X, int64_t ldx,
+                    int trans, uint16_t* hi, uint16_t* lo, int64_t ldp, int32_t* d_sexp) {
+    if (!h || (role != 0 && role != 1) || (trans != 0 && trans != 1) || rows < 0 || cols < 0)
+        return SPLIT3_ERR_INVALID_VALUE;
+    if (rows == 0 || cols == 0) return SPLIT3_OK;
+    const int64_t prow = role == 0 ? rows : cols, pk = role == 0 ? cols : rows;   // planes prow x pk
+    const int64_t stored_cols = trans ? rows : cols;
+    if (!X || !hi || !lo || !d_sexp || ldx < stored_cols || ldp < pk || ldp % 8 || !aligned(hi, 16) ||
+        !aligned(lo, 16))
+        return SPLIT3_ERR_INVALID_VALUE;
+    (void)prow;
+    if (set_dev(h)) return SPLIT3_ERR_CUDA;
+    float* d_max = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(h->d_counters) + 64);
+    if (cudaMemsetAsync(d_max, 0, 4, h->stream) != cudaSuccess) return SPLIT3_ERR_CUDA;
+    int launches = 0;
+    const int64_t sr = trans ? cols : rows, sc = trans ? rows : cols;
+    int n = split3::launch_maxabs(h->stream, sr, sc, X, ldx, d_max, nullptr, h->num_sms);
+    if (n < 0) return SPLIT3_ERR_CUDA;
+    launches += n;
+    split3_matrix m = {X, ldx, trans, nullptr, nullptr, 0, nullptr};
+    int st = split_operand(h, role, rows, cols, &m, d_max, hi, lo, ldp, d_sexp, &launches);
+    if (st) return st;
     h->last_launches = launches;
     return SPLIT3_OK;
 }
@@ -458,7 +551,7 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
         int err = 0;
         n = split3::launch_gemm3(s0, mr, N, K, w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa, w.ldpa, w.sA, w.B1t, w.B2t,
                                  w.ldpb, w.sB, dC + r0 * N, N, terms_of(flags), h->num_sms, h->promo_kb,
-                                 h->wave_sync ? h->d_counters : nullptr, h->tune, &err);
+                                 h->wave_sync ? h->d_counters : nullptr, h->tune, nullptr, 0, &err);
         if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
         launches += n;
         if (cudaEventRecord(h->ev_rows[b], s0) != cudaSuccess || cudaStreamWaitEvent(h->s_out, h->ev_rows[b], 0) != cudaSuccess ||

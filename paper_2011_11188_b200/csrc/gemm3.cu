@@ -235,7 +235,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
              const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
              int M, int N, int K, int promo_kb, const int32_t* __restrict__ d_sA,
              const int32_t* __restrict__ d_sB, float* __restrict__ C, int64_t ldc,
-             unsigned* __restrict__ wave_counter, const GemmTune tune) {
+             unsigned* __restrict__ wave_counter, const GemmTune tune, int k_slices,
+             float* __restrict__ partial) {
     using G = Geo<BN_>;
     constexpr int STAGES = G::STAGES;
     constexpr int STAGE_BYTES = G::STAGE_BYTES;
@@ -272,6 +273,10 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     const int64_t num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + BN_ - 1) / BN_;
     const int64_t num_tiles = num_m * num_n;
     const int num_kb = (K + BK - 1) / BK;
+    // work unit u = slice * num_tiles + tile; slice s covers k-blocks [s*kps, min((s+1)*kps, num_kb))
+    // (split-K for problems with fewer tiles than CTA pairs; the host guarantees non-empty slices)
+    const int kps = (num_kb + k_slices - 1) / k_slices;
+    const int64_t num_units = num_tiles * k_slices;
     const int64_t pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
 
     if (warp == 0 && lane == 0) {
@@ -307,9 +312,12 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         uint32_t phase = 0;
         unsigned wave_target = 0;   // cumulative arrivals expected up to this tile index
         int64_t idx = 0;
-        for (int64_t tile = pair; tile < num_tiles; tile += num_pairs, idx++) {
+        for (int64_t unit = pair; unit < num_units; unit += num_pairs, idx++) {
+            const int64_t tile = unit % num_tiles;
+            const int kb_begin = (int)(unit / num_tiles) * kps;
+            const int kb_end = kb_begin + kps < num_kb ? kb_begin + kps : num_kb;
             if (wave_counter && idx > 0) {
-                int64_t active = num_tiles - idx * num_pairs;   // pairs with an idx-th tile
+                int64_t active = num_units - idx * num_pairs;   // pairs with an idx-th unit
                 if (active > num_pairs) active = num_pairs;
                 wave_target += 2u * (unsigned)active;
                 if (elect_one()) wave_sync(wave_counter, wave_target);
@@ -319,7 +327,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             tile_coords(tile, num_m, num_n, tune.group_m, mb, nb);
             const int32_t y_a = (int32_t)(mb * 2 * BM + crank * BM);
             const int32_t y_b = (int32_t)(nb * BN_ + crank * BNH);
-            for (int kb = 0; kb < num_kb; kb++) {
+            for (int kb = kb_begin; kb < kb_end; kb++) {
                 mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
                 const uint32_t fb = smem_u32(&full_bar[stage]);
                 uint8_t* st = smem + stage * STAGE_BYTES;
@@ -348,13 +356,15 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             uint32_t phase = 0;
             uint32_t cc = 0;       // global D_hi chunk counter
             uint32_t tc = 0;       // tile counter
-            for (int64_t tile = pair; tile < num_tiles; tile += num_pairs, tc++) {
+            for (int64_t unit = pair; unit < num_units; unit += num_pairs, tc++) {
+                const int kb_begin = (int)(unit / num_tiles) * kps;
+                const int kb_end = kb_begin + kps < num_kb ? kb_begin + kps : num_kb;
                 const uint32_t t_mid = tmem_base + COL_MID;
                 const uint32_t t_lo = tmem_base + COL_LO;
                 bool mid_ready = false;
-                for (int kb = 0; kb < num_kb; kb++) {
-                    const bool chunk_start = (kb % promo_kb) == 0;
-                    if (chunk_start && kb > 0) cc++;
+                for (int kb = kb_begin; kb < kb_end; kb++) {
+                    const bool chunk_start = ((kb - kb_begin) % promo_kb) == 0;
+                    if (chunk_start && kb > kb_begin) cc++;
                     const uint32_t hb = HB == 2 ? (cc & 1) : 0;
                     const uint32_t hphase = HB == 2 ? ((cc >> 1) & 1) : (cc & 1);
                     const uint32_t t_hi = tmem_base + hb * BN_;
@@ -365,7 +375,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     const uint64_t a2 = sdesc_sw128(smem_u32(st + TILE_A_BYTES));
                     const uint64_t b1 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES));
                     const uint64_t b2 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES + TILE_B_BYTES));
-                    const bool hi_first = kb == 0;
+                    const bool hi_first = kb == kb_begin;
                     auto issue_mid = [&]() {
                         if (!HAS_MID) return;
                         if (!mid_ready) {
@@ -377,7 +387,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
 #pragma unroll
                             for (int k = 0; k < BK / 16; k++) {
                                 const uint64_t dk = (uint64_t)(2 * k);
-                                const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+                                const uint32_t acc = (kb > kb_begin || k > 0) ? 1u : 0u;
                                 mma_pair(t_mid, a1 + dk, b2 + dk, IDESC, acc);
                                 mma_pair(t_mid, a2 + dk, b1 + dk, IDESC, 1u);
                                 if (TERMS == 4) mma_pair(t_lo, a2 + dk, b2 + dk, IDESC, acc);
@@ -402,9 +412,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     if (hi_first) { issue_hi(); issue_mid(); } else { issue_mid(); issue_hi(); }
                     if (elect_one()) {
                         mma_commit_pair(smem_u32(&empty_bar[stage]));        // stage free in both CTAs
-                        const bool chunk_end = ((kb + 1) % promo_kb) == 0 || kb + 1 == num_kb;
+                        const bool chunk_end = ((kb + 1 - kb_begin) % promo_kb) == 0 || kb + 1 == kb_end;
                         if (chunk_end) mma_commit_pair(smem_u32(&hfull_bar[hb]));   // D_hi chunk ready
-                        if (HAS_MID && kb + 1 == num_kb) mma_commit_pair(smem_u32(&mfull_bar[0]));
+                        if (HAS_MID && kb + 1 == kb_end) mma_commit_pair(smem_u32(&mfull_bar[0]));
                     }
                     __syncwarp();
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -423,13 +433,17 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         const bool vec_ok = (ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(C) & 15u) == 0);
         const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * NCOL);
         uint32_t cc = 0, tc = 0;
-        for (int64_t tile = pair; tile < num_tiles; tile += num_pairs, tc++) {
+        for (int64_t unit = pair; unit < num_units; unit += num_pairs, tc++) {
+            const int64_t tile = unit % num_tiles;
+            const int slice = (int)(unit / num_tiles);
+            const int kb_begin = slice * kps;
+            const int kb_end = kb_begin + kps < num_kb ? kb_begin + kps : num_kb;
             int64_t mb, nb;
             tile_coords(tile, num_m, num_n, tune.group_m, mb, nb);
             float master[NCOL];
 #pragma unroll
             for (int j = 0; j < NCOL; j++) master[j] = 0.0f;
-            for (int kb0 = 0; kb0 < num_kb; kb0 += promo_kb, cc++) {
+            for (int kb0 = kb_begin; kb0 < kb_end; kb0 += promo_kb, cc++) {
                 const uint32_t hb = HB == 2 ? (cc & 1) : 0;
                 const uint32_t hphase = HB == 2 ? ((cc >> 1) & 1) : (cc & 1);
                 mbar_wait(smem_u32(&hfull_bar[hb]), hphase);
@@ -466,6 +480,24 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                 __syncwarp();
                 if (lane == 0) mbar_arrive_leader(smem_u32(&mempty_bar[0]));   // D_mid free early
             }
+            if (k_slices > 1) {                          // split-K: raw partial, reduced later
+                const int64_t row = mb * 2 * BM + crank * BM + quad * 32 + lane;
+                const int64_t col0 = nb * BN_ + half * NCOL;
+                if (row < M) {
+                    float* prow = partial + ((int64_t)slice * M + row) * N + col0;
+                    if ((N % 4) == 0 && col0 + NCOL <= N) {
+#pragma unroll
+                        for (int j = 0; j < NCOL / 4; j++)
+                            reinterpret_cast<float4*>(prow)[j] =
+                                make_float4(master[4 * j], master[4 * j + 1], master[4 * j + 2], master[4 * j + 3]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < NCOL; j++)
+                            if (col0 + j < N) prow[j] = master[j];
+                    }
+                }
+                continue;
+            }
             if (fast) {                                  // warp-uniform branch
 #pragma unroll
                 for (int j = 0; j < NCOL; j++) master[j] = master[j] * fscale;
@@ -499,6 +531,24 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                      "r"(TMEM_COLS)
                      : "memory");
+    }
+}
+
+// Split-K reduction: C = 2^(sA+sB) * sum_{s=0}^{S-1} P[s]  (fixed order -> deterministic).
+__global__ void __launch_bounds__(256) ksplit_reduce_kernel(const float* __restrict__ P, int S, int64_t M,
+                                                            int64_t N, float* __restrict__ C, int64_t ldc,
+                                                            const int32_t* __restrict__ d_sA,
+                                                            const int32_t* __restrict__ d_sB) {
+    const int sAB = *d_sA + *d_sB;
+    const bool fast = sAB >= -126 && sAB <= 127;
+    const float f = fast ? __uint_as_float((unsigned)(sAB + 127) << 23) : 1.0f;
+    const double fd = __longlong_as_double((long long)(sAB + 1023) << 52);
+    const int64_t total = M * N;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        float acc = P[i];
+        for (int s = 1; s < S; s++) acc = __fadd_rn(acc, P[(int64_t)s * total + i]);
+        const int64_t r = i / N, c = i - r * N;
+        C[r * ldc + c] = fast ? acc * f : __double2float_rn(__dmul_rn((double)acc, fd));
     }
 }
 
@@ -539,7 +589,7 @@ template <int TERMS, int BN_>
 int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap& a1,
              const CUtensorMap& a2, const CUtensorMap& b1, const CUtensorMap& b2,
              const int32_t* d_sA, const int32_t* d_sB, float* C, int64_t ldc, int num_sms,
-             int promo_kb, unsigned* wave_counter, const GemmTune& tune) {
+             int promo_kb, unsigned* wave_counter, const GemmTune& tune, int k_slices, float* partial) {
     constexpr int SMEM_BYTES = Geo<BN_>::SMEM;
     static bool attr_set = false;
     if (!attr_set) {
@@ -548,23 +598,40 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
             return -1;
         attr_set = true;
     }
-    const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN_ - 1) / BN_);
+    const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN_ - 1) / BN_) * k_slices;
     const int64_t pairs = num_sms / 2;
     const int grid = 2 * (int)(tiles < pairs ? tiles : pairs);
     if (wave_counter && cudaMemsetAsync(wave_counter, 0, sizeof(unsigned), st) != cudaSuccess) return -1;
     gemm3_kernel<TERMS, BN_><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(a1, a2, b1, b2, (int)M, (int)N, (int)K,
                                                                promo_kb, d_sA, d_sB, C, ldc, wave_counter,
-                                                               tune);
+                                                               tune, k_slices, partial);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 }  // namespace
 
+int gemm3_k_slices(int64_t M, int64_t N, int64_t K, int terms, int num_sms, int promo_kb) {
+    const int bn = terms == 4 ? 128 : 256;
+    const int64_t tiles = ((M + 255) / 256) * ((N + bn - 1) / bn);
+    const int64_t pairs = num_sms / 2;
+    const int64_t num_kb = (K + 63) / 64;
+    if (tiles >= pairs || tiles == 0) return 1;
+    const int promo = promo_kb > 0 ? promo_kb : kDefaultPromoKb;
+    // at least 4 k-blocks (and one promotion chunk) per slice, at most 16 slices
+    int64_t S = pairs / tiles;
+    const int64_t max_by_k = num_kb / (promo > 4 ? promo : 4);
+    if (S > max_by_k) S = max_by_k;
+    if (S > 16) S = 16;
+    if (S < 2) return 1;
+    const int64_t kps = (num_kb + S - 1) / S;
+    return (int)((num_kb + kps - 1) / kps);   // every slice non-empty
+}
+
 int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_t* A1,
                  const uint16_t* A2, int64_t ldpa, const int32_t* d_sA, const uint16_t* B1t,
                  const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB, float* C, int64_t ldc,
                  int terms, int num_sms, int promo_kb, unsigned* wave_counter, const GemmTuneIn& tin,
-                 int* err) {
+                 float* partial, int64_t partial_elems, int* err) {
     CUtensorMap ma1, ma2, mb1, mb2;
     const uint16_t* A2e = terms == 1 ? A1 : A2;
     const uint16_t* B2e = terms == 1 ? B1t : B2t;
@@ -580,11 +647,23 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     auto pol = [](int p) { return p == 1 ? kPolicyFirst : (p == 2 ? kPolicyLast : kPolicyNormal); };
     tune.pol_a = pol(tin.pol_a);
     tune.pol_b = pol(tin.pol_b);
+    int S = partial ? gemm3_k_slices(M, N, K, terms, num_sms, promo) : 1;
+    if (S > 1 && (int64_t)S * M * N > partial_elems) S = 1;
     int r;
-    if (terms == 1) r = launch_t<1, 256>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune);
-    else if (terms == 4) r = launch_t<4, 128>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune);
-    else r = launch_t<3, 256>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune);
-    if (r < 0) *err = 4;
+    if (terms == 1)
+        r = launch_t<1, 256>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, S, partial);
+    else if (terms == 4)
+        r = launch_t<4, 128>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, S, partial);
+    else
+        r = launch_t<3, 256>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, S, partial);
+    if (r < 0) { *err = 4; return -1; }
+    if (S > 1) {
+        int64_t blocks = (M * N + 255) / 256;
+        if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+        ksplit_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(partial, S, M, N, C, ldc, d_sA, d_sB);
+        if (cudaPeekAtLastError() != cudaSuccess) { *err = 4; return -1; }
+        r += 1;
+    }
     return r;
 }
 

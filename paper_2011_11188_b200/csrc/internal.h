@@ -36,11 +36,17 @@ struct GemmTune {
     uint64_t pol_a, pol_b;
 };
 
-// terms: 1, 3 or 4.  Returns kernels launched (1) or -1 on error (*err set to a status).
+// Number of K slices the GEMM uses for (M, N, K) (split-K when there are fewer tile pairs than
+// CTA pairs); the partial buffer needs slices * M * N floats.
+int gemm3_k_slices(int64_t M, int64_t N, int64_t K, int terms, int num_sms, int promo_kb);
+
+// terms: 1, 3 or 4.  `partial` (may be NULL: no split-K) holds partial_elems floats.
+// Returns kernels launched (1, or 2 with the split-K reduction) or -1 (*err set to a status).
 int launch_gemm3(cudaStream_t s, int64_t M, int64_t N, int64_t K,
                  const uint16_t* A1, const uint16_t* A2, int64_t ldpa, const int32_t* d_sA,
                  const uint16_t* B1t, const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB,
                  float* C, int64_t ldc, int terms, int num_sms, int promo_kb,
-                 unsigned* wave_counter, const GemmTuneIn& tune, int* err);
+                 unsigned* wave_counter, const GemmTuneIn& tune, float* partial, int64_t partial_elems,
+                 int* err);
 
 }  // namespace split3

@@ -38,7 +38,29 @@ EXPORTS = (
     "split3_status_string", "split3_maxabs", "split3_split", "split3_gemm_planes",
     "split3_last_launch_count", "split3_timing_enable", "split3_timing_read",
     "split3_set_promotion", "split3_set_wave_sync", "split3_set_schedule",
+    "split3_sgemm_ex", "split3_presplit",
 )
+
+class split3_matrix(ctypes.Structure):
+    """ctypes mirror of include/split3.h's split3_matrix."""
+    _fields_ = [("data", ctypes.c_void_p), ("ld", ctypes.c_int64), ("trans", ctypes.c_int),
+                ("hi", ctypes.c_void_p), ("lo", ctypes.c_void_p), ("ldp", ctypes.c_int64),
+                ("d_sexp", ctypes.c_void_p)]
+
+
+class Planes:
+    """A pre-split operand (split3_presplit): FP16 planes (int16 tensors holding binary16 bits,
+    K-major with padded leading dimension) and the device scale exponent.  role 0 = A operand
+    (planes M x K), role 1 = B operand (planes N x K = op(B)^T)."""
+
+    def __init__(self, hi, lo, sexp, role, rows, cols):
+        self.hi, self.lo, self.sexp = hi, lo, sexp
+        self.role, self.rows, self.cols = role, rows, cols   # op(X) is rows x cols
+
+    @property
+    def shape(self):
+        return (self.rows, self.cols)
+
 
 _lib = None
 _lock = threading.Lock()
@@ -86,6 +108,10 @@ def load() -> ctypes.CDLL:
         lib.split3_set_promotion.argtypes = [_p, ctypes.c_int]
         lib.split3_set_wave_sync.argtypes = [_p, ctypes.c_int]
         lib.split3_set_schedule.argtypes = [_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        lib.split3_sgemm_ex.argtypes = [_p, _i64, _i64, _i64, ctypes.POINTER(split3_matrix),
+                                        ctypes.POINTER(split3_matrix), _p, _i64, ctypes.c_uint32]
+        lib.split3_presplit.argtypes = [_p, ctypes.c_int, _i64, _i64, _p, _i64, ctypes.c_int, _p, _p,
+                                        _i64, _p]
         lib.split3_timing_read.argtypes = [_p, ctypes.POINTER(ctypes.c_double),
                                            ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]
         lib.split3_status_string.restype = ctypes.c_char_p
@@ -216,6 +242,54 @@ class Handle:
             raise NotFiniteError(st, "split3_sgemm", int(self._lib.split3_last_bad_index(self._h)))
         if st != OK:
             raise Split3Error(st, "split3_sgemm")
+        return out
+
+    def presplit(self, X: torch.Tensor, role: int, trans: bool = False) -> Planes:
+        """Split op(X) once (role 0: an A operand, role 1: a B operand) for reuse."""
+        _check_mat(X, "X")
+        rows, cols = (X.shape[1], X.shape[0]) if trans else (X.shape[0], X.shape[1])
+        prow, pk = (rows, cols) if role == 0 else (cols, rows)
+        ldp = plane_ld(pk)
+        hi = torch.empty((prow, ldp), dtype=torch.int16, device=X.device)
+        lo = torch.empty((prow, ldp), dtype=torch.int16, device=X.device)
+        sexp = torch.zeros(1, dtype=torch.int32, device=X.device)
+        self._bind_stream()
+        st = self._lib.split3_presplit(self._h, int(role), rows, cols, _ptr(X), _ld(X), int(trans),
+                                       _ptr(hi), _ptr(lo), ldp, _ptr(sexp))
+        if st != OK:
+            raise Split3Error(st, "split3_presplit")
+        return Planes(hi, lo, sexp, role, rows, cols)
+
+    def sgemm_ex(self, A, B, transA: bool = False, transB: bool = False, out=None,
+                 four_term: bool = False, one_term: bool = False, check_finite: bool = False):
+        """C = op(A) @ op(B); A / B are fp32 CUDA tensors or Planes from presplit()."""
+        def desc(X, trans, role, name):
+            if isinstance(X, Planes):
+                if X.role != role:
+                    raise ValueError(f"{name}: planes were split for role {X.role}")
+                return split3_matrix(None, 0, 0, X.hi.data_ptr(), X.lo.data_ptr(), X.hi.stride(0),
+                                     X.sexp.data_ptr()), X.shape
+            _check_mat(X, name)
+            shp = (X.shape[1], X.shape[0]) if trans else tuple(X.shape)
+            return split3_matrix(X.data_ptr(), _ld(X), int(trans), None, None, 0, None), shp
+
+        da, (M, K) = desc(A, transA, 0, "A")
+        db, (K2, N) = desc(B, transB, 1, "B")
+        if K != K2:
+            raise ValueError(f"inner dimensions differ: {K} vs {K2}")
+        dev = A.hi.device if isinstance(A, Planes) else A.device
+        if out is None:
+            out = torch.empty((M, N), dtype=torch.float32, device=dev)
+        _check_mat(out, "C")
+        flags = _flags(four_term, one_term, check_finite)
+        self._ensure_ws(self.workspace_size(M, N, K, flags))
+        self._bind_stream()
+        st = self._lib.split3_sgemm_ex(self._h, M, N, K, ctypes.byref(da), ctypes.byref(db),
+                                       _ptr(out), _ld(out), flags)
+        if st == ERR_NOT_FINITE:
+            raise NotFiniteError(st, "split3_sgemm_ex", int(self._lib.split3_last_bad_index(self._h)))
+        if st != OK:
+            raise Split3Error(st, "split3_sgemm_ex")
         return out
 
     def sgemm_host(self, A, B, out=None, four_term=False, one_term=False):
