@@ -332,13 +332,20 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
         record(h, ev0);
     }
     // a1: per-matrix max-abs (reading R1) of the fp32 operands (max|op(X)| = max|X|)
-    if (needA) {
+    if (needA && needB && !check) {
+        const int64_t ra = A->trans ? K : M, ca = A->trans ? M : K;
+        const int64_t rb = B->trans ? N : K, cb = B->trans ? K : N;
+        if ((n = split3::launch_maxabs2(h->stream, ra, ca, A->data, A->ld, w.maxA, rb, cb, B->data, B->ld, w.maxB,
+                                        h->num_sms)) < 0)
+            return SPLIT3_ERR_CUDA;
+        launches += n;
+    } else if (needA) {
         const int64_t r = A->trans ? K : M, c = A->trans ? M : K;
         if ((n = split3::launch_maxabs(h->stream, r, c, A->data, A->ld, w.maxA, check ? w.badA : nullptr, h->num_sms)) < 0)
             return SPLIT3_ERR_CUDA;
         launches += n;
     }
-    if (needB) {
+    if (needB && !(needA && !check)) {
         const int64_t r = B->trans ? N : K, c = B->trans ? K : N;
         if ((n = split3::launch_maxabs(h->stream, r, c, B->data, B->ld, w.maxB, check ? w.badB : nullptr, h->num_sms)) < 0)
             return SPLIT3_ERR_CUDA;

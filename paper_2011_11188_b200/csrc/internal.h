@@ -13,6 +13,10 @@ inline int64_t plane_ld(int64_t k) { return ((k + 7) / 8) * 8; }
 // Each launcher returns the number of kernels it launched (>= 0) or -1 on a launch error.
 int launch_maxabs(cudaStream_t s, int64_t rows, int64_t cols, const float* X, int64_t ld,
                   float* d_max, long long* d_bad, int num_sms);
+// max-abs of two matrices in one launch (no bad-index tracking); falls back to two launches
+// when either is strided or misaligned.
+int launch_maxabs2(cudaStream_t s, int64_t rows0, int64_t cols0, const float* X0, int64_t ld0, float* d_max0,
+                   int64_t rows1, int64_t cols1, const float* X1, int64_t ld1, float* d_max1, int num_sms);
 int launch_split(cudaStream_t s, int64_t rows, int64_t cols, const float* X, int64_t ld,
                  const float* d_max, uint16_t* hi, uint16_t* lo, int64_t ldp, int32_t* d_sexp,
                  int num_sms);

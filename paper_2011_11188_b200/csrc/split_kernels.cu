@@ -88,6 +88,41 @@ __global__ void __launch_bounds__(256) maxabs_1d_kernel(const float* __restrict_
     block_fold(m, bad, d_max, d_bad);
 }
 
+// Two contiguous matrices in one launch: blocks [0, gx) reduce X0 into d_max0, the rest X1.
+__global__ void __launch_bounds__(256) maxabs2_1d_kernel(const float* __restrict__ X0, int64_t n0, float* d_max0,
+                                                         const float* __restrict__ X1, int64_t n1, float* d_max1,
+                                                         int gx) {
+    const bool first = (int)blockIdx.x < gx;
+    const float* X = first ? X0 : X1;
+    const int64_t n = first ? n0 : n1;
+    float* d_max = first ? d_max0 : d_max1;
+    const int64_t b = first ? blockIdx.x : blockIdx.x - gx;
+    const int64_t nb = first ? gx : gridDim.x - gx;
+    unsigned m = 0;
+    long long bad = LLONG_MAX;
+    const int64_t tid = b * blockDim.x + threadIdx.x;
+    const int64_t nthr = nb * blockDim.x;
+    const int64_t n4 = n / 4;
+    const float4* X4 = reinterpret_cast<const float4*>(X);
+    int64_t i = tid;
+    for (; i + 3 * nthr < n4; i += 4 * nthr) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) v[u] = __ldcs(X4 + i + u * nthr);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            fold1(v[u].x, 0, m, bad); fold1(v[u].y, 0, m, bad);
+            fold1(v[u].z, 0, m, bad); fold1(v[u].w, 0, m, bad);
+        }
+    }
+    for (; i < n4; i += nthr) {
+        float4 v = __ldcs(X4 + i);
+        fold1(v.x, 0, m, bad); fold1(v.y, 0, m, bad); fold1(v.z, 0, m, bad); fold1(v.w, 0, m, bad);
+    }
+    for (int64_t j = n4 * 4 + tid; j < n; j += nthr) fold1(__ldcs(X + j), 0, m, bad);
+    block_fold(m, LLONG_MAX, d_max, nullptr);
+}
+
 // Strided matrix: grid-stride over rows, threads over columns.
 __global__ void __launch_bounds__(256) maxabs_2d_kernel(const float* __restrict__ X, int64_t rows,
                                                         int64_t cols, int64_t ld, float* d_max,
@@ -135,19 +170,32 @@ __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ X,
     const float f = pow2_neg(s);
     if (d_sexp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *d_sexp = s;
     if (VEC) {
+        // U rows per iteration: U independent 16-B loads in flight per thread before any store
+        constexpr int U = 4;
         const int64_t c4n = cols / 4;
-        for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
-            const float4* xr = reinterpret_cast<const float4*>(X + r * ld);
-            uint2* h1r = reinterpret_cast<uint2*>(hi + r * ldp);
-            uint2* h2r = reinterpret_cast<uint2*>(lo + r * ldp);
+        const int64_t gy = gridDim.y;
+        for (int64_t r0 = blockIdx.y; r0 < rows; r0 += U * gy) {
             for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < c4n;
                  c += (int64_t)gridDim.x * blockDim.x) {
-                float4 v = __ldcs(xr + c);
-                unsigned short a[4], b[4];
-                split1(v.x, f, a[0], b[0]); split1(v.y, f, a[1], b[1]);
-                split1(v.z, f, a[2], b[2]); split1(v.w, f, a[3], b[3]);
-                h1r[c] = make_uint2(a[0] | ((unsigned)a[1] << 16), a[2] | ((unsigned)a[3] << 16));
-                h2r[c] = make_uint2(b[0] | ((unsigned)b[1] << 16), b[2] | ((unsigned)b[3] << 16));
+                float4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int64_t r = r0 + u * gy;
+                    if (r < rows) v[u] = __ldcs(reinterpret_cast<const float4*>(X + r * ld) + c);
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int64_t r = r0 + u * gy;
+                    if (r < rows) {
+                        unsigned short a[4], b[4];
+                        split1(v[u].x, f, a[0], b[0]); split1(v[u].y, f, a[1], b[1]);
+                        split1(v[u].z, f, a[2], b[2]); split1(v[u].w, f, a[3], b[3]);
+                        __stcs(reinterpret_cast<uint2*>(hi + r * ldp) + c,
+                               make_uint2(a[0] | ((unsigned)a[1] << 16), a[2] | ((unsigned)a[3] << 16)));
+                        __stcs(reinterpret_cast<uint2*>(lo + r * ldp) + c,
+                               make_uint2(b[0] | ((unsigned)b[1] << 16), b[2] | ((unsigned)b[3] << 16)));
+                    }
+                }
             }
         }
     } else {
@@ -182,35 +230,46 @@ __global__ void __launch_bounds__(256) split_t_kernel(const float* __restrict__ 
     if (d_sexp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *d_sexp = s;
     const int t = threadIdx.x;
     const int64_t ntr = (rows + TT - 1) / TT, ntc = (cols + TT - 1) / TT;
-    for (int64_t tile = blockIdx.x; tile < ntr * ntc; tile += gridDim.x) {
-        const int64_t r0 = (tile % ntr) * TT;   // consecutive blocks walk down X's rows (K)
-        const int64_t c0 = (tile / ntr) * TT;
-        // load + split: thread t covers X rows r0 + t/16 + 16 i, columns c0 + 4 (t%16) .. +3
+    const int64_t ntiles = ntr * ntc;
+    // thread t covers X rows r0 + t/16 + 16 i (i < 4), columns c0 + 4 (t%16) .. +3
+    const int cc = 4 * (t % 16);
+    float v[4][4];
+    auto load_tile = [&](int64_t tile) {
+        const int64_t r0 = (tile % ntr) * TT, c0 = (tile / ntr) * TT;
 #pragma unroll
         for (int i = 0; i < 4; i++) {
-            const int rr = t / 16 + 16 * i;
-            const int cc = 4 * (t % 16);
-            const int64_t r = r0 + rr, c = c0 + cc;
-            float v[4] = {0.f, 0.f, 0.f, 0.f};
+            const int64_t r = r0 + t / 16 + 16 * i, c = c0 + cc;
+            v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0.f;
             if (r < rows) {
                 if (VEC && c + 3 < cols) {
                     float4 q = __ldcs(reinterpret_cast<const float4*>(X + r * ld + c));
-                    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+                    v[i][0] = q.x; v[i][1] = q.y; v[i][2] = q.z; v[i][3] = q.w;
                 } else {
 #pragma unroll
                     for (int j = 0; j < 4; j++)
-                        if (c + j < cols) v[j] = X[r * ld + c + j];
+                        if (c + j < cols) v[i][j] = X[r * ld + c + j];
                 }
             }
+        }
+    };
+    int64_t tile = blockIdx.x;
+    if (tile < ntiles) load_tile(tile);
+    for (; tile < ntiles; tile += gridDim.x) {
+        const int64_t r0 = (tile % ntr) * TT;   // consecutive blocks walk down X's rows (K)
+        const int64_t c0 = (tile / ntr) * TT;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int rr = t / 16 + 16 * i;
 #pragma unroll
             for (int j = 0; j < 4; j++) {
                 unsigned short a, b;
-                split1(v[j], f, a, b);
+                split1(v[i][j], f, a, b);
                 s1[cc + j][rr] = a;
                 s2[cc + j][rr] = b;
             }
         }
         __syncthreads();
+        if (tile + gridDim.x < ntiles) load_tile(tile + gridDim.x);   // in flight during the stores
         // store: plane row n = c0 + t/4 gets K entries r0 + 16 (t%4) .. +15 (two 16-B chunks)
         {
             const int nn = t / 4, kk = 16 * (t % 4);
@@ -224,8 +283,8 @@ __global__ void __launch_bounds__(256) split_t_kernel(const float* __restrict__ 
                     if (k < ldp) {   // chunk lies inside the padded row (ldp % 8 == 0)
                         uint4 w1 = make_uint4(p1[4 * h], p1[4 * h + 1], p1[4 * h + 2], p1[4 * h + 3]);
                         uint4 w2 = make_uint4(p2[4 * h], p2[4 * h + 1], p2[4 * h + 2], p2[4 * h + 3]);
-                        *reinterpret_cast<uint4*>(hi + n * ldp + k) = w1;
-                        *reinterpret_cast<uint4*>(lo + n * ldp + k) = w2;
+                        __stcs(reinterpret_cast<uint4*>(hi + n * ldp + k), w1);
+                        __stcs(reinterpret_cast<uint4*>(lo + n * ldp + k), w2);
                     }
                 }
             }
@@ -262,6 +321,29 @@ int launch_maxabs(cudaStream_t st, int64_t rows, int64_t cols, const float* X, i
         dim3 grid((unsigned)bx, (unsigned)grid_rows(rows, num_sms, bx));
         maxabs_2d_kernel<<<grid, 256, 0, st>>>(X, rows, cols, ld, d_max, d_bad);
     }
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_maxabs2(cudaStream_t st, int64_t rows0, int64_t cols0, const float* X0, int64_t ld0, float* d_max0,
+                   int64_t rows1, int64_t cols1, const float* X1, int64_t ld1, float* d_max1, int num_sms) {
+    const bool ok = ld0 == cols0 && ld1 == cols1 && aligned16(X0) && aligned16(X1) && rows0 > 0 && cols0 > 0 &&
+                    rows1 > 0 && cols1 > 0;
+    if (!ok) {
+        int a = launch_maxabs(st, rows0, cols0, X0, ld0, d_max0, nullptr, num_sms);
+        if (a < 0) return -1;
+        int b = launch_maxabs(st, rows1, cols1, X1, ld1, d_max1, nullptr, num_sms);
+        return b < 0 ? -1 : a + b;
+    }
+    const int64_t n0 = rows0 * cols0, n1 = rows1 * cols1;
+    const int64_t total_blocks = (int64_t)num_sms * 8;
+    int64_t g0 = (int64_t)((double)total_blocks * (double)n0 / (double)(n0 + n1));
+    int64_t need0 = (n0 / 4 + 255) / 256, need1 = (n1 / 4 + 255) / 256;
+    if (g0 > need0) g0 = need0;
+    if (g0 < 1) g0 = 1;
+    int64_t g1 = total_blocks - g0;
+    if (g1 > need1) g1 = need1;
+    if (g1 < 1) g1 = 1;
+    maxabs2_1d_kernel<<<(unsigned)(g0 + g1), 256, 0, st>>>(X0, n0, d_max0, X1, n1, d_max1, (int)g0);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
