@@ -119,3 +119,37 @@ def test_ex_check_finite_index_in_stored_matrix(h):
     with pytest.raises(s3.NotFiniteError) as ei:
         h.sgemm_ex(A, torch.ones((20, 5), device="cuda"), transA=True, check_finite=True)
     assert ei.value.index == 4 * 30 + 7
+
+
+@pytest.mark.parametrize("M,N,K,kw", [(300, 200, 500, {}), (257, 1030, 129, {"four_term": True}),
+                                      (256, 8192, 4096, {}), (700, 900, 1500, {"transA": True}),
+                                      (1, 1, 1, {}), (2048, 2560, 128, {"one_term": True})])
+def test_canaries_around_output_and_workspace(h, M, N, K, kw):
+    """No write outside C (rows/cols around a strided view) or past the declared workspace size
+    (compute-sanitizer is not available on this pool: guard regions instead)."""
+    import ctypes
+
+    import paper_2011_11188_b200.split3 as s3
+
+    transA = kw.pop("transA", False)
+    A = torch_matrix("uniform", K if transA else M, M if transA else K, seed=3, device="cuda")
+    B = torch_matrix("loguni", K, N, seed=4, device="cuda")
+    big = torch.full((M + 16, N + 12), 12345.0, device="cuda")
+    C = big[8:8 + M, 4:4 + N]
+    flags = (s3.FOUR_TERM if kw.get("four_term") else 0) | (s3.ONE_TERM if kw.get("one_term") else 0)
+    need = h.workspace_size(M, N, K, flags)
+    ws = torch.full((need + 4096,), 0x5A, dtype=torch.uint8, device="cuda")
+    st = h._lib.split3_sgemm_set_workspace(h._h, ctypes.c_void_p(ws.data_ptr()), need)
+    assert st == 0
+    h._ws = ws      # keep alive; the binding will not shrink it
+    try:
+        h.sgemm_ex(A, B, transA=transA, out=C, **kw)
+        torch.cuda.synchronize()
+        assert torch.all(ws[need:] == 0x5A)
+        outside = big.clone()
+        outside[8:8 + M, 4:4 + N] = 12345.0          # everything but C must still be the canary
+        assert torch.all(outside == 12345.0)
+        assert torch.isfinite(C).all()
+    finally:
+        h._ws = None
+        h._ensure_ws(256)
