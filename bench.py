@@ -57,18 +57,36 @@ def peaks():
 
 # ----------------------------------------------------------------- clocks -----
 class ClockSampler:
-    """nvidia-smi sampling DURING the timed region (the profiling recipe's clocks line)."""
+    """SM clock / power / throttle reasons sampled DURING the timed region (10 ms, NVML in-process;
+    nvidia-smi -lms 100 as a fallback) — the profiling recipe's clocks line."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event-reason bits
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.proc = None
         self.lines = []
+        self.nv = None
+        self.samples = []
+        self.stop_flag = False
 
     def start(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            self.pynvml = pynvml
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nv = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
@@ -79,13 +97,36 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        nv, p = self.nv, self.pynvml
+        while not self.stop_flag:
+            try:
+                sm = p.nvmlDeviceGetClockInfo(nv, p.NVML_CLOCK_SM)
+                mx = p.nvmlDeviceGetMaxClockInfo(nv, p.NVML_CLOCK_SM)
+                pw = p.nvmlDeviceGetPowerUsage(nv) / 1000.0
+                rs = p.nvmlDeviceGetCurrentClocksEventReasons(nv)
+                self.samples.append((sm, mx, pw, rs))
+            except Exception:
+                pass
+            time.sleep(0.01)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nv is not None:
+            self.stop_flag = True
+            self.t.join(timeout=2)
+            if not self.samples:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+            reasons = sorted({name for s in self.samples for bit, name in self.REASONS.items() if s[3] & bit})
+            return {"sm_mhz": float(np.median([s[0] for s in self.samples])),
+                    "sm_max_mhz": float(max(s[1] for s in self.samples)),
+                    "power_w_max": float(max(s[2] for s in self.samples)),
+                    "samples": len(self.samples), "source": "nvml 10 ms", "reasons": reasons}
         if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -110,7 +151,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "power_w_max": max(pw),
-                "samples": len(sm), "reasons": sorted(reasons)}
+                "samples": len(sm), "source": "nvidia-smi 100 ms", "reasons": sorted(reasons)}
 
 
 # ------------------------------------------------------------- cpu oracle -----
@@ -194,7 +235,9 @@ def workload_config(args, world):
             "M": args.n * pr, "N": args.n * pc, "K": args.n, "terms": args.terms,
             "inputs": "fp32", "tensor_core": "fp16 x fp16 -> fp32 accumulate (tcgen05 kind::f16)",
             "parallelism": f"2d-tile {pr}x{pc}" if world > 1 else "single",
-            "l2": "inputs 1 GiB/matrix > 126 MB L2: no flush needed"}
+            "l2": f"inputs {args.n * args.n * 4 / 2**30:.2f} GiB/matrix" + (
+                " > 126 MB L2: no flush needed" if args.n * args.n * 4 > 126e6 else
+                " < L2: inputs re-read from L2 between steps (small config)")}
 
 
 def grid_shape(world):
@@ -259,7 +302,7 @@ def main():
     h.timing_enable(True)
     h.timing_read()
     sampler.start()
-    time.sleep(0.3)
+    time.sleep(0.05)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()

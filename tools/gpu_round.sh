@@ -13,6 +13,6 @@ echo "launch list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm3 -s 3 -c 1 \
     -o gpurun_out/gemm3_full_$TAG python bench.py $LARGS > gpurun_out/ncu_full_$TAG.log 2>&1
 echo "full rc=$?"
-timeout 900 ncu --set full --clock-control none -k regex:split_t_kernel -s 3 -c 1 \
+timeout 900 ncu --set full --clock-control none -k regex:"split" -s 6 -c 2 \
     -o gpurun_out/split_t_full_$TAG python bench.py $LARGS > gpurun_out/ncu_split_$TAG.log 2>&1
 echo "split full rc=$?"
