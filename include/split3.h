@@ -170,6 +170,31 @@ int split3_gemm_planes(split3_handle_t h, int64_t M, int64_t N, int64_t K,
  * gpu_launches count; memsets are not counted). */
 int split3_last_launch_count(split3_handle_t h);
 
+/* ---- dense-network step helpers ----------------------------
+ * The GEMMs of a dense-layer training step go through split3_sgemm_ex; these FP32 kernels do the
+ * rest (SPEC.md mlp ledger: bias, activations, softmax/cross-entropy never in fp16).  All are
+ * deterministic (fixed reduction orders).  Device pointers, row-major, asynchronous on the
+ * handle's stream. */
+
+/* H = act(Z + b): b (length N, may be NULL) broadcast over the M rows; act = ReLU if relu != 0. */
+int split3_bias_act(split3_handle_t h, int64_t M, int64_t N, const float *Z, int64_t ldz, const float *b,
+                    float *H, int64_t ldh, int relu);
+
+/* dZ = dH * 1[H > 0] (ReLU backward through its output), packed M x N. */
+int split3_relu_backward(split3_handle_t h, int64_t M, int64_t N, const float *dH, const float *H, float *dZ);
+
+/* Row-wise softmax cross-entropy of logits L (M x N, packed): P = softmax(L) with max-subtraction,
+ * dL = (P - onehot(labels)) / M, and *d_loss = mean_r -log P[r, labels[r]] in fp64.
+ * P, dL, labels, d_loss may be NULL (skipped); row_scratch: M doubles (device) when d_loss != NULL. */
+int split3_softmax_xent(split3_handle_t h, int64_t M, int64_t N, const float *L, const int32_t *labels,
+                        float *P, float *dL, double *row_scratch, double *d_loss_sum);
+
+/* db[c] = sum_r dZ[r, c] (row order), dZ packed M x N. */
+int split3_bias_grad(split3_handle_t h, int64_t M, int64_t N, const float *dZ, float *db);
+
+/* w -= lr * g over n elements. */
+int split3_sgd_update(split3_handle_t h, int64_t n, float *w, const float *g, float lr);
+
 /* ---- numerics knob ------------------------------------------------------------------- */
 
 /* D_hi promotion period (DESIGN.md §3 R9): the tcgen05 FP32 accumulator truncates, so the

@@ -430,6 +430,52 @@ int split3_presplit(split3_handle_t h, int role, int64_t rows, int64_t cols, con
     return SPLIT3_OK;
 }
 
+int split3_bias_act(split3_handle_t h, int64_t M, int64_t N, const float* Z, int64_t ldz, const float* b,
+                    float* H, int64_t ldh, int relu) {
+    if (!h || M < 0 || N < 0) return SPLIT3_ERR_INVALID_VALUE;
+    if (M == 0 || N == 0) return SPLIT3_OK;
+    if (!Z || !H || ldz < N || ldh < N) return SPLIT3_ERR_INVALID_VALUE;
+    if (set_dev(h)) return SPLIT3_ERR_CUDA;
+    return split3::launch_bias_act(h->stream, M, N, Z, ldz, b, H, ldh, relu != 0, h->num_sms) < 0 ? SPLIT3_ERR_CUDA
+                                                                                                  : SPLIT3_OK;
+}
+
+int split3_relu_backward(split3_handle_t h, int64_t M, int64_t N, const float* dH, const float* H, float* dZ) {
+    if (!h || M < 0 || N < 0) return SPLIT3_ERR_INVALID_VALUE;
+    if (M == 0 || N == 0) return SPLIT3_OK;
+    if (!dH || !H || !dZ) return SPLIT3_ERR_INVALID_VALUE;
+    if (set_dev(h)) return SPLIT3_ERR_CUDA;
+    return split3::launch_relu_bwd(h->stream, M, N, dH, H, dZ, h->num_sms) < 0 ? SPLIT3_ERR_CUDA : SPLIT3_OK;
+}
+
+int split3_softmax_xent(split3_handle_t h, int64_t M, int64_t N, const float* L, const int32_t* labels, float* P,
+                        float* dL, double* row_scratch, double* d_loss_sum) {
+    if (!h || M < 0 || N < 0) return SPLIT3_ERR_INVALID_VALUE;
+    if (M == 0 || N == 0) return SPLIT3_OK;
+    if (!L || (d_loss_sum && (!row_scratch || !labels)) || (dL && !labels)) return SPLIT3_ERR_INVALID_VALUE;
+    if (set_dev(h)) return SPLIT3_ERR_CUDA;
+    return split3::launch_softmax_xent(h->stream, M, N, L, labels, P, dL, d_loss_sum ? row_scratch : nullptr,
+                                       d_loss_sum) < 0
+               ? SPLIT3_ERR_CUDA
+               : SPLIT3_OK;
+}
+
+int split3_bias_grad(split3_handle_t h, int64_t M, int64_t N, const float* dZ, float* db) {
+    if (!h || M < 0 || N < 0) return SPLIT3_ERR_INVALID_VALUE;
+    if (N == 0) return SPLIT3_OK;
+    if (!dZ || !db) return SPLIT3_ERR_INVALID_VALUE;
+    if (set_dev(h)) return SPLIT3_ERR_CUDA;
+    return split3::launch_col_sum(h->stream, M, N, dZ, db, h->num_sms) < 0 ? SPLIT3_ERR_CUDA : SPLIT3_OK;
+}
+
+int split3_sgd_update(split3_handle_t h, int64_t n, float* w, const float* g, float lr) {
+    if (!h || n < 0) return SPLIT3_ERR_INVALID_VALUE;
+    if (n == 0) return SPLIT3_OK;
+    if (!w || !g) return SPLIT3_ERR_INVALID_VALUE;
+    if (set_dev(h)) return SPLIT3_ERR_CUDA;
+    return split3::launch_sgd(h->stream, n, w, g, lr, h->num_sms) < 0 ? SPLIT3_ERR_CUDA : SPLIT3_OK;
+}
+
 int split3_set_schedule(split3_handle_t h, int group_m, int l2_policy_a, int l2_policy_b) {
     if (!h || group_m < 0 || group_m > 4096 || l2_policy_a < 0 || l2_policy_a > 2 || l2_policy_b < 0 ||
         l2_policy_b > 2)

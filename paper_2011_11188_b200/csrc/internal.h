@@ -53,4 +53,13 @@ int launch_gemm3(cudaStream_t s, int64_t M, int64_t N, int64_t K,
                  unsigned* wave_counter, const GemmTuneIn& tune, float* partial, int64_t partial_elems,
                  int* err);
 
+// ---- mlp_kernels.cu (NEXT #3: the non-GEMM steps of a dense-network training step) --------
+int launch_bias_act(cudaStream_t s, int64_t M, int64_t N, const float* Z, int64_t ldz, const float* b, float* H,
+                    int64_t ldh, int relu, int num_sms);
+int launch_relu_bwd(cudaStream_t s, int64_t M, int64_t N, const float* dH, const float* H, float* dZ, int num_sms);
+int launch_softmax_xent(cudaStream_t s, int64_t M, int64_t N, const float* L, const int32_t* labels, float* P,
+                        float* dL, double* row_loss, double* loss_sum);
+int launch_col_sum(cudaStream_t s, int64_t M, int64_t N, const float* dZ, float* db, int num_sms);
+int launch_sgd(cudaStream_t s, int64_t n, float* w, const float* g, float lr, int num_sms);
+
 }  // namespace split3

@@ -1,0 +1,139 @@
+// mlp_kernels.cu — the non-GEMM steps of a dense-network training step.
+//
+// PAPER.md:301 (§3.2 closing): "the form of operations in DNN are theoretically able to well
+// approximate operations of fp32 using mixed-precision operations in fp16".  The GEMMs of the
+// step run through split3_sgemm_ex (3 FP16 products); everything here stays FP32 (SPEC.md's
+// ledger: bias, activations and softmax/cross-entropy never in fp16).  All kernels are
+// HBM-bound elementwise / row / column passes; results are deterministic (fixed reduction
+// orders, no floating-point atomics except the fp64 loss sum, which is reduced per block first
+// and then added in block order by a second pass).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace split3 {
+namespace {
+
+// H = act(Z + b), b broadcast over rows.  act: 0 identity, 1 ReLU.
+__global__ void __launch_bounds__(256) bias_act_kernel(int64_t M, int64_t N, const float* __restrict__ Z,
+                                                       int64_t ldz, const float* __restrict__ b,
+                                                       float* __restrict__ H, int64_t ldh, int relu) {
+    const int64_t total = M * N;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / N, c = i - r * N;
+        float v = __fadd_rn(Z[r * ldz + c], b ? b[c] : 0.0f);
+        if (relu) v = v > 0.0f ? v : 0.0f;
+        H[r * ldh + c] = v;
+    }
+}
+
+// dZ = dH * 1[H > 0]   (ReLU backward through its output)
+__global__ void __launch_bounds__(256) relu_bwd_kernel(int64_t M, int64_t N, const float* __restrict__ dH,
+                                                       const float* __restrict__ H, float* __restrict__ dZ) {
+    const int64_t total = M * N;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+        dZ[i] = H[i] > 0.0f ? dH[i] : 0.0f;
+}
+
+// Row-wise softmax cross-entropy: one warp per row.  P = softmax(L) (max-subtracted),
+// dL = (P - onehot(label)) / M, row_loss[r] = -log P[r, label] in fp64.
+__global__ void __launch_bounds__(256) softmax_xent_kernel(int64_t M, int64_t N, const float* __restrict__ L,
+                                                           const int32_t* __restrict__ labels,
+                                                           float* __restrict__ P, float* __restrict__ dL,
+                                                           double* __restrict__ row_loss) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (row >= M) return;
+    const float* l = L + row * N;
+    float mx = -INFINITY;
+    for (int64_t c = lane; c < N; c += 32) mx = fmaxf(mx, l[c]);
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    double s = 0.0;
+    for (int64_t c = lane; c < N; c += 32) s += (double)expf(l[c] - mx);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const int32_t y = labels ? labels[row] : -1;
+    const float inv_m = 1.0f / (float)M;
+    for (int64_t c = lane; c < N; c += 32) {
+        const float p = (float)((double)expf(l[c] - mx) / s);
+        if (P) P[row * N + c] = p;
+        if (dL) dL[row * N + c] = (p - (c == y ? 1.0f : 0.0f)) * inv_m;
+    }
+    if (lane == 0 && row_loss) row_loss[row] = (y >= 0) ? -((double)(l[y] - mx) - log(s)) : 0.0;
+}
+
+// db[c] = sum_r dZ[r, c] in row order (deterministic): one thread per column, coalesced rows.
+__global__ void __launch_bounds__(256) col_sum_kernel(int64_t M, int64_t N, const float* __restrict__ dZ,
+                                                      float* __restrict__ db) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < N; c += (int64_t)gridDim.x * blockDim.x) {
+        float acc = 0.0f;
+        for (int64_t r = 0; r < M; r++) acc = __fadd_rn(acc, dZ[r * N + c]);
+        db[c] = acc;
+    }
+}
+
+// sum of n doubles in index order (single block, fixed tree): out[0] = sum
+__global__ void __launch_bounds__(256) sum_f64_kernel(int64_t n, const double* __restrict__ x, double* out) {
+    __shared__ double sh[256];
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += x[i];
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+// w -= lr * g
+__global__ void __launch_bounds__(256) sgd_kernel(int64_t n, float* __restrict__ w, const float* __restrict__ g,
+                                                  float lr) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        w[i] = __fmaf_rn(-lr, g[i], w[i]);
+}
+
+inline unsigned grid_for(int64_t work, int num_sms) {
+    int64_t g = (work + 255) / 256;
+    const int64_t cap = (int64_t)num_sms * 16;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (unsigned)g;
+}
+
+inline int ok() { return cudaPeekAtLastError() == cudaSuccess ? 1 : -1; }
+
+}  // namespace
+
+int launch_bias_act(cudaStream_t st, int64_t M, int64_t N, const float* Z, int64_t ldz, const float* b, float* H,
+                    int64_t ldh, int relu, int num_sms) {
+    bias_act_kernel<<<grid_for(M * N, num_sms), 256, 0, st>>>(M, N, Z, ldz, b, H, ldh, relu);
+    return ok();
+}
+int launch_relu_bwd(cudaStream_t st, int64_t M, int64_t N, const float* dH, const float* H, float* dZ, int num_sms) {
+    relu_bwd_kernel<<<grid_for(M * N, num_sms), 256, 0, st>>>(M, N, dH, H, dZ);
+    return ok();
+}
+int launch_softmax_xent(cudaStream_t st, int64_t M, int64_t N, const float* L, const int32_t* labels, float* P,
+                        float* dL, double* row_loss, double* loss_sum) {
+    const unsigned g = (unsigned)((M + 7) / 8);
+    softmax_xent_kernel<<<g, 256, 0, st>>>(M, N, L, labels, P, dL, row_loss);
+    if (ok() < 0) return -1;
+    if (row_loss && loss_sum) {
+        sum_f64_kernel<<<1, 256, 0, st>>>(M, row_loss, loss_sum);
+        if (ok() < 0) return -1;
+        return 2;
+    }
+    return 1;
+}
+int launch_col_sum(cudaStream_t st, int64_t M, int64_t N, const float* dZ, float* db, int num_sms) {
+    col_sum_kernel<<<grid_for(N, num_sms), 256, 0, st>>>(M, N, dZ, db);
+    return ok();
+}
+int launch_sgd(cudaStream_t st, int64_t n, float* w, const float* g, float lr, int num_sms) {
+    sgd_kernel<<<grid_for(n, num_sms), 256, 0, st>>>(n, w, g, lr);
+    return ok();
+}
+
+}  // namespace split3

@@ -1,0 +1,89 @@
+"""Dense network trained with split-FP16 GEMMs.
+
+"the form of operations in DNN are theoretically able to well approximate operations of fp32
+using mixed-precision operations in fp16".  Every matrix product of the step —
+forward Z = H W, backward dW = H^T dZ and dH = dZ W^T — runs through split3_sgemm_ex (3 FP16
+tensor-core products, or 4 / 1 as controls); bias, ReLU, softmax cross-entropy, bias gradients
+and the SGD update are the library's FP32 kernels (SPEC.md mlp ledger: only GEMMs in reduced
+precision).  Architecture: ReLU hidden layers, softmax output, mean cross-entropy.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from .split3 import Handle, handle
+
+MODES = {"three": {}, "four": {"four_term": True}, "one": {"one_term": True}}
+
+
+class DenseNet:
+    def __init__(self, sizes, seed: int = 0, mode: str = "three", device="cuda", h: Handle | None = None):
+        if mode not in MODES:
+            raise ValueError(f"mode must be one of {sorted(MODES)}")
+        self.sizes = list(sizes)
+        self.mode = mode
+        self.h = h or handle(torch.device(device))
+        rng = np.random.Generator(np.random.PCG64(seed))
+        self.W, self.b = [], []
+        for fin, fout in zip(self.sizes[:-1], self.sizes[1:]):
+            lim = math.sqrt(6.0 / (fin + fout))   # Glorot uniform (SPEC.md mlp ledger)
+            w = ((2.0 * rng.random((fin, fout)) - 1.0) * lim).astype(np.float32)
+            self.W.append(torch.from_numpy(w).to(device))
+            self.b.append(torch.zeros(fout, dtype=torch.float32, device=device))
+
+    @classmethod
+    def from_weights(cls, Ws, bs, mode="three", h=None):
+        net = cls.__new__(cls)
+        net.sizes = [Ws[0].shape[0]] + [w.shape[1] for w in Ws]
+        net.mode = mode
+        net.h = h or handle(Ws[0].device)
+        net.W = [w.contiguous() for w in Ws]
+        net.b = [b.contiguous() for b in bs]
+        return net
+
+    def _mm(self, A, B, transA=False, transB=False):
+        return self.h.sgemm_ex(A, B, transA=transA, transB=transB, **MODES[self.mode])
+
+    def forward(self, X):
+        """Per-layer activations [X, H1, ..., logits] (logits before softmax)."""
+        acts = [X]
+        L = len(self.W)
+        for i, (w, b) in enumerate(zip(self.W, self.b)):
+            Z = self._mm(acts[-1], w)
+            acts.append(self.h.bias_act(Z, b, relu=i < L - 1, out=Z))
+        return acts
+
+    def predict_proba(self, X):
+        P, _, _ = self.h.softmax_xent(self.forward(X)[-1], None, want_probs=True, want_grad=False)
+        return P
+
+    def loss(self, X, y):
+        _, _, loss = self.h.softmax_xent(self.forward(X)[-1], y, want_probs=False, want_grad=False)
+        return float(loss)
+
+    def backward(self, X, y):
+        """(loss, [dW], [db]) of the mean softmax cross-entropy."""
+        acts = self.forward(X)
+        _, dZ, loss = self.h.softmax_xent(acts[-1], y, want_probs=False, want_grad=True)
+        dWs, dbs = [None] * len(self.W), [None] * len(self.W)
+        for i in range(len(self.W) - 1, -1, -1):
+            dWs[i] = self._mm(acts[i], dZ, transA=True)          # H^T dZ
+            dbs[i] = self.h.bias_grad(dZ)
+            if i > 0:
+                dH = self._mm(dZ, self.W[i], transB=True)         # dZ W^T
+                dZ = self.h.relu_backward(dH, acts[i], out=dH)
+        return float(loss), dWs, dbs
+
+    def step(self, X, y, lr: float):
+        loss, dWs, dbs = self.backward(X, y)
+        for w, g in zip(self.W, dWs):
+            self.h.sgd_update(w, g, lr)
+        for b, g in zip(self.b, dbs):
+            self.h.sgd_update(b, g, lr)
+        return loss
+
+    def accuracy(self, X, y):
+        return float((self.forward(X)[-1].argmax(dim=1) == y).float().mean())

@@ -38,7 +38,8 @@ EXPORTS = (
     "split3_status_string", "split3_maxabs", "split3_split", "split3_gemm_planes",
     "split3_last_launch_count", "split3_timing_enable", "split3_timing_read",
     "split3_set_promotion", "split3_set_wave_sync", "split3_set_schedule",
-    "split3_sgemm_ex", "split3_presplit",
+    "split3_sgemm_ex", "split3_presplit", "split3_bias_act", "split3_relu_backward",
+    "split3_softmax_xent", "split3_bias_grad", "split3_sgd_update",
 )
 
 class split3_matrix(ctypes.Structure):
@@ -110,6 +111,11 @@ def load() -> ctypes.CDLL:
         lib.split3_set_schedule.argtypes = [_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         lib.split3_sgemm_ex.argtypes = [_p, _i64, _i64, _i64, ctypes.POINTER(split3_matrix),
                                         ctypes.POINTER(split3_matrix), _p, _i64, ctypes.c_uint32]
+        lib.split3_bias_act.argtypes = [_p, _i64, _i64, _p, _i64, _p, _p, _i64, ctypes.c_int]
+        lib.split3_relu_backward.argtypes = [_p, _i64, _i64, _p, _p, _p]
+        lib.split3_softmax_xent.argtypes = [_p, _i64, _i64, _p, _p, _p, _p, _p, _p]
+        lib.split3_bias_grad.argtypes = [_p, _i64, _i64, _p, _p]
+        lib.split3_sgd_update.argtypes = [_p, _i64, _p, _p, ctypes.c_float]
         lib.split3_presplit.argtypes = [_p, ctypes.c_int, _i64, _i64, _p, _i64, ctypes.c_int, _p, _p,
                                         _i64, _p]
         lib.split3_timing_read.argtypes = [_p, ctypes.POINTER(ctypes.c_double),
@@ -291,6 +297,51 @@ class Handle:
         if st != OK:
             raise Split3Error(st, "split3_sgemm_ex")
         return out
+
+    # -- dense-network step helpers (NEXT #3) ------------------------------------------
+    def _chk(self, st, what):
+        if st != OK:
+            raise Split3Error(st, what)
+
+    def bias_act(self, Z, b, relu: bool, out=None):
+        out = torch.empty_like(Z) if out is None else out
+        self._bind_stream()
+        self._chk(self._lib.split3_bias_act(self._h, Z.shape[0], Z.shape[1], _ptr(Z), _ld(Z), _ptr(b),
+                                            _ptr(out), _ld(out), int(relu)), "split3_bias_act")
+        return out
+
+    def relu_backward(self, dH, H, out=None):
+        out = torch.empty_like(dH) if out is None else out
+        self._bind_stream()
+        self._chk(self._lib.split3_relu_backward(self._h, dH.shape[0], dH.shape[1], _ptr(dH), _ptr(H),
+                                                 _ptr(out)), "split3_relu_backward")
+        return out
+
+    def softmax_xent(self, L, labels=None, want_probs=True, want_grad=True):
+        """(P, dL, loss) for logits L (M x N) and int32 labels; loss is a 0-d fp64 device tensor."""
+        M, N = L.shape
+        P = torch.empty_like(L) if want_probs else None
+        dL = torch.empty_like(L) if (want_grad and labels is not None) else None
+        loss = torch.zeros((), dtype=torch.float64, device=L.device) if labels is not None else None
+        rows = torch.empty(M, dtype=torch.float64, device=L.device) if labels is not None else None
+        self._bind_stream()
+        self._chk(self._lib.split3_softmax_xent(self._h, M, N, _ptr(L), _ptr(labels), _ptr(P), _ptr(dL),
+                                                _ptr(rows), _ptr(loss)), "split3_softmax_xent")
+        if loss is not None:
+            loss = loss / M
+        return P, dL, loss
+
+    def bias_grad(self, dZ, out=None):
+        out = torch.empty(dZ.shape[1], dtype=torch.float32, device=dZ.device) if out is None else out
+        self._bind_stream()
+        self._chk(self._lib.split3_bias_grad(self._h, dZ.shape[0], dZ.shape[1], _ptr(dZ), _ptr(out)),
+                  "split3_bias_grad")
+        return out
+
+    def sgd_update(self, w, g, lr: float):
+        self._bind_stream()
+        self._chk(self._lib.split3_sgd_update(self._h, w.numel(), _ptr(w), _ptr(g), float(lr)),
+                  "split3_sgd_update")
 
     def sgemm_host(self, A, B, out=None, four_term=False, one_term=False):
         """C = A @ B with HOST (numpy / CPU torch) buffers: copies inside the C-ABI call."""

@@ -73,3 +73,16 @@ def torch_matrix(kind: str, rows: int, cols: int, seed: int, device="cuda"):
         bits = torch.where(exp >= 30, bits & ~0x1000, bits)
         return bits.to(torch.int16).view(torch.float16).to(torch.float32)
     raise ValueError(f"unknown kind {kind!r}")
+
+
+def make_blobs(n: int, classes: int, dim: int, separation: float, seed: int):
+    """Seeded Gaussian clusters (SPEC.md mlp make_blobs): class means at distance ~separation,
+    unit-variance noise.  Returns (X float32 n x dim, y int32 n)."""
+    if classes < 2:
+        raise ValueError("classes must be >= 2")
+    rng = np.random.Generator(np.random.PCG64(seed))
+    centers = rng.standard_normal((classes, dim))
+    centers *= (separation / np.sqrt(2.0)) / np.linalg.norm(centers, axis=1, keepdims=True)
+    y = rng.integers(0, classes, size=n).astype(np.int32)
+    X = (centers[y] + rng.standard_normal((n, dim))).astype(np.float32)
+    return X, y
