@@ -101,8 +101,8 @@ size_t ws_bytes_for(int64_t M, int64_t N, int64_t K, bool planesA, bool planesB,
     size_t b = kScalarBytes + 2 * align256((size_t)M * (size_t)plane_ld(K) * 2) +
                2 * align256((size_t)N * (size_t)plane_ld(K) * 2);
     if (terms_for_partials) {
-        const int S = split3::gemm3_k_slices(M, N, K, terms_for_partials, 148, 0);
-        if (S > 1) b += align256((size_t)S * M * N * 4);
+        const split3::SplitPlan p = split3::gemm3_split_plan(M, N, K, terms_for_partials, 148, 0);
+        b += align256((size_t)split3::gemm3_partial_elems(p, terms_for_partials) * 4);
     }
     return b;
 }

@@ -206,6 +206,24 @@ __device__ __forceinline__ void tile_coords(int64_t tile, int64_t num_m, int64_t
 }
 
 
+__device__ __forceinline__ void decode_unit(int64_t u, const SplitPlan& p, int num_kb, int kps, int64_t& tile,
+                                            int& kb_begin, int& kb_end, int& slot) {
+    if (u < p.whole) {
+        tile = u;
+        kb_begin = 0;
+        kb_end = num_kb;
+        slot = -1;
+        return;
+    }
+    const int64_t v = u - p.whole;
+    const int64_t t = v % p.nsplit;
+    const int s = (int)(v / p.nsplit);
+    tile = p.whole + t;
+    kb_begin = s * kps;
+    kb_end = kb_begin + kps < num_kb ? kb_begin + kps : num_kb;
+    slot = (int)v;   // = s * nsplit + t
+}
+
 // Tile geometry per instantiation: BN_ = 256 (3-term, 1-term) or 128 (4-term: D_lo needs TMEM).
 template <int BN_>
 struct Geo {
@@ -235,7 +253,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
              const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
              int M, int N, int K, int promo_kb, const int32_t* __restrict__ d_sA,
              const int32_t* __restrict__ d_sB, float* __restrict__ C, int64_t ldc,
-             unsigned* __restrict__ wave_counter, const GemmTune tune, int k_slices,
+             unsigned* __restrict__ wave_counter, const GemmTune tune, const SplitPlan plan,
              float* __restrict__ partial) {
     using G = Geo<BN_>;
     constexpr int STAGES = G::STAGES;
@@ -273,10 +291,11 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     const int64_t num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + BN_ - 1) / BN_;
     const int64_t num_tiles = num_m * num_n;
     const int num_kb = (K + BK - 1) / BK;
-    // work unit u = slice * num_tiles + tile; slice s covers k-blocks [s*kps, min((s+1)*kps, num_kb))
-    // (split-K for problems with fewer tiles than CTA pairs; the host guarantees non-empty slices)
-    const int kps = (num_kb + k_slices - 1) / k_slices;
-    const int64_t num_units = num_tiles * k_slices;
+    // Work units (SplitPlan, host-chosen): units [0, whole) are whole tiles 0..whole-1; the
+    // remaining `nsplit` tiles (the tail wave, or all tiles of a small problem) are cut into
+    // `slices` K slices of kps k-blocks: unit whole + s*nsplit + t = slice s of tile whole + t.
+    const int kps = (num_kb + plan.slices - 1) / plan.slices;
+    const int64_t num_units = plan.whole + plan.nsplit * plan.slices;
     const int64_t pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
 
     if (warp == 0 && lane == 0) {
@@ -313,9 +332,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         unsigned wave_target = 0;   // cumulative arrivals expected up to this tile index
         int64_t idx = 0;
         for (int64_t unit = pair; unit < num_units; unit += num_pairs, idx++) {
-            const int64_t tile = unit % num_tiles;
-            const int kb_begin = (int)(unit / num_tiles) * kps;
-            const int kb_end = kb_begin + kps < num_kb ? kb_begin + kps : num_kb;
+            int64_t tile;
+            int kb_begin, kb_end, slot;
+            decode_unit(unit, plan, num_kb, kps, tile, kb_begin, kb_end, slot);
             if (wave_counter && idx > 0) {
                 int64_t active = num_units - idx * num_pairs;   // pairs with an idx-th unit
                 if (active > num_pairs) active = num_pairs;
@@ -357,8 +376,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             uint32_t cc = 0;       // global D_hi chunk counter
             uint32_t tc = 0;       // tile counter
             for (int64_t unit = pair; unit < num_units; unit += num_pairs, tc++) {
-                const int kb_begin = (int)(unit / num_tiles) * kps;
-                const int kb_end = kb_begin + kps < num_kb ? kb_begin + kps : num_kb;
+                int64_t tile_unused;
+                int kb_begin, kb_end, slot;
+                decode_unit(unit, plan, num_kb, kps, tile_unused, kb_begin, kb_end, slot);
                 const uint32_t t_mid = tmem_base + COL_MID;
                 const uint32_t t_lo = tmem_base + COL_LO;
                 bool mid_ready = false;
@@ -434,10 +454,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * NCOL);
         uint32_t cc = 0, tc = 0;
         for (int64_t unit = pair; unit < num_units; unit += num_pairs, tc++) {
-            const int64_t tile = unit % num_tiles;
-            const int slice = (int)(unit / num_tiles);
-            const int kb_begin = slice * kps;
-            const int kb_end = kb_begin + kps < num_kb ? kb_begin + kps : num_kb;
+            int64_t tile;
+            int kb_begin, kb_end, slot;
+            decode_unit(unit, plan, num_kb, kps, tile, kb_begin, kb_end, slot);
             int64_t mb, nb;
             tile_coords(tile, num_m, num_n, tune.group_m, mb, nb);
             float master[NCOL];
@@ -480,22 +499,14 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                 __syncwarp();
                 if (lane == 0) mbar_arrive_leader(smem_u32(&mempty_bar[0]));   // D_mid free early
             }
-            if (k_slices > 1) {                          // split-K: raw partial, reduced later
-                const int64_t row = mb * 2 * BM + crank * BM + quad * 32 + lane;
-                const int64_t col0 = nb * BN_ + half * NCOL;
-                if (row < M) {
-                    float* prow = partial + ((int64_t)slice * M + row) * N + col0;
-                    if ((N % 4) == 0 && col0 + NCOL <= N) {
+            if (slot >= 0) {                              // split tile: raw partial, reduced later
+                // tile-local partial block (2*BM x BN_) of slot `slot`
+                const int lr = crank * BM + quad * 32 + lane;
+                float* prow = partial + ((int64_t)slot * (2 * BM) + lr) * BN_ + half * NCOL;
 #pragma unroll
-                        for (int j = 0; j < NCOL / 4; j++)
-                            reinterpret_cast<float4*>(prow)[j] =
-                                make_float4(master[4 * j], master[4 * j + 1], master[4 * j + 2], master[4 * j + 3]);
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < NCOL; j++)
-                            if (col0 + j < N) prow[j] = master[j];
-                    }
-                }
+                for (int j = 0; j < NCOL / 4; j++)
+                    reinterpret_cast<float4*>(prow)[j] =
+                        make_float4(master[4 * j], master[4 * j + 1], master[4 * j + 2], master[4 * j + 3]);
                 continue;
             }
             if (fast) {                                  // warp-uniform branch
@@ -534,21 +545,30 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     }
 }
 
-// Split-K reduction: C = 2^(sA+sB) * sum_{s=0}^{S-1} P[s]  (fixed order -> deterministic).
-__global__ void __launch_bounds__(256) ksplit_reduce_kernel(const float* __restrict__ P, int S, int64_t M,
-                                                            int64_t N, float* __restrict__ C, int64_t ldc,
+// Split-tile reduction: for each split tile t and element (r, c) of its 256 x BN block,
+// C = 2^(sA+sB) * sum_{s=0}^{S-1} P[s*nsplit + t][r][c]  (fixed slice order -> deterministic).
+__global__ void __launch_bounds__(256) ksplit_reduce_kernel(const float* __restrict__ P, SplitPlan plan, int bn,
+                                                            int64_t M, int64_t N, int group_m,
+                                                            float* __restrict__ C, int64_t ldc,
                                                             const int32_t* __restrict__ d_sA,
                                                             const int32_t* __restrict__ d_sB) {
     const int sAB = *d_sA + *d_sB;
     const bool fast = sAB >= -126 && sAB <= 127;
     const float f = fast ? __uint_as_float((unsigned)(sAB + 127) << 23) : 1.0f;
     const double fd = __longlong_as_double((long long)(sAB + 1023) << 52);
-    const int64_t total = M * N;
+    const int64_t blk = (int64_t)(2 * BM) * bn;
+    const int64_t total = plan.nsplit * blk;
+    const int64_t num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + bn - 1) / bn;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        float acc = P[i];
-        for (int s = 1; s < S; s++) acc = __fadd_rn(acc, P[(int64_t)s * total + i]);
-        const int64_t r = i / N, c = i - r * N;
-        C[r * ldc + c] = fast ? acc * f : __double2float_rn(__dmul_rn((double)acc, fd));
+        const int64_t t = i / blk, e = i - t * blk;
+        const int64_t r = e / bn, c = e - r * bn;
+        int64_t mb, nb;
+        tile_coords(plan.whole + t, num_m, num_n, group_m, mb, nb);
+        const int64_t row = mb * 2 * BM + r, col = nb * bn + c;
+        if (row >= M || col >= N) continue;
+        float acc = P[t * blk + e];
+        for (int s = 1; s < plan.slices; s++) acc = __fadd_rn(acc, P[((int64_t)s * plan.nsplit + t) * blk + e]);
+        C[row * ldc + col] = fast ? acc * f : __double2float_rn(__dmul_rn((double)acc, fd));
     }
 }
 
@@ -589,7 +609,7 @@ template <int TERMS, int BN_>
 int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap& a1,
              const CUtensorMap& a2, const CUtensorMap& b1, const CUtensorMap& b2,
              const int32_t* d_sA, const int32_t* d_sB, float* C, int64_t ldc, int num_sms,
-             int promo_kb, unsigned* wave_counter, const GemmTune& tune, int k_slices, float* partial) {
+             int promo_kb, unsigned* wave_counter, const GemmTune& tune, const SplitPlan& plan, float* partial) {
     constexpr int SMEM_BYTES = Geo<BN_>::SMEM;
     static bool attr_set = false;
     if (!attr_set) {
@@ -598,33 +618,49 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
             return -1;
         attr_set = true;
     }
-    const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN_ - 1) / BN_) * k_slices;
+    const int64_t tiles = plan.whole + plan.nsplit * plan.slices;   // work units
     const int64_t pairs = num_sms / 2;
     const int grid = 2 * (int)(tiles < pairs ? tiles : pairs);
     if (wave_counter && cudaMemsetAsync(wave_counter, 0, sizeof(unsigned), st) != cudaSuccess) return -1;
     gemm3_kernel<TERMS, BN_><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(a1, a2, b1, b2, (int)M, (int)N, (int)K,
                                                                promo_kb, d_sA, d_sB, C, ldc, wave_counter,
-                                                               tune, k_slices, partial);
+                                                               tune, plan, partial);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 }  // namespace
 
-int gemm3_k_slices(int64_t M, int64_t N, int64_t K, int terms, int num_sms, int promo_kb) {
+SplitPlan gemm3_split_plan(int64_t M, int64_t N, int64_t K, int terms, int num_sms, int promo_kb) {
     const int bn = terms == 4 ? 128 : 256;
     const int64_t tiles = ((M + 255) / 256) * ((N + bn - 1) / bn);
     const int64_t pairs = num_sms / 2;
     const int64_t num_kb = (K + 63) / 64;
-    if (tiles >= pairs || tiles == 0) return 1;
+    SplitPlan p;
+    p.whole = tiles;
+    p.nsplit = 0;
+    p.slices = 1;
+    if (tiles == 0 || pairs < 1) return p;
     const int promo = promo_kb > 0 ? promo_kb : kDefaultPromoKb;
-    // at least 4 k-blocks (and one promotion chunk) per slice, at most 16 slices
-    int64_t S = pairs / tiles;
-    const int64_t max_by_k = num_kb / (promo > 4 ? promo : 4);
+    const int64_t max_by_k = num_kb / (promo > 4 ? promo : 4);   // >= 4 k-blocks per slice
+    // tiles split along K: all of them when there is less than one wave, else the tail wave
+    const int64_t rem = tiles < pairs ? tiles : tiles % pairs;
+    if (rem == 0) return p;
+    int64_t S = pairs / rem;
     if (S > max_by_k) S = max_by_k;
     if (S > 16) S = 16;
-    if (S < 2) return 1;
+    if (S < 2) return p;
     const int64_t kps = (num_kb + S - 1) / S;
-    return (int)((num_kb + kps - 1) / kps);   // every slice non-empty
+    S = (num_kb + kps - 1) / kps;              // every slice non-empty
+    if (S < 2) return p;
+    p.whole = tiles - rem;
+    p.nsplit = rem;
+    p.slices = (int)S;
+    return p;
+}
+
+int64_t gemm3_partial_elems(const SplitPlan& p, int terms) {
+    const int bn = terms == 4 ? 128 : 256;
+    return p.slices > 1 ? (int64_t)p.slices * p.nsplit * 256 * bn : 0;
 }
 
 int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_t* A1,
@@ -647,20 +683,25 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     auto pol = [](int p) { return p == 1 ? kPolicyFirst : (p == 2 ? kPolicyLast : kPolicyNormal); };
     tune.pol_a = pol(tin.pol_a);
     tune.pol_b = pol(tin.pol_b);
-    int S = partial ? gemm3_k_slices(M, N, K, terms, num_sms, promo) : 1;
-    if (S > 1 && (int64_t)S * M * N > partial_elems) S = 1;
+    SplitPlan plan = gemm3_split_plan(M, N, K, terms, num_sms, promo);
+    if (plan.slices > 1 && (!partial || gemm3_partial_elems(plan, terms) > partial_elems)) {
+        plan.whole += plan.nsplit;   // no room for partials: whole tiles only
+        plan.nsplit = 0;
+        plan.slices = 1;
+    }
     int r;
     if (terms == 1)
-        r = launch_t<1, 256>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, S, partial);
+        r = launch_t<1, 256>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial);
     else if (terms == 4)
-        r = launch_t<4, 128>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, S, partial);
+        r = launch_t<4, 128>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial);
     else
-        r = launch_t<3, 256>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, S, partial);
+        r = launch_t<3, 256>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial);
     if (r < 0) { *err = 4; return -1; }
-    if (S > 1) {
-        int64_t blocks = (M * N + 255) / 256;
+    if (plan.slices > 1) {
+        const int bn = terms == 4 ? 128 : 256;
+        int64_t blocks = (plan.nsplit * 256 * bn + 255) / 256;
         if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
-        ksplit_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(partial, S, M, N, C, ldc, d_sA, d_sB);
+        ksplit_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(partial, plan, bn, M, N, tune.group_m, C, ldc, d_sA, d_sB);
         if (cudaPeekAtLastError() != cudaSuccess) { *err = 4; return -1; }
         r += 1;
     }

@@ -40,9 +40,16 @@ struct GemmTune {
     uint64_t pol_a, pol_b;
 };
 
-// Number of K slices the GEMM uses for (M, N, K) (split-K when there are fewer tile pairs than
-// CTA pairs); the partial buffer needs slices * M * N floats.
-int gemm3_k_slices(int64_t M, int64_t N, int64_t K, int terms, int num_sms, int promo_kb);
+// Work split of the persistent GEMM: `whole` tiles run over the full K; the last `nsplit` tiles
+// (all tiles of a problem with fewer tiles than CTA pairs, else the tail wave) are cut into
+// `slices` K slices whose partials are reduced in a fixed order (deterministic).
+struct SplitPlan {
+    int64_t whole;
+    int64_t nsplit;
+    int slices;
+};
+SplitPlan gemm3_split_plan(int64_t M, int64_t N, int64_t K, int terms, int num_sms, int promo_kb);
+int64_t gemm3_partial_elems(const SplitPlan& p, int terms);   // floats of partial workspace
 
 // terms: 1, 3 or 4.  `partial` (may be NULL: no split-K) holds partial_elems floats.
 // Returns kernels launched (1, or 2 with the split-K reduction) or -1 (*err set to a status).

@@ -140,7 +140,7 @@ def test_dist_driver_nccl_one_rank(h):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
-        M, N, K = 2048, 2560, 640     # >= 74 pair tiles: neither path uses split-K
+        M, N, K = 512, 256 * 37, 640     # 74 pair tiles: no tile is split along K
         A = torch_matrix("uniform", M, K, seed=7, device="cuda")
         B = torch_matrix("loguni", K, N, seed=8, device="cuda")
         tile = d2.sgemm_2d(A, B, M, N, d2.CudaOps(h))
