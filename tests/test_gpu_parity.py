@@ -400,3 +400,27 @@ def test_host_pipeline_bitwise_equals_device(h, M, N):
     for flags in (0, 0):   # twice: reuse of the handle's streams/events
         h.sgemm_host_ptr(M, N, K, Ah.data_ptr(), Bh.data_ptr(), Ch.data_ptr(), flags)
         assert torch.equal(Ch.view(torch.int32), ref.view(torch.int32))
+
+
+def test_planes_exhaustive_fp32_range(h, orc):
+    """Every fp32 bit pattern with |x| < 2^15 (2 x 0x47000000 ~ 2.4e9 values, in 2^28-pattern
+    chunks): GPU planes == oracle planes, bit for bit (the GPU cvt.rn.f16.f32 pin).
+    Each chunk is split with its own max-abs scale on both sides."""
+    chunk = 1 << 28
+    checked = 0
+    for sign in (0, 0x80000000):
+        for start in range(0, 0x47000000, chunk):
+            n = min(chunk, 0x47000000 - start)
+            bits = torch.arange(start, start + n, dtype=torch.int64, device="cuda") + sign
+            X = bits.to(torch.int32).view(torch.float32).view(n // 4096, 4096) if n % 4096 == 0 else None
+            assert X is not None
+            del bits
+            hi, lo, s, _ = _gpu_split(h, X, transpose=False)
+            hi_o, lo_o, s_o = orc.split(X.cpu().numpy())
+            assert s == s_o
+            assert np.array_equal(_planes_np(hi, X.shape[0], 4096), hi_o)
+            assert np.array_equal(_planes_np(lo, X.shape[0], 4096), lo_o)
+            checked += n
+            del X, hi, lo
+            torch.cuda.empty_cache()
+    assert checked == 2 * 0x47000000
