@@ -116,9 +116,15 @@ class CudaOps:
 
 
 def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, groups=None,
-             out: torch.Tensor | None = None, four_term=False, one_term=False):
+             out: torch.Tensor | None = None, four_term=False, one_term=False, overlap: bool = True):
     """One rank's share of C = A*B.  A_blk: its (M/P) x K block of A; B_blk: its K x (N/P)
-    block of B.  Returns the rank's m x n C tile (see the module docstring)."""
+    block of B.  Returns the rank's m x n C tile (see the module docstring).
+
+    overlap (NCCL only): the B^T panel is gathered first; the GEMM on the rank's OWN A rows then
+    runs on the compute stream while the A panel is all-gathered on a communication stream; the
+    other row blocks follow when it lands.  Each row block is a separate GEMM over whole tiles,
+    so every C element is computed exactly as in the non-overlapped schedule.
+    """
     world = dist.get_world_size()
     rank = dist.get_rank()
     pr, pc = grid_for(world)
@@ -128,6 +134,8 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
         groups = make_groups(world)
     row_groups, col_groups = groups
     dev = A_blk.device
+    m, n = M // pr, N // pc
+    mb = M // world                      # rows of one A block
     # 1-2: global max-abs of A and B (exact, order-free)
     mx = torch.zeros(2, dtype=torch.float32, device=dev)
     ops.maxabs_into(A_blk, mx[0:1])
@@ -136,17 +144,49 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
     # 3: local split with the global scale
     a_hi, a_lo, sA = ops.split(A_blk, mx[0:1], False)
     b_hi, b_lo, sB = ops.split(B_blk, mx[1:2], True)
-    # 4: plane panels
-    A1 = _gather_rows(a_hi, row_groups[i], pc)
+    rowblocks = overlap and pc > 1
+    use_streams = rowblocks and dev.type == "cuda" and dist.get_backend() == "nccl"
+    # 4a: B^T panel (needed by every row block)
     B1t = _gather_rows(b_hi, col_groups[j], pr)
-    if one_term:
-        A2, B2t = A1, B1t
+    B2t = B1t if one_term else _gather_rows(b_lo, col_groups[j], pr)
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float32, device=dev)
+    if not rowblocks:
+        # 4b + 5: A panel, then one GEMM on the whole tile
+        A1 = _gather_rows(a_hi, row_groups[i], pc)
+        A2 = A1 if one_term else _gather_rows(a_lo, row_groups[i], pc)
+        res = ops.gemm(m, n, K, A1, A2, sA, B1t, B2t, sB, out, four_term, one_term)
+        if res is not out:
+            out.copy_(res)
+        return out
+    # 4b under 5a: gather the A panel (side stream under NCCL) while the own rows are multiplied
+    compute = torch.cuda.current_stream(dev) if use_streams else None
+    comm = torch.cuda.Stream(device=dev) if use_streams else None
+    if use_streams:
+        comm.wait_stream(compute)
+        with torch.cuda.stream(comm):
+            A1 = _gather_rows(a_hi, row_groups[i], pc)
+            A2 = A1 if one_term else _gather_rows(a_lo, row_groups[i], pc)
+    own = slice(j * mb, (j + 1) * mb)
+    res = ops.gemm(mb, n, K, a_hi, a_hi if one_term else a_lo, sA, B1t, B2t, sB, out[own], four_term, one_term)
+    if res is not None and res.data_ptr() != out[own].data_ptr():
+        out[own].copy_(res)
+    if use_streams:
+        compute.wait_stream(comm)
     else:
-        A2 = _gather_rows(a_lo, row_groups[i], pc)
-        B2t = _gather_rows(b_lo, col_groups[j], pr)
-    m, n = M // pr, N // pc
-    # 5: local GEMM on the C tile
-    return ops.gemm(m, n, K, A1, A2, sA, B1t, B2t, sB, out, four_term, one_term)
+        A1 = _gather_rows(a_hi, row_groups[i], pc)
+        A2 = A1 if one_term else _gather_rows(a_lo, row_groups[i], pc)
+    for q in range(pc):
+        if q == j:
+            continue
+        rs = slice(q * mb, (q + 1) * mb)
+        res = ops.gemm(mb, n, K, A1[rs], A2[rs], sA, B1t, B2t, sB, out[rs], four_term, one_term)
+        if res is not None and res.data_ptr() != out[rs].data_ptr():
+            out[rs].copy_(res)
+    if use_streams:
+        A1.record_stream(compute)
+        A2.record_stream(compute)
+    return out
 
 
 class TileGemm:

@@ -70,7 +70,7 @@ class OracleOps:
         return torch.from_numpy(C)
 
 
-def _worker(rank, world, port, M, N, K, terms, q):
+def _worker(rank, world, port, M, N, K, terms, q, overlap=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -82,8 +82,11 @@ def _worker(rank, world, port, M, N, K, terms, q):
         B = numpy_matrix("uniform", K, N, seed=2)
         r0, r1 = d2.a_block_rows(M, world, rank)
         c0, c1 = d2.b_block_cols(N, world, rank)
+        pr, pc = d2.grid_for(world)
+        out = torch.empty((M // pr, N // pc), dtype=torch.float64)   # the oracle's fp64 tile
         tile = d2.sgemm_2d(torch.from_numpy(A[r0:r1].copy()), torch.from_numpy(B[:, c0:c1].copy()),
-                           M, N, OracleOps(oracle), four_term=terms == 4, one_term=terms == 1)
+                           M, N, OracleOps(oracle), out=out, four_term=terms == 4, one_term=terms == 1,
+                           overlap=overlap)
         full = oracle.sgemm(A, B, terms=terms)
         tr0, tr1, tc0, tc1 = d2.c_tile(M, N, world, rank)
         ok = np.array_equal(tile.numpy(), full[tr0:tr1, tc0:tc1])
@@ -100,13 +103,14 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world,terms", [(2, 3), (4, 3), (2, 4)])
-def test_sgemm_2d_matches_single_process(orc, world, terms):
+@pytest.mark.parametrize("world,terms,overlap", [(2, 3, True), (4, 3, True), (2, 4, True), (2, 3, False),
+                                                (4, 1, False)])
+def test_sgemm_2d_matches_single_process(orc, world, terms, overlap):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     M, N, K = 16 * world, 12 * world, 40
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, M, N, K, terms, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, M, N, K, terms, q, overlap)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
