@@ -211,11 +211,10 @@ __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ X,
 }
 
 // Transposed split: X is rows x cols (row-major), planes are cols x rows (ldp >= rows), i.e.
-// the K-major layout of B^T the GEMM reads.  64 x 64 tiles through shared memory: coalesced
-// float4 reads along X's rows, coalesced 16-byte writes along the planes' rows.
-constexpr int TT = 64;
-constexpr int TPAD = TT + 2;   // halves per smem row (132 B: 4-B aligned, breaks bank stride)
-
+// the K-major layout of B^T the GEMM reads.  64 x 64 tiles through shared memory (measured:
+// 32 x 64 ties, 128 x 64 and N-fastest tile orders are slower): 256-B reads along X's rows,
+// full 128-B lines written along the planes' rows; the next tile's loads are in flight while the
+// current tile is stored.
 template <bool VEC>
 __global__ void __launch_bounds__(256) split_t_kernel(const float* __restrict__ X, int64_t rows,
                                                       int64_t cols, int64_t ld,
@@ -223,31 +222,34 @@ __global__ void __launch_bounds__(256) split_t_kernel(const float* __restrict__ 
                                                       uint16_t* __restrict__ hi,
                                                       uint16_t* __restrict__ lo, int64_t ldp,
                                                       int32_t* d_sexp) {
-    __shared__ __align__(16) unsigned short s1[TT][TPAD];
-    __shared__ __align__(16) unsigned short s2[TT][TPAD];
+    constexpr int TK = 64, TN = 64;   // X rows (K) x X columns (N) per tile
+    constexpr int TKP = TK + 2;       // halves per smem row (132 B: 4-B aligned, breaks the bank stride)
+    __shared__ __align__(16) unsigned short s1[TN][TKP];
+    __shared__ __align__(16) unsigned short s2[TN][TKP];
     const int s = scale_exp_dev(*d_max);
     const float f = pow2_neg(s);
     if (d_sexp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *d_sexp = s;
     const int t = threadIdx.x;
-    const int64_t ntr = (rows + TT - 1) / TT, ntc = (cols + TT - 1) / TT;
+    const int64_t ntr = (rows + TK - 1) / TK, ntc = (cols + TN - 1) / TN;
     const int64_t ntiles = ntr * ntc;
-    // thread t covers X rows r0 + t/16 + 16 i (i < 4), columns c0 + 4 (t%16) .. +3
+    // thread t covers the adjacent X rows rr, rr + 1 with rr = 2 (t/16) + 32 i (i < 2) and the
+    // columns cc .. cc+3, cc = 4 (t%16): its two rows of a column pack into one 32-bit smem store.
     const int cc = 4 * (t % 16);
-    float v[4][4];
+    float v[4][4];   // [2 i + row parity][column]
     auto load_tile = [&](int64_t tile) {
-        const int64_t r0 = (tile % ntr) * TT, c0 = (tile / ntr) * TT;
+        const int64_t r0 = (tile % ntr) * TK, c0 = (tile / ntr) * TN;
 #pragma unroll
-        for (int i = 0; i < 4; i++) {
-            const int64_t r = r0 + t / 16 + 16 * i, c = c0 + cc;
-            v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0.f;
+        for (int q = 0; q < 4; q++) {
+            const int64_t r = r0 + 2 * (t / 16) + 32 * (q >> 1) + (q & 1), c = c0 + cc;
+            v[q][0] = v[q][1] = v[q][2] = v[q][3] = 0.f;
             if (r < rows) {
                 if (VEC && c + 3 < cols) {
-                    float4 q = __ldcs(reinterpret_cast<const float4*>(X + r * ld + c));
-                    v[i][0] = q.x; v[i][1] = q.y; v[i][2] = q.z; v[i][3] = q.w;
+                    float4 w = __ldcs(reinterpret_cast<const float4*>(X + r * ld + c));
+                    v[q][0] = w.x; v[q][1] = w.y; v[q][2] = w.z; v[q][3] = w.w;
                 } else {
 #pragma unroll
                     for (int j = 0; j < 4; j++)
-                        if (c + j < cols) v[i][j] = X[r * ld + c + j];
+                        if (c + j < cols) v[q][j] = X[r * ld + c + j];
                 }
             }
         }
@@ -255,17 +257,18 @@ __global__ void __launch_bounds__(256) split_t_kernel(const float* __restrict__ 
     int64_t tile = blockIdx.x;
     if (tile < ntiles) load_tile(tile);
     for (; tile < ntiles; tile += gridDim.x) {
-        const int64_t r0 = (tile % ntr) * TT;   // consecutive blocks walk down X's rows (K)
-        const int64_t c0 = (tile / ntr) * TT;
+        const int64_t r0 = (tile % ntr) * TK;   // consecutive blocks walk down X's rows (K)
+        const int64_t c0 = (tile / ntr) * TN;
 #pragma unroll
-        for (int i = 0; i < 4; i++) {
-            const int rr = t / 16 + 16 * i;
+        for (int i = 0; i < 2; i++) {
+            const int rr = 2 * (t / 16) + 32 * i;
 #pragma unroll
             for (int j = 0; j < 4; j++) {
-                unsigned short a, b;
-                split1(v[i][j], f, a, b);
-                s1[cc + j][rr] = a;
-                s2[cc + j][rr] = b;
+                unsigned short a0, b0, a1, b1;
+                split1(v[2 * i][j], f, a0, b0);
+                split1(v[2 * i + 1][j], f, a1, b1);
+                *reinterpret_cast<unsigned*>(&s1[cc + j][rr]) = a0 | ((unsigned)a1 << 16);
+                *reinterpret_cast<unsigned*>(&s2[cc + j][rr]) = b0 | ((unsigned)b1 << 16);
             }
         }
         __syncthreads();
@@ -366,7 +369,7 @@ int launch_split_t(cudaStream_t st, int64_t rows, int64_t cols, const float* X, 
                    int num_sms) {
     if (rows <= 0 || cols <= 0) return 0;
     const bool vec = (ld % 4 == 0) && aligned16(X);
-    int64_t tiles = ((rows + TT - 1) / TT) * ((cols + TT - 1) / TT);
+    int64_t tiles = ((rows + 63) / 64) * ((cols + 63) / 64);
     int64_t cap = (int64_t)num_sms * 8;
     int g = (int)(tiles < cap ? tiles : cap);
     if (vec) split_t_kernel<true><<<g, 256, 0, st>>>(X, rows, cols, ld, d_max, hi, lo, ldp, d_sexp);
