@@ -75,6 +75,13 @@ def _load():
             lib.orc_sgemm_sampled.restype = _i64
             lib.orc_sgemm_sampled.argtypes = [_i64, _i64, _i64, _p, _i64, _p, _i64,
                                               _i64, _p, _i64, _p, ctypes.c_int, _p, _p, _p]
+            lib.orc_encbf16.restype = ctypes.c_uint16
+            lib.orc_encbf16.argtypes = [ctypes.c_double]
+            lib.orc_decbf16.restype = ctypes.c_double
+            lib.orc_decbf16.argtypes = [ctypes.c_uint16]
+            lib.orc_encbf16_array.argtypes = [_i64, _p, _p]
+            lib.orc_split_bf16x3.argtypes = [_i64, _i64, _p, _i64, _p, _p, _p, _i64]
+            lib.orc_gemm_bf16x3.argtypes = [_i64, _i64, _i64, _p, _p, _p, _i64, _p, _p, _p, _i64, _p, _i64]
             lib.orc_num_threads.restype = ctypes.c_int
             lib.orc_set_num_threads.argtypes = [ctypes.c_int]
             _lib = lib
@@ -233,6 +240,46 @@ def sgemm_sampled(A, B, rows, cols, terms: int = 3):
     if bad >= 0:
         raise ValueError(f"non-finite entry at index {bad}")
     return out, int(sA[0]), int(sB[0])
+
+
+# ------------------------------------------------------- bf16 x 3 (NEXT #4) ---
+
+def encbf16(x) -> np.ndarray:
+    """RNE fp64 -> bfloat16 bit patterns (uint16), bit by bit."""
+    xd = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty(xd.shape, np.uint16)
+    _load().orc_encbf16_array(xd.size, _ptr(xd), _ptr(out))
+    return out
+
+
+def decbf16(h) -> np.ndarray:
+    h = np.ascontiguousarray(h, dtype=np.uint16)
+    return (h.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def split_bf16x3(X):
+    """(X1, X2, X3) bfloat16 planes (uint16) of a row-major fp32 matrix (no scale)."""
+    X = _f32(X)
+    rows, cols = X.shape
+    p = [np.empty((rows, cols), np.uint16) for _ in range(3)]
+    _load().orc_split_bf16x3(rows, cols, _ptr(X), cols, _ptr(p[0]), _ptr(p[1]), _ptr(p[2]), cols)
+    return tuple(p)
+
+
+def gemm_bf16x3_planes(X, Y):
+    """6-term product of bf16x3 planes X = (X1,X2,X3) (M x K), Y = (Y1,Y2,Y3) (K x N), fp64."""
+    X = [np.ascontiguousarray(v, np.uint16) for v in X]
+    Y = [np.ascontiguousarray(v, np.uint16) for v in Y]
+    M, K = X[0].shape
+    _, N = Y[0].shape
+    C = np.empty((M, N), np.float64)
+    _load().orc_gemm_bf16x3(M, N, K, _ptr(X[0]), _ptr(X[1]), _ptr(X[2]), K, _ptr(Y[0]), _ptr(Y[1]),
+                            _ptr(Y[2]), N, _ptr(C), N)
+    return C
+
+
+def sgemm_bf16x3(A, B):
+    return gemm_bf16x3_planes(split_bf16x3(A), split_bf16x3(B))
 
 
 def num_threads() -> int:

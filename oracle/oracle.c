@@ -319,6 +319,113 @@ int64_t orc_sgemm_sampled(int64_t M, int64_t N, int64_t K,
     return -1;
 }
 
+/* ------------------------------------------------------------------------------
+ * bf16 x 3 split ("the 16-bit bfloat16 format ... has the
+ * advantage of having the same range as fp32"): no scale.  bfloat16 = binary32 with 8
+ * significant bits; RN-even, subnormals kept, overflow -> inf, NaN -> 0x7FC0.
+ *     X1 = RNbf(x),  X2 = RNbf(x - X1),  X3 = RNbf(x - X1 - X2)   (residuals exact in fp64)
+ * Product (6 of the 9 terms, i + j <= 4):  C = X1Y1 + [X1Y2 + X2Y1 + X1Y3 + X2Y2 + X3Y1].
+ * ---------------------------------------------------------------------------- */
+uint16_t orc_encbf16(double x)
+{
+    uint64_t b;
+    memcpy(&b, &x, sizeof b);
+    uint16_t sign = (uint16_t)((b >> 63) << 15);
+    int e = (int)((b >> 52) & 0x7FF);
+    uint64_t mant = b & ((1ULL << 52) - 1);
+    if (e == 0x7FF)
+        return mant ? (uint16_t)0x7FC0 : (uint16_t)(sign | 0x7F80);
+    if (e == 0)
+        return sign;                    /* |x| < 2^-1022: far below the bf16 subnormal range */
+    int E = e - 1023;
+    uint64_t sig = (1ULL << 52) | mant;
+    if (E > 127)
+        return (uint16_t)(sign | 0x7F80);
+    if (E >= -126) {                    /* normal: 8 significant bits */
+        int shift = 52 - 7;
+        uint64_t q = sig >> shift;
+        uint64_t rem = sig & ((1ULL << shift) - 1);
+        uint64_t half = 1ULL << (shift - 1);
+        if (rem > half || (rem == half && (q & 1)))
+            q++;
+        if (q == 256) {
+            q = 128;
+            E++;
+        }
+        if (E > 127)
+            return (uint16_t)(sign | 0x7F80);
+        return (uint16_t)(sign | (uint16_t)((E + 127) << 7) | (uint16_t)(q & 0x7F));
+    }
+    /* subnormal bf16: multiple q of 2^-133;  q = sig * 2^(E - 52 + 133) */
+    int shift = 52 - 133 - E;           /* = -81 - E >= 46 */
+    if (shift > 54)
+        return sign;
+    uint64_t q = sig >> shift;
+    uint64_t rem = sig & ((1ULL << shift) - 1);
+    uint64_t half = 1ULL << (shift - 1);
+    if (rem > half || (rem == half && (q & 1)))
+        q++;
+    return (uint16_t)(sign | (uint16_t)q);
+}
+
+double orc_decbf16(uint16_t h)
+{
+    uint32_t w = (uint32_t)h << 16;
+    float f;
+    memcpy(&f, &w, sizeof f);
+    return (double)f;                   /* bf16 is the top half of binary32: exact */
+}
+
+void orc_encbf16_array(int64_t n, const double *x, uint16_t *h)
+{
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; i++)
+        h[i] = orc_encbf16(x[i]);
+}
+
+void orc_split_bf16x3(int64_t rows, int64_t cols, const float *X, int64_t ld,
+                      uint16_t *p1, uint16_t *p2, uint16_t *p3, int64_t ldp)
+{
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < rows; i++) {
+        for (int64_t j = 0; j < cols; j++) {
+            double x = (double)X[i * ld + j];
+            uint16_t h1 = orc_encbf16(x);
+            double r1 = x - orc_decbf16(h1);
+            uint16_t h2 = orc_encbf16(r1);
+            double r2 = r1 - orc_decbf16(h2);
+            uint16_t h3 = orc_encbf16(r2);
+            p1[i * ldp + j] = h1;
+            p2[i * ldp + j] = h2;
+            p3[i * ldp + j] = h3;
+        }
+    }
+}
+
+/* C = X1Y1 + (X1Y2 + X2Y1 + X1Y3 + X2Y2 + X3Y1), fp64 sums of exact products.
+ * X planes M x K row-major (ldx), Y planes K x N row-major (ldy). */
+void orc_gemm_bf16x3(int64_t M, int64_t N, int64_t K,
+                     const uint16_t *X1, const uint16_t *X2, const uint16_t *X3, int64_t ldx,
+                     const uint16_t *Y1, const uint16_t *Y2, const uint16_t *Y3, int64_t ldy,
+                     double *C, int64_t ldc)
+{
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < M; i++) {
+        for (int64_t j = 0; j < N; j++) {
+            double hi = 0.0, rest = 0.0;
+            for (int64_t k = 0; k < K; k++) {
+                double x1 = orc_decbf16(X1[i * ldx + k]), x2 = orc_decbf16(X2[i * ldx + k]),
+                       x3 = orc_decbf16(X3[i * ldx + k]);
+                double y1 = orc_decbf16(Y1[k * ldy + j]), y2 = orc_decbf16(Y2[k * ldy + j]),
+                       y3 = orc_decbf16(Y3[k * ldy + j]);
+                hi += x1 * y1;
+                rest += x1 * y2 + x2 * y1 + x1 * y3 + x2 * y2 + x3 * y1;
+            }
+            C[i * ldc + j] = hi + rest;
+        }
+    }
+}
+
 int orc_num_threads(void)
 {
 #ifdef _OPENMP
