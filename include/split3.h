@@ -51,7 +51,11 @@ typedef enum split3_status {
 #define SPLIT3_FOUR_TERM    (1u << 0)  /* keep the dropped 2^-22 A2B2 term (Eq. A_2 in full) */
 #define SPLIT3_CHECK_FINITE (1u << 1)  /* synchronise; reject NaN/Inf inputs */
 #define SPLIT3_ONE_TERM     (1u << 2)  /* control: a1b1 * A1B1 only (a scaled plain FP16 GEMM) */
-#define SPLIT3_FLAGS_MASK   (SPLIT3_FOUR_TERM | SPLIT3_CHECK_FINITE | SPLIT3_ONE_TERM)
+#define SPLIT3_BF16X3       (1u << 3)  /* variant: x = X1 + X2 + X3 in bfloat16 (no
+                                          scale), C = X1Y1 + (X1Y2 + X2Y1 + X1Y3 + X2Y2
+                                          + X3Y1): 6 BF16 products; fp32 operands only (no pre-split);
+                                          |x| >= 3.39e38 overflows bf16 */
+#define SPLIT3_FLAGS_MASK   (SPLIT3_FOUR_TERM | SPLIT3_CHECK_FINITE | SPLIT3_ONE_TERM | SPLIT3_BF16X3)
 
 /* ---- handle ------------------------------------------------------------------------ */
 
@@ -155,6 +159,11 @@ int split3_maxabs(split3_handle_t h, int64_t rows, int64_t cols, const float *X,
 int split3_split(split3_handle_t h, int64_t rows, int64_t cols, const float *X, int64_t ldx,
                  const float *d_maxabs, uint16_t *hi, uint16_t *lo, int64_t ldp, int transpose,
                  int32_t *d_sexp);
+
+/* bf16 x 3 planes of X (SPLIT3_BF16X3's split, no scale): p1..p3 rows x cols (transpose = 0) or
+ * cols x rows (transpose = 1), bfloat16 bit patterns, ldp a multiple of 8, 16-byte aligned. */
+int split3_split_bf16x3(split3_handle_t h, int64_t rows, int64_t cols, const float *X, int64_t ldx,
+                        uint16_t *p1, uint16_t *p2, uint16_t *p3, int64_t ldp, int transpose);
 
 /* GEMM from planes: A1, A2 are M x K (K-major, ldpa), B1t, B2t are N x K (K-major, ldpb),
  * i.e. the planes of B TRANSPOSED.  *d_sA, *d_sB are the device scale exponents.  Computes

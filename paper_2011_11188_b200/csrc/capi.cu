@@ -109,9 +109,33 @@ size_t ws_bytes_for(int64_t M, int64_t N, int64_t K, bool planesA, bool planesB,
 
 size_t ws_size(int64_t M, int64_t N, int64_t K) { return ws_bytes_for(M, N, K, true, true, 3); }
 
+// bf16 x 3: three planes per operand (scalars block as usual; sA = sB stay 0: no scale)
+struct CarveBF3 {
+    uint16_t *A[3], *B[3];
+    int64_t ldp;
+    size_t end;
+};
+CarveBF3 carve_bf3(void* ws, int64_t M, int64_t N, int64_t K) {
+    CarveBF3 c;
+    uint8_t* b = static_cast<uint8_t*>(ws);
+    c.ldp = plane_ld(K);
+    size_t off = kScalarBytes;
+    const size_t pa = align256((size_t)M * (size_t)c.ldp * 2), pb = align256((size_t)N * (size_t)c.ldp * 2);
+    for (int i = 0; i < 3; i++) { c.A[i] = reinterpret_cast<uint16_t*>(b + off); off += pa; }
+    for (int i = 0; i < 3; i++) { c.B[i] = reinterpret_cast<uint16_t*>(b + off); off += pb; }
+    c.end = off;
+    return c;
+}
+size_t ws_bytes_bf3(int64_t M, int64_t N, int64_t K, bool partials) {
+    size_t b = kScalarBytes + 3 * align256((size_t)M * (size_t)plane_ld(K) * 2) + 3 * align256((size_t)N * (size_t)plane_ld(K) * 2);
+    if (partials) b += align256((size_t)split3::gemm3_partial_elems(split3::gemm3_split_plan(M, N, K, 6, 148, 0), 6) * 4);
+    return b;
+}
+
 inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
 inline int terms_of(uint32_t flags) {
+    if (flags & SPLIT3_BF16X3) return 6;
     if (flags & SPLIT3_ONE_TERM) return 1;
     if (flags & SPLIT3_FOUR_TERM) return 4;
     return 3;
@@ -182,6 +206,8 @@ int split3_sgemm_destroy(split3_handle_t h) {
 }
 
 size_t split3_sgemm_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags) {
+    if (M < 0 || N < 0 || K < 0) return 0;
+    if (flags & SPLIT3_BF16X3) return ws_bytes_bf3(M, N, K, true);
     return ws_bytes_for(M, N, K, true, true, terms_of(flags));
 }
 
@@ -224,6 +250,21 @@ int split3_split(split3_handle_t h, int64_t rows, int64_t cols, const float* X, 
     int n = transpose
                 ? split3::launch_split_t(h->stream, rows, cols, X, ldx, d_maxabs, hi, lo, ldp, d_sexp, h->num_sms)
                 : split3::launch_split(h->stream, rows, cols, X, ldx, d_maxabs, hi, lo, ldp, d_sexp, h->num_sms);
+    if (n < 0) return SPLIT3_ERR_CUDA;
+    h->last_launches = n;
+    return SPLIT3_OK;
+}
+
+int split3_split_bf16x3(split3_handle_t h, int64_t rows, int64_t cols, const float* X, int64_t ldx,
+                        uint16_t* p1, uint16_t* p2, uint16_t* p3, int64_t ldp, int transpose) {
+    if (!h || rows < 0 || cols < 0 || (transpose != 0 && transpose != 1)) return SPLIT3_ERR_INVALID_VALUE;
+    if (rows == 0 || cols == 0) return SPLIT3_OK;
+    const int64_t need = transpose ? rows : cols;
+    if (!X || !p1 || !p2 || !p3 || ldx < cols || ldp < need || ldp % 8 || !aligned(p1, 16) || !aligned(p2, 16) ||
+        !aligned(p3, 16))
+        return SPLIT3_ERR_INVALID_VALUE;
+    if (set_dev(h)) return SPLIT3_ERR_CUDA;
+    int n = split3::launch_split_bf16x3(h->stream, rows, cols, X, ldx, p1, p2, p3, ldp, transpose, h->num_sms);
     if (n < 0) return SPLIT3_ERR_CUDA;
     h->last_launches = n;
     return SPLIT3_OK;
@@ -292,11 +333,73 @@ static bool operand_ok(const split3_matrix* X, int64_t opr, int64_t opc, int rol
     return X->ld >= (stored_cols > 1 ? stored_cols : 1);
 }
 
+// bf16 x 3 variant of split3_sgemm_ex (NEXT #4): fp32 operands only, no scale pass.
+static int sgemm_bf16x3(split3_ctx* h, int64_t M, int64_t N, int64_t K, const split3_matrix* A,
+                        const split3_matrix* B, float* C, int64_t ldc, uint32_t flags) {
+    if (A->hi || B->hi) return SPLIT3_ERR_NOT_IMPLEMENTED;     // pre-split planes are FP16 x 2
+    if (h->ws_bytes < ws_bytes_bf3(M, N, K, false)) return SPLIT3_ERR_WORKSPACE;
+    CarveBF3 w = carve_bf3(h->ws, M, N, K);
+    Carve sc = carve(h->ws, M, N, K);    // the scalars block (sA = sB = 0, bad indices)
+    if (cudaMemsetAsync(h->ws, 0, 32, h->stream) != cudaSuccess) return SPLIT3_ERR_CUDA;
+    int launches = 0, n;
+    if (flags & SPLIT3_CHECK_FINITE) {
+        if (cudaMemsetAsync(sc.badA, 0xFF, 16, h->stream) != cudaSuccess ||
+            cudaMemsetAsync(reinterpret_cast<uint8_t*>(sc.badA) + 7, 0x7F, 1, h->stream) != cudaSuccess ||
+            cudaMemsetAsync(reinterpret_cast<uint8_t*>(sc.badB) + 7, 0x7F, 1, h->stream) != cudaSuccess)
+            return SPLIT3_ERR_CUDA;
+        const int64_t ra = A->trans ? K : M, ca = A->trans ? M : K, rb = B->trans ? N : K, cb = B->trans ? K : N;
+        if ((n = split3::launch_maxabs(h->stream, ra, ca, A->data, A->ld, sc.maxA, sc.badA, h->num_sms)) < 0 ||
+            (launches += n, n = split3::launch_maxabs(h->stream, rb, cb, B->data, B->ld, sc.maxB, sc.badB, h->num_sms)) < 0)
+            return SPLIT3_ERR_CUDA;
+        launches += n;
+        long long bad[2];
+        if (cudaMemcpyAsync(bad, sc.badA, 16, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
+            cudaStreamSynchronize(h->stream) != cudaSuccess)
+            return SPLIT3_ERR_CUDA;
+        if (bad[0] != INT64_MAX || bad[1] != INT64_MAX) {
+            h->last_bad = bad[0] != INT64_MAX ? bad[0] : M * K + bad[1];
+            h->last_launches = launches;
+            return SPLIT3_ERR_NOT_FINITE;
+        }
+    }
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+    if (h->timing && h->ev_used + 3 <= 3 * 4096) {
+        ev0 = next_event(h); ev1 = next_event(h); ev2 = next_event(h);
+        if (!ev0 || !ev1 || !ev2) return SPLIT3_ERR_CUDA;
+        record(h, ev0);
+    }
+    {   // role A: planes M x K (transposing split iff transA); role B: planes N x K (iff !transB)
+        const int64_t ra = A->trans ? K : M, ca = A->trans ? M : K;
+        if ((n = split3::launch_split_bf16x3(h->stream, ra, ca, A->data, A->ld, w.A[0], w.A[1], w.A[2], w.ldp,
+                                             A->trans, h->num_sms)) < 0)
+            return SPLIT3_ERR_CUDA;
+        launches += n;
+        const int64_t rb = B->trans ? N : K, cb = B->trans ? K : N;
+        if ((n = split3::launch_split_bf16x3(h->stream, rb, cb, B->data, B->ld, w.B[0], w.B[1], w.B[2], w.ldp,
+                                             !B->trans, h->num_sms)) < 0)
+            return SPLIT3_ERR_CUDA;
+        launches += n;
+    }
+    record(h, ev1);
+    float* partial = reinterpret_cast<float*>(static_cast<uint8_t*>(h->ws) + w.end);
+    size_t reserved = ws_bytes_bf3(M, N, K, true) - w.end;
+    if (reserved > h->ws_bytes - w.end) reserved = h->ws_bytes - w.end;
+    int err = 0;
+    n = split3::launch_gemm3(h->stream, M, N, K, w.A[0], w.A[1], w.ldp, sc.sA, w.B[0], w.B[1], w.ldp, sc.sB, C, ldc,
+                             6, h->num_sms, h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune, partial,
+                             (int64_t)(reserved / 4), &err, w.A[2], w.B[2]);
+    if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
+    record(h, ev2);
+    h->last_launches = launches + n;
+    return SPLIT3_OK;
+}
+
 int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const split3_matrix* A,
                     const split3_matrix* B, float* C, int64_t ldc, uint32_t flags) {
     if (!h || M < 0 || N < 0 || K < 0 || !A || !B) return SPLIT3_ERR_INVALID_VALUE;
     if (flags & ~SPLIT3_FLAGS_MASK) return SPLIT3_ERR_INVALID_VALUE;
     if ((flags & SPLIT3_ONE_TERM) && (flags & SPLIT3_FOUR_TERM)) return SPLIT3_ERR_INVALID_VALUE;
+    if ((flags & SPLIT3_BF16X3) && (flags & (SPLIT3_ONE_TERM | SPLIT3_FOUR_TERM))) return SPLIT3_ERR_INVALID_VALUE;
     h->last_launches = 0;
     h->last_bad = -1;
     if (M == 0 || N == 0) return SPLIT3_OK;
@@ -311,6 +414,7 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
         return SPLIT3_OK;
     }
     if (!h->ws || h->ws_bytes < kScalarBytes) return SPLIT3_ERR_WORKSPACE;
+    if (flags & SPLIT3_BF16X3) return sgemm_bf16x3(h, M, N, K, A, B, C, ldc, flags);
     const bool needA = A->hi == nullptr, needB = B->hi == nullptr;
     const size_t need = ws_bytes_for(M, N, K, needA, needB, 0);
     if (h->ws_bytes < need) return SPLIT3_ERR_WORKSPACE;
@@ -545,7 +649,7 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
     float* dA = reinterpret_cast<float*>(base);
     float* dB = reinterpret_cast<float*>(base + align256((size_t)M * K * 4));
     float* dC = reinterpret_cast<float*>(base + align256((size_t)M * K * 4) + align256((size_t)K * N * 4));
-    if (K == 0 || (flags & SPLIT3_CHECK_FINITE)) {   // serial path
+    if (K == 0 || (flags & (SPLIT3_CHECK_FINITE | SPLIT3_BF16X3))) {   // serial path
         if (K > 0 &&
             (cudaMemcpyAsync(dA, A_host, (size_t)M * K * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
              cudaMemcpyAsync(dB, B_host, (size_t)K * N * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess))

@@ -185,9 +185,9 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
 }
 
 // Instruction descriptor, kind::f16: A = B = F16, D = F32, both K-major, M x N.
-__host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
+__host__ __device__ constexpr uint32_t make_idesc(int m, int n, bool bf16 = false) {
     return (1u << 4)                              // D format F32
-         | (0u << 7) | (0u << 10)                 // A, B format F16
+         | ((bf16 ? 1u : 0u) << 7) | ((bf16 ? 1u : 0u) << 10)   // A, B format F16 (0) / BF16 (1)
          | (0u << 15) | (0u << 16)                // A, B K-major
          | ((uint32_t)(n >> 3) << 17)             // N >> 3
          | ((uint32_t)(m >> 4) << 24);            // M >> 4
@@ -224,12 +224,13 @@ __device__ __forceinline__ void decode_unit(int64_t u, const SplitPlan& p, int n
     slot = (int)v;   // = s * nsplit + t
 }
 
-// Tile geometry per instantiation: BN_ = 256 (3-term, 1-term) or 128 (4-term: D_lo needs TMEM).
-template <int BN_>
+// Tile geometry per instantiation: BN_ = 256 (3-term, 1-term, bf16x3) or 128 (4-term: D_lo
+// needs TMEM); PL = planes per operand (2, or 3 for bf16x3).
+template <int BN_, int PL = 2>
 struct Geo {
     static constexpr int BNH = BN_ / 2;                               // B^T rows loaded per CTA
     static constexpr int TILE_B_BYTES = BNH * BK * 2;
-    static constexpr int STAGE_BYTES = 2 * TILE_A_BYTES + 2 * TILE_B_BYTES;
+    static constexpr int STAGE_BYTES = PL * TILE_A_BYTES + PL * TILE_B_BYTES;
     static constexpr int STAGES = (220 * 1024) / STAGE_BYTES > 6 ? 6 : (220 * 1024) / STAGE_BYTES;
     static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
@@ -251,11 +252,14 @@ template <int TERMS, int BN_>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapA2,
              const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
+             const __grid_constant__ CUtensorMap mapA3, const __grid_constant__ CUtensorMap mapB3,
              int M, int N, int K, int promo_kb, const int32_t* __restrict__ d_sA,
              const int32_t* __restrict__ d_sB, float* __restrict__ C, int64_t ldc,
              unsigned* __restrict__ wave_counter, const GemmTune tune, const SplitPlan plan,
              float* __restrict__ partial) {
-    using G = Geo<BN_>;
+    constexpr bool BF3 = TERMS == 6;                 // bf16 x 3 split (NEXT #4): 3 planes, 6 products
+    constexpr int PL = BF3 ? 3 : 2;
+    using G = Geo<BN_, PL>;
     constexpr int STAGES = G::STAGES;
     constexpr int STAGE_BYTES = G::STAGE_BYTES;
     constexpr int TILE_B_BYTES = G::TILE_B_BYTES;
@@ -268,7 +272,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     constexpr uint32_t COL_LO = COL_MID + BN_;
     static_assert(HB * BN_ + (HAS_MID ? BN_ : 0) + (TERMS == 4 ? BN_ : 0) <= 512, "TMEM budget");
     constexpr uint32_t TX_BYTES = 2u * (LOAD_LO ? STAGE_BYTES : TILE_A_BYTES + TILE_B_BYTES);
-    constexpr uint32_t IDESC = make_idesc(2 * BM, BN_);
+    constexpr uint32_t IDESC = make_idesc(2 * BM, BN_, BF3);
+    constexpr int B_OFF = PL * TILE_A_BYTES;         // B planes follow the A planes in a stage
     constexpr int NCOL = BN_ / 2;                    // columns per epilogue warp (2 warps per quadrant)
     constexpr uint32_t EPI_ARRIVALS = 2 * NUM_EPI_WARPS;
 
@@ -301,6 +306,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&mapA1); tma_prefetch(&mapB1);
         if (LOAD_LO) { tma_prefetch(&mapA2); tma_prefetch(&mapB2); }
+        if (BF3) { tma_prefetch(&mapA3); tma_prefetch(&mapB3); }
         for (int i = 0; i < STAGES; i++) {
             mbar_init(smem_u32(&full_bar[i]), 1);
             mbar_init(smem_u32(&empty_bar[i]), 1);
@@ -354,11 +360,14 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                 if (elect_one()) {
                     if (leader) mbar_expect_tx(fb, TX_BYTES);
                     tma_load_2d_pair(smem_u32(st), &mapA1, fb, x, y_a, tune.pol_a);
-                    tma_load_2d_pair(smem_u32(st + 2 * TILE_A_BYTES), &mapB1, fb, x, y_b, tune.pol_b);
+                    tma_load_2d_pair(smem_u32(st + B_OFF), &mapB1, fb, x, y_b, tune.pol_b);
                     if (LOAD_LO) {
                         tma_load_2d_pair(smem_u32(st + TILE_A_BYTES), &mapA2, fb, x, y_a, tune.pol_a);
-                        tma_load_2d_pair(smem_u32(st + 2 * TILE_A_BYTES + TILE_B_BYTES), &mapB2, fb, x, y_b,
-                                         tune.pol_b);
+                        tma_load_2d_pair(smem_u32(st + B_OFF + TILE_B_BYTES), &mapB2, fb, x, y_b, tune.pol_b);
+                    }
+                    if (BF3) {
+                        tma_load_2d_pair(smem_u32(st + 2 * TILE_A_BYTES), &mapA3, fb, x, y_a, tune.pol_a);
+                        tma_load_2d_pair(smem_u32(st + B_OFF + 2 * TILE_B_BYTES), &mapB3, fb, x, y_b, tune.pol_b);
                     }
                 }
                 __syncwarp();
@@ -393,8 +402,10 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     uint8_t* st = smem + stage * STAGE_BYTES;
                     const uint64_t a1 = sdesc_sw128(smem_u32(st));
                     const uint64_t a2 = sdesc_sw128(smem_u32(st + TILE_A_BYTES));
-                    const uint64_t b1 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES));
-                    const uint64_t b2 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES + TILE_B_BYTES));
+                    const uint64_t a3 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES));
+                    const uint64_t b1 = sdesc_sw128(smem_u32(st + B_OFF));
+                    const uint64_t b2 = sdesc_sw128(smem_u32(st + B_OFF + TILE_B_BYTES));
+                    const uint64_t b3 = sdesc_sw128(smem_u32(st + B_OFF + 2 * TILE_B_BYTES));
                     const bool hi_first = kb == kb_begin;
                     auto issue_mid = [&]() {
                         if (!HAS_MID) return;
@@ -411,6 +422,11 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                                 mma_pair(t_mid, a1 + dk, b2 + dk, IDESC, acc);
                                 mma_pair(t_mid, a2 + dk, b1 + dk, IDESC, 1u);
                                 if (TERMS == 4) mma_pair(t_lo, a2 + dk, b2 + dk, IDESC, acc);
+                                if (BF3) {          // the 2^-16-weighted products share D_mid
+                                    mma_pair(t_mid, a1 + dk, b3 + dk, IDESC, 1u);
+                                    mma_pair(t_mid, a2 + dk, b2 + dk, IDESC, 1u);
+                                    mma_pair(t_mid, a3 + dk, b1 + dk, IDESC, 1u);
+                                }
                             }
                         }
                         __syncwarp();
@@ -488,6 +504,11 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                             master[c * 16 + j] = __fmaf_rn(
                                 __fmaf_rn(__uint_as_float(lo[j]), 0x1p-11f, __uint_as_float(mid[j])), 0x1p-11f,
                                 master[c * 16 + j]);
+                    } else if (BF3) {      // bf16 planes carry no scale: C = D_hi + D_mid
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 16; j++)
+                            master[c * 16 + j] = __fadd_rn(master[c * 16 + j], __uint_as_float(mid[j]));
                     } else {
                         tmem_ld_wait();
 #pragma unroll
@@ -607,10 +628,11 @@ bool make_plane_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K,
 
 template <int TERMS, int BN_>
 int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap& a1,
-             const CUtensorMap& a2, const CUtensorMap& b1, const CUtensorMap& b2,
+             const CUtensorMap& a2, const CUtensorMap& b1, const CUtensorMap& b2, const CUtensorMap& a3,
+             const CUtensorMap& b3,
              const int32_t* d_sA, const int32_t* d_sB, float* C, int64_t ldc, int num_sms,
              int promo_kb, unsigned* wave_counter, const GemmTune& tune, const SplitPlan& plan, float* partial) {
-    constexpr int SMEM_BYTES = Geo<BN_>::SMEM;
+    constexpr int SMEM_BYTES = Geo<BN_, TERMS == 6 ? 3 : 2>::SMEM;
     static bool attr_set = false;
     if (!attr_set) {
         if (cudaFuncSetAttribute(gemm3_kernel<TERMS, BN_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -622,7 +644,7 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
     const int64_t pairs = num_sms / 2;
     const int grid = 2 * (int)(tiles < pairs ? tiles : pairs);
     if (wave_counter && cudaMemsetAsync(wave_counter, 0, sizeof(unsigned), st) != cudaSuccess) return -1;
-    gemm3_kernel<TERMS, BN_><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(a1, a2, b1, b2, (int)M, (int)N, (int)K,
+    gemm3_kernel<TERMS, BN_><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(a1, a2, b1, b2, a3, b3, (int)M, (int)N, (int)K,
                                                                promo_kb, d_sA, d_sB, C, ldc, wave_counter,
                                                                tune, plan, partial);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
@@ -667,8 +689,8 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
                  const uint16_t* A2, int64_t ldpa, const int32_t* d_sA, const uint16_t* B1t,
                  const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB, float* C, int64_t ldc,
                  int terms, int num_sms, int promo_kb, unsigned* wave_counter, const GemmTuneIn& tin,
-                 float* partial, int64_t partial_elems, int* err) {
-    CUtensorMap ma1, ma2, mb1, mb2;
+                 float* partial, int64_t partial_elems, int* err, const uint16_t* A3, const uint16_t* B3t) {
+    CUtensorMap ma1, ma2, mb1, mb2, ma3, mb3;
     const uint16_t* A2e = terms == 1 ? A1 : A2;
     const uint16_t* B2e = terms == 1 ? B1t : B2t;
     const int bnh = (terms == 4 ? 128 : 256) / 2;
@@ -677,6 +699,11 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
         *err = 4;   // SPLIT3_ERR_CUDA
         return -1;
     }
+    if (terms == 6 && (!A3 || !B3t || !make_plane_map(&ma3, A3, M, K, ldpa, BM) || !make_plane_map(&mb3, B3t, N, K, ldpb, bnh))) {
+        *err = 4;
+        return -1;
+    }
+    if (terms != 6) { ma3 = ma1; mb3 = mb1; }
     const int promo = promo_kb > 0 ? promo_kb : kDefaultPromoKb;
     GemmTune tune;
     tune.group_m = tin.group_m > 0 ? tin.group_m : kDefaultGroupM;
@@ -691,11 +718,13 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     }
     int r;
     if (terms == 1)
-        r = launch_t<1, 256>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial);
+        r = launch_t<1, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial);
     else if (terms == 4)
-        r = launch_t<4, 128>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial);
+        r = launch_t<4, 128>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial);
+    else if (terms == 6)
+        r = launch_t<6, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial);
     else
-        r = launch_t<3, 256>(st, M, N, K, ma1, ma2, mb1, mb2, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial);
+        r = launch_t<3, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial);
     if (r < 0) { *err = 4; return -1; }
     if (plan.slices > 1) {
         const int bn = terms == 4 ? 128 : 256;

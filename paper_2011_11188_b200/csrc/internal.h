@@ -20,6 +20,9 @@ int launch_maxabs2(cudaStream_t s, int64_t rows0, int64_t cols0, const float* X0
 int launch_split(cudaStream_t s, int64_t rows, int64_t cols, const float* X, int64_t ld,
                  const float* d_max, uint16_t* hi, uint16_t* lo, int64_t ldp, int32_t* d_sexp,
                  int num_sms);
+// bf16 x 3 planes (no scale); transpose as for launch_split_t
+int launch_split_bf16x3(cudaStream_t s, int64_t rows, int64_t cols, const float* X, int64_t ld, uint16_t* p1,
+                        uint16_t* p2, uint16_t* p3, int64_t ldp, int transpose, int num_sms);
 int launch_split_t(cudaStream_t s, int64_t rows, int64_t cols, const float* X, int64_t ld,
                    const float* d_max, uint16_t* hi, uint16_t* lo, int64_t ldp, int32_t* d_sexp,
                    int num_sms);
@@ -51,14 +54,14 @@ struct SplitPlan {
 SplitPlan gemm3_split_plan(int64_t M, int64_t N, int64_t K, int terms, int num_sms, int promo_kb);
 int64_t gemm3_partial_elems(const SplitPlan& p, int terms);   // floats of partial workspace
 
-// terms: 1, 3 or 4.  `partial` (may be NULL: no split-K) holds partial_elems floats.
+// terms: 1, 3, 4, or 6 (= bf16 x 3: planes A1..A3, B1t..B3t, 6 products, no scale).  `partial` (may be NULL: no split-K) holds partial_elems floats.
 // Returns kernels launched (1, or 2 with the split-K reduction) or -1 (*err set to a status).
 int launch_gemm3(cudaStream_t s, int64_t M, int64_t N, int64_t K,
                  const uint16_t* A1, const uint16_t* A2, int64_t ldpa, const int32_t* d_sA,
                  const uint16_t* B1t, const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB,
                  float* C, int64_t ldc, int terms, int num_sms, int promo_kb,
                  unsigned* wave_counter, const GemmTuneIn& tune, float* partial, int64_t partial_elems,
-                 int* err);
+                 int* err, const uint16_t* A3 = nullptr, const uint16_t* B3t = nullptr);
 
 // ---- mlp_kernels.cu (NEXT #3: the non-GEMM steps of a dense-network training step) --------
 int launch_bias_act(cudaStream_t s, int64_t M, int64_t N, const float* Z, int64_t ldz, const float* b, float* H,

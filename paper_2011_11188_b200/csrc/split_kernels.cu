@@ -9,6 +9,7 @@
 //
 // Both are HBM-bound streaming kernels: 4 B/el read for a1; 4 B/el read + 2x2 B/el written
 // for a2.  float4 loads, grids sized in multiples of the SM count, grid-stride loops.
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <climits>
 #include <stdint.h>
@@ -296,6 +297,76 @@ __global__ void __launch_bounds__(256) split_t_kernel(const float* __restrict__ 
     }
 }
 
+// ---- bf16 x 3 split: x = X1 + X2 + X3, X_i = RN_bf16 of the running
+// residual (exact in fp32); no scale (bfloat16 has the range of fp32).
+__device__ __forceinline__ void split_bf3(float x, unsigned short& h1, unsigned short& h2, unsigned short& h3) {
+    __nv_bfloat16 a = __float2bfloat16_rn(x);
+    float r1 = __fsub_rn(x, __bfloat162float(a));
+    __nv_bfloat16 b = __float2bfloat16_rn(r1);
+    float r2 = __fsub_rn(r1, __bfloat162float(b));
+    __nv_bfloat16 c = __float2bfloat16_rn(r2);
+    h1 = __bfloat16_as_ushort(a);
+    h2 = __bfloat16_as_ushort(b);
+    h3 = __bfloat16_as_ushort(c);
+}
+
+// planes rows x cols (ldp), grid-stride over elements (row-major)
+__global__ void __launch_bounds__(256) split_bf3_kernel(const float* __restrict__ X, int64_t rows, int64_t cols,
+                                                        int64_t ld, uint16_t* __restrict__ p1,
+                                                        uint16_t* __restrict__ p2, uint16_t* __restrict__ p3,
+                                                        int64_t ldp) {
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+        for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x) {
+            unsigned short a, b, d;
+            split_bf3(__ldcs(X + r * ld + c), a, b, d);
+            p1[r * ldp + c] = a;
+            p2[r * ldp + c] = b;
+            p3[r * ldp + c] = d;
+        }
+}
+
+// planes cols x rows (transposed, ldp >= rows) through 64 x 64 shared-memory tiles
+__global__ void __launch_bounds__(256) split_bf3_t_kernel(const float* __restrict__ X, int64_t rows, int64_t cols,
+                                                          int64_t ld, uint16_t* __restrict__ p1,
+                                                          uint16_t* __restrict__ p2, uint16_t* __restrict__ p3,
+                                                          int64_t ldp) {
+    __shared__ __align__(16) unsigned short sm[3][64][66];
+    const int t = threadIdx.x;
+    const int64_t ntr = (rows + 63) / 64, ntc = (cols + 63) / 64;
+    for (int64_t tile = blockIdx.x; tile < ntr * ntc; tile += gridDim.x) {
+        const int64_t r0 = (tile % ntr) * 64, c0 = (tile / ntr) * 64;
+#pragma unroll
+        for (int i = 0; i < 16; i++) {          // 64 x 64 elements, 16 per thread, coalesced along X's rows
+            const int rr = (t / 64) + 4 * i, cc = t % 64;
+            const int64_t r = r0 + rr, c = c0 + cc;
+            const float x = (r < rows && c < cols) ? X[r * ld + c] : 0.0f;
+            unsigned short a, b, d;
+            split_bf3(x, a, b, d);
+            sm[0][cc][rr] = a;
+            sm[1][cc][rr] = b;
+            sm[2][cc][rr] = d;
+        }
+        __syncthreads();
+        const int nn = t / 4, kk = 16 * (t % 4);
+        const int64_t n = c0 + nn;
+        if (n < cols) {
+#pragma unroll
+            for (int p = 0; p < 3; p++) {
+                uint16_t* dst = p == 0 ? p1 : (p == 1 ? p2 : p3);
+                const unsigned* src = reinterpret_cast<const unsigned*>(&sm[p][nn][kk]);
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const int64_t k = r0 + kk + 8 * h;
+                    if (k < ldp)
+                        __stcs(reinterpret_cast<uint4*>(dst + n * ldp + k),
+                               make_uint4(src[4 * h], src[4 * h + 1], src[4 * h + 2], src[4 * h + 3]));
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 inline int grid_rows(int64_t rows, int num_sms, int64_t blocks_x) {
@@ -361,6 +432,22 @@ int launch_split(cudaStream_t st, int64_t rows, int64_t cols, const float* X, in
     dim3 grid((unsigned)bx, (unsigned)grid_rows(rows, num_sms, bx));
     if (vec) split_kernel<true><<<grid, 256, 0, st>>>(X, rows, cols, ld, d_max, hi, lo, ldp, d_sexp);
     else split_kernel<false><<<grid, 256, 0, st>>>(X, rows, cols, ld, d_max, hi, lo, ldp, d_sexp);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_split_bf16x3(cudaStream_t st, int64_t rows, int64_t cols, const float* X, int64_t ld, uint16_t* p1,
+                        uint16_t* p2, uint16_t* p3, int64_t ldp, int transpose, int num_sms) {
+    if (rows <= 0 || cols <= 0) return 0;
+    if (transpose) {
+        int64_t tiles = ((rows + 63) / 64) * ((cols + 63) / 64);
+        int64_t cap = (int64_t)num_sms * 8;
+        split_bf3_t_kernel<<<(unsigned)(tiles < cap ? tiles : cap), 256, 0, st>>>(X, rows, cols, ld, p1, p2, p3, ldp);
+    } else {
+        int64_t bx = (cols + 255) / 256;
+        if (bx > 64) bx = 64;
+        dim3 grid((unsigned)bx, (unsigned)grid_rows(rows, num_sms, bx));
+        split_bf3_kernel<<<grid, 256, 0, st>>>(X, rows, cols, ld, p1, p2, p3, ldp);
+    }
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -29,6 +29,7 @@ THREE_TERM = 0
 FOUR_TERM = 1 << 0
 CHECK_FINITE = 1 << 1
 ONE_TERM = 1 << 2
+BF16X3 = 1 << 3
 
 # every symbol include/split3.h declares (checked by tests/test_capi.py)
 EXPORTS = (
@@ -38,7 +39,7 @@ EXPORTS = (
     "split3_status_string", "split3_maxabs", "split3_split", "split3_gemm_planes",
     "split3_last_launch_count", "split3_timing_enable", "split3_timing_read",
     "split3_set_promotion", "split3_set_wave_sync", "split3_set_schedule",
-    "split3_sgemm_ex", "split3_presplit", "split3_bias_act", "split3_relu_backward",
+    "split3_sgemm_ex", "split3_presplit", "split3_split_bf16x3", "split3_bias_act", "split3_relu_backward",
     "split3_softmax_xent", "split3_bias_grad", "split3_sgd_update",
 )
 
@@ -111,6 +112,7 @@ def load() -> ctypes.CDLL:
         lib.split3_set_schedule.argtypes = [_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         lib.split3_sgemm_ex.argtypes = [_p, _i64, _i64, _i64, ctypes.POINTER(split3_matrix),
                                         ctypes.POINTER(split3_matrix), _p, _i64, ctypes.c_uint32]
+        lib.split3_split_bf16x3.argtypes = [_p, _i64, _i64, _p, _i64, _p, _p, _p, _i64, ctypes.c_int]
         lib.split3_bias_act.argtypes = [_p, _i64, _i64, _p, _i64, _p, _p, _i64, ctypes.c_int]
         lib.split3_relu_backward.argtypes = [_p, _i64, _i64, _p, _p, _p]
         lib.split3_softmax_xent.argtypes = [_p, _i64, _i64, _p, _p, _p, _p, _p, _p]
@@ -139,8 +141,8 @@ def plane_ld(k: int) -> int:
     return (k + 7) // 8 * 8
 
 
-def _flags(four_term: bool, one_term: bool, check_finite: bool) -> int:
-    f = 0
+def _flags(four_term: bool, one_term: bool, check_finite: bool, bf16x3: bool = False) -> int:
+    f = BF16X3 if bf16x3 else 0
     if four_term:
         f |= FOUR_TERM
     if one_term:
@@ -228,7 +230,8 @@ class Handle:
 
     # -- the whole method ---------------------------------------------------------
     def sgemm(self, A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None,
-              four_term: bool = False, one_term: bool = False, check_finite: bool = False):
+              four_term: bool = False, one_term: bool = False, check_finite: bool = False,
+              bf16x3: bool = False):
         """C = A @ B (fp32, row-major; leading-dimension strides allowed)."""
         _check_mat(A, "A")
         _check_mat(B, "B")
@@ -239,7 +242,7 @@ class Handle:
         if out is None:
             out = torch.empty((M, N), dtype=torch.float32, device=A.device)
         _check_mat(out, "C")
-        flags = _flags(four_term, one_term, check_finite)
+        flags = _flags(four_term, one_term, check_finite, bf16x3)
         self._ensure_ws(self.workspace_size(M, N, K, flags))
         self._bind_stream()
         st = self._lib.split3_sgemm(self._h, M, N, K, _ptr(A), _ld(A), _ptr(B), _ld(B),
@@ -267,7 +270,8 @@ class Handle:
         return Planes(hi, lo, sexp, role, rows, cols)
 
     def sgemm_ex(self, A, B, transA: bool = False, transB: bool = False, out=None,
-                 four_term: bool = False, one_term: bool = False, check_finite: bool = False):
+                 four_term: bool = False, one_term: bool = False, check_finite: bool = False,
+                 bf16x3: bool = False):
         """C = op(A) @ op(B); A / B are fp32 CUDA tensors or Planes from presplit()."""
         def desc(X, trans, role, name):
             if isinstance(X, Planes):
@@ -287,7 +291,7 @@ class Handle:
         if out is None:
             out = torch.empty((M, N), dtype=torch.float32, device=dev)
         _check_mat(out, "C")
-        flags = _flags(four_term, one_term, check_finite)
+        flags = _flags(four_term, one_term, check_finite, bf16x3)
         self._ensure_ws(self.workspace_size(M, N, K, flags))
         self._bind_stream()
         st = self._lib.split3_sgemm_ex(self._h, M, N, K, ctypes.byref(da), ctypes.byref(db),
@@ -402,6 +406,20 @@ class Handle:
             raise Split3Error(st, "split3_split")
         return hi, lo, d_sexp
 
+    def split_bf16x3(self, X: torch.Tensor, transpose: bool = False):
+        """bf16 x 3 planes (int16 tensors holding bfloat16 bits) of X, padded leading dimension."""
+        _check_mat(X, "X")
+        rows, cols = X.shape
+        prow, pcol = (cols, rows) if transpose else (rows, cols)
+        ldp = plane_ld(pcol)
+        ps = [torch.empty((prow, ldp), dtype=torch.int16, device=X.device) for _ in range(3)]
+        self._bind_stream()
+        st = self._lib.split3_split_bf16x3(self._h, rows, cols, _ptr(X), _ld(X), *[_ptr(p) for p in ps], ldp,
+                                           int(transpose))
+        if st != OK:
+            raise Split3Error(st, "split3_split_bf16x3")
+        return ps
+
     def gemm_planes(self, M, N, K, A1, A2, d_sA, B1t, B2t, d_sB, out=None,
                     four_term=False, one_term=False):
         """C from planes: A1/A2 M x ldp, B1t/B2t N x ldp (K-major), device scale exponents."""
@@ -444,7 +462,7 @@ def handle(device=None) -> Handle:
     return h
 
 
-def sgemm(A, B, out=None, four_term=False, one_term=False, check_finite=False):
+def sgemm(A, B, out=None, four_term=False, one_term=False, check_finite=False, bf16x3=False):
     """C = A @ B emulated with FP16 tensor-core GEMMs (arXiv 2011.11188, Appendix A)."""
     return handle(A.device).sgemm(A, B, out=out, four_term=four_term, one_term=one_term,
-                                  check_finite=check_finite)
+                                  check_finite=check_finite, bf16x3=bf16x3)

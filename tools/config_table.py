@@ -41,6 +41,7 @@ CONFIGS = [("D1 N=64", 64, 64, 64, "uniform", "uniform", 3)]
 for n in (4096, 16384):
     for t in (3, 4):
         CONFIGS.append((f"D2 N={n}", n, n, n, "uniform", "uniform", t))
+    CONFIGS.append((f"NEXT#4 bf16x3 N={n}", n, n, n, "uniform", "uniform", 6))
 for M in (256, 1024, 4096):
     for KN in (1024, 4096, 8192):
         CONFIGS.append((f"D3 dense M={M}", M, KN, KN, "uniform", "glorot", 3))
@@ -58,6 +59,8 @@ for name, M, N, K, ka, kb, terms in CONFIGS:
     if "pre-split" in name:
         Wp = h.presplit(B, role=1)
         call = lambda: h.sgemm_ex(A, Wp, out=C)    # noqa: E731
+    elif terms == 6:
+        call = lambda: h.sgemm(A, B, out=C, bf16x3=True)   # noqa: E731
     else:
         call = lambda: h.sgemm(A, B, out=C, four_term=four)   # noqa: E731
     call()
