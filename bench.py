@@ -330,8 +330,9 @@ def main():
 
     # roofline of the dominant kernel (the tcgen05 GEMM): algorithmic FP16 FLOPs per launch
     n_prod = {3: 3, 4: 4, 1: 1}[args.terms]
-    gemm_avg_ms = gemm_ms / max(ncalls, 1)
-    achieved = n_prod * 2.0 * M_loc * N_loc * K / (gemm_avg_ms / 1e3) / 1e12 if ncalls else None
+    # per STEP (the 2-D driver issues one GEMM launch per row block of the rank's tile)
+    gemm_step_ms = gemm_ms / args.steps
+    achieved = n_prod * 2.0 * M_loc * N_loc * K / (gemm_step_ms / 1e3) / 1e12 if ncalls else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "gemm3_traffic.json")
     if os.path.exists(prof):
@@ -347,9 +348,10 @@ def main():
                 "peak_src": f"{pk['src']} bf16_tflops_sustained (fp16 = bf16 nominal rate)",
                 "frac_of_burst": (achieved / pk["tc_burst"]) if achieved else None,
                 "gemm_share_of_step": gemm_ms / max(t_ms, 1e-9) if ncalls else None,
-                "split_ms_per_step": split_ms / max(ncalls, 1),
-                "split_hbm_gbs": (12.0 * 2 * n * n / (split_ms / max(ncalls, 1) / 1e3) / 1e9)
-                if ncalls and split_ms > 0 else None}
+                "gemm_launches_per_step": ncalls / args.steps,
+                "split_ms_per_step": split_ms / args.steps if world == 1 else None,
+                "split_hbm_gbs": (12.0 * 2 * n * n / (split_ms / args.steps / 1e3) / 1e9)
+                if ncalls and split_ms > 0 and world == 1 else None}
 
     # e2e through the C-ABI with HOST buffers (H2D of A, B and D2H of C inside the timed region)
     e2e = None
@@ -373,6 +375,34 @@ def main():
         e2e = {"value": 2.0 * n ** 3 / (te / 1e3) / 1e12, "unit": "TFLOPS",
                "h2d_bytes_per_step": 2 * n * n * 4, "d2h_bytes_per_step": n * n * 4,
                "ms_per_step": te, "api": "split3_sgemm_host (pinned host buffers)"}
+    elif not args.no_e2e:
+        # each rank: its A and B blocks from pinned host memory -> sgemm_2d -> its C tile to host
+        Ah = tg.A_blk.cpu().pin_memory()
+        Bh = tg.B_blk.cpu().pin_memory()
+        Ch = torch.empty(tuple(tg.C.shape), dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            tg.A_blk.copy_(Ah, non_blocking=True)
+            tg.B_blk.copy_(Bh, non_blocking=True)
+            tg.run()
+            Ch.copy_(tg.C, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        x1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([x0.elapsed_time(x1) / args.e2e_steps], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        te = float(t.item())
+        e2e = {"value": 2.0 * n ** 3 * world / (te / 1e3) / 1e12, "unit": "TFLOPS",
+               "h2d_bytes_per_step": int(Ah.numel() + Bh.numel()) * 4 * world,
+               "d2h_bytes_per_step": int(Ch.numel()) * 4 * world, "ms_per_step": te,
+               "api": "paper_2011_11188_b200.dist.sgemm_2d (pinned host blocks, max over ranks)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
