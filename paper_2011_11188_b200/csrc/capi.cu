@@ -12,6 +12,11 @@
 #include "../../include/split3.h"
 #include "internal.h"
 
+// handle-owned device scratch: [0] wave counter, [4] max-abs ticket, [16] presplit max,
+// [64..] max-abs block partials (2 x kMaxPartials floats)
+constexpr size_t kMaxPartials = 2048;
+constexpr size_t kCounterBytes = 64 + 2 * kMaxPartials * 4;
+
 struct split3_ctx {
     int device = 0;
     int num_sms = 148;
@@ -23,6 +28,7 @@ struct split3_ctx {
     int promo_kb = 0;   // 0 = library default
     int wave_sync = 1;  // GEMM wave lockstep hint (L2 locality)
     split3::GemmTuneIn tune;
+    unsigned wave_base = 0;           // running value of the device wave counter (d_counters[0])
     unsigned* d_counters = nullptr;   // 256 B of device scratch owned by the handle
     // host-buffer entry: copy-in / copy-out streams and events, created on first use
     cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -176,10 +182,12 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
     c->stream = static_cast<cudaStream_t>(cuda_stream);
-    if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(&c->d_counters, 256) != cudaSuccess) {
+    if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(&c->d_counters, kCounterBytes) != cudaSuccess ||
+        cudaMemset(c->d_counters, 0, kCounterBytes) != cudaSuccess) {
         delete c;
         return SPLIT3_ERR_CUDA;
     }
+    c->tune.wave_base = &c->wave_base;
     *h = c;
     return SPLIT3_OK;
 }
@@ -420,8 +428,10 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     if (h->ws_bytes < need) return SPLIT3_ERR_WORKSPACE;
     Carve w = carve(h->ws, M, N, K);
     const bool check = (flags & SPLIT3_CHECK_FINITE) != 0;
-    // scalars: maxA = maxB = 0.0f, sA = sB = 0, badA = badB = INT64_MAX
-    if (cudaMemsetAsync(h->ws, 0, 32, h->stream) != cudaSuccess) return SPLIT3_ERR_CUDA;
+    // scalars: maxA = maxB = 0.0f, sA = sB = 0, badA = badB = INT64_MAX.  The common path (both
+    // operands fp32, no check) needs no reset: the two-matrix max-abs writes maxA/maxB itself.
+    const bool fast_max = needA && needB && !check;
+    if (!fast_max && cudaMemsetAsync(h->ws, 0, 32, h->stream) != cudaSuccess) return SPLIT3_ERR_CUDA;
     int launches = 0, n;
     if (check) {
         if (cudaMemsetAsync(w.badA, 0xFF, 16, h->stream) != cudaSuccess ||
@@ -436,11 +446,13 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
         record(h, ev0);
     }
     // a1: per-matrix max-abs (reading R1) of the fp32 operands (max|op(X)| = max|X|)
-    if (needA && needB && !check) {
+    if (fast_max) {
         const int64_t ra = A->trans ? K : M, ca = A->trans ? M : K;
         const int64_t rb = B->trans ? N : K, cb = B->trans ? K : N;
+        float* parts = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(h->d_counters) + 64);
+        unsigned* ticket = h->d_counters + 1;
         if ((n = split3::launch_maxabs2(h->stream, ra, ca, A->data, A->ld, w.maxA, rb, cb, B->data, B->ld, w.maxB,
-                                        h->num_sms)) < 0)
+                                        h->num_sms, parts, (int)kMaxPartials, ticket)) < 0)
             return SPLIT3_ERR_CUDA;
         launches += n;
     } else if (needA) {
@@ -520,7 +532,7 @@ int split3_presplit(split3_handle_t h, int role, int64_t rows, int64_t cols, con
         return SPLIT3_ERR_INVALID_VALUE;
     (void)prow;
     if (set_dev(h)) return SPLIT3_ERR_CUDA;
-    float* d_max = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(h->d_counters) + 64);
+    float* d_max = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(h->d_counters) + 16);
     if (cudaMemsetAsync(d_max, 0, 4, h->stream) != cudaSuccess) return SPLIT3_ERR_CUDA;
     int launches = 0;
     const int64_t sr = trans ? cols : rows, sc = trans ? rows : cols;

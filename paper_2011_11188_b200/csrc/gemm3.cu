@@ -74,13 +74,14 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // i-th tile, then waits — at most kWaveWaitNs — until all CTAs that have an i-th tile did.  A
 // performance hint only: the bounded wait can never deadlock (e.g. if not all CTAs are resident).
 constexpr uint64_t kWaveWaitNs = 200000;
+// The counter is never reset: launches continue from the base the host tracks (wrap-safe).
 __device__ __forceinline__ void wave_sync(unsigned* counter, unsigned target) {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
     const uint64_t t0 = globaltimer_ns();
     unsigned v;
     do {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
-        if (v >= target) break;
+        if ((int)(v - target) >= 0) break;
         __nanosleep(64);
     } while (globaltimer_ns() - t0 < kWaveWaitNs);
 }
@@ -255,8 +256,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
              const __grid_constant__ CUtensorMap mapA3, const __grid_constant__ CUtensorMap mapB3,
              int M, int N, int K, int promo_kb, const int32_t* __restrict__ d_sA,
              const int32_t* __restrict__ d_sB, float* __restrict__ C, int64_t ldc,
-             unsigned* __restrict__ wave_counter, const GemmTune tune, const SplitPlan plan,
-             float* __restrict__ partial) {
+             unsigned* __restrict__ wave_counter, unsigned wave_base, const GemmTune tune,
+             const SplitPlan plan, float* __restrict__ partial) {
     constexpr bool BF3 = TERMS == 6;                 // bf16 x 3 split (NEXT #4): 3 planes, 6 products
     constexpr int PL = BF3 ? 3 : 2;
     using G = Geo<BN_, PL>;
@@ -335,7 +336,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         // ===================== TMA producer (both CTAs; warp-uniform, one elected lane) =====
         int stage = 0;
         uint32_t phase = 0;
-        unsigned wave_target = 0;   // cumulative arrivals expected up to this tile index
+        unsigned wave_target = wave_base;   // cumulative arrivals expected up to this unit index
         int64_t idx = 0;
         for (int64_t unit = pair; unit < num_units; unit += num_pairs, idx++) {
             int64_t tile;
@@ -631,7 +632,8 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
              const CUtensorMap& a2, const CUtensorMap& b1, const CUtensorMap& b2, const CUtensorMap& a3,
              const CUtensorMap& b3,
              const int32_t* d_sA, const int32_t* d_sB, float* C, int64_t ldc, int num_sms,
-             int promo_kb, unsigned* wave_counter, const GemmTune& tune, const SplitPlan& plan, float* partial) {
+             int promo_kb, unsigned* wave_counter, unsigned* wave_base, const GemmTune& tune, const SplitPlan& plan,
+             float* partial) {
     constexpr int SMEM_BYTES = Geo<BN_, TERMS == 6 ? 3 : 2>::SMEM;
     static bool attr_set = false;
     if (!attr_set) {
@@ -643,10 +645,15 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
     const int64_t tiles = plan.whole + plan.nsplit * plan.slices;   // work units
     const int64_t pairs = num_sms / 2;
     const int grid = 2 * (int)(tiles < pairs ? tiles : pairs);
-    if (wave_counter && cudaMemsetAsync(wave_counter, 0, sizeof(unsigned), st) != cudaSuccess) return -1;
+    const unsigned base = wave_base ? *wave_base : 0u;
     gemm3_kernel<TERMS, BN_><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(a1, a2, b1, b2, a3, b3, (int)M, (int)N, (int)K,
-                                                               promo_kb, d_sA, d_sB, C, ldc, wave_counter,
+                                                               promo_kb, d_sA, d_sB, C, ldc, wave_counter, base,
                                                                tune, plan, partial);
+    if (wave_base && wave_counter) {   // arrivals of this launch: one per CTA per unit index >= 1
+        const int64_t pairs_launched = grid / 2;
+        const int64_t extra = tiles > pairs_launched ? tiles - pairs_launched : 0;
+        *wave_base = base + 2u * (unsigned)extra;
+    }
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -690,6 +697,7 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
                  const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB, float* C, int64_t ldc,
                  int terms, int num_sms, int promo_kb, unsigned* wave_counter, const GemmTuneIn& tin,
                  float* partial, int64_t partial_elems, int* err, const uint16_t* A3, const uint16_t* B3t) {
+    unsigned* wave_base = wave_counter ? tin.wave_base : nullptr;
     CUtensorMap ma1, ma2, mb1, mb2, ma3, mb3;
     const uint16_t* A2e = terms == 1 ? A1 : A2;
     const uint16_t* B2e = terms == 1 ? B1t : B2t;
@@ -718,13 +726,13 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     }
     int r;
     if (terms == 1)
-        r = launch_t<1, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial);
+        r = launch_t<1, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
     else if (terms == 4)
-        r = launch_t<4, 128>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial);
+        r = launch_t<4, 128>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
     else if (terms == 6)
-        r = launch_t<6, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial);
+        r = launch_t<6, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
     else
-        r = launch_t<3, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial);
+        r = launch_t<3, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
     if (r < 0) { *err = 4; return -1; }
     if (plan.slices > 1) {
         const int bn = terms == 4 ? 128 : 256;

@@ -13,10 +13,13 @@ inline int64_t plane_ld(int64_t k) { return ((k + 7) / 8) * 8; }
 // Each launcher returns the number of kernels it launched (>= 0) or -1 on a launch error.
 int launch_maxabs(cudaStream_t s, int64_t rows, int64_t cols, const float* X, int64_t ld,
                   float* d_max, long long* d_bad, int num_sms);
-// max-abs of two matrices in one launch (no bad-index tracking); falls back to two launches
-// when either is strided or misaligned.
+// max-abs of two matrices in one launch (no bad-index tracking): block partials (<= max_parts
+// per matrix) + the last block's reduction write *d_max0 / *d_max1 directly (no reset needed;
+// `ticket` must be 0 before the first use and is left 0).  Strided or misaligned operands fall
+// back to two atomic launches after resetting *d_max0 / *d_max1.
 int launch_maxabs2(cudaStream_t s, int64_t rows0, int64_t cols0, const float* X0, int64_t ld0, float* d_max0,
-                   int64_t rows1, int64_t cols1, const float* X1, int64_t ld1, float* d_max1, int num_sms);
+                   int64_t rows1, int64_t cols1, const float* X1, int64_t ld1, float* d_max1, int num_sms,
+                   float* partials, int max_parts, unsigned* ticket);
 int launch_split(cudaStream_t s, int64_t rows, int64_t cols, const float* X, int64_t ld,
                  const float* d_max, uint16_t* hi, uint16_t* lo, int64_t ldp, int32_t* d_sexp,
                  int num_sms);
@@ -37,6 +40,7 @@ constexpr int kDefaultGroupM = 8;     // raster group, in pair m-blocks
 struct GemmTuneIn {
     int group_m = 0;                  // 0 = default
     int pol_a = 0, pol_b = 0;         // L2 policy for A / B plane loads: 0 normal, 1 evict_first, 2 evict_last
+    unsigned* wave_base = nullptr;    // host-side running base of the (never reset) wave counter
 };
 struct GemmTune {
     int group_m;

@@ -89,14 +89,15 @@ __global__ void __launch_bounds__(256) maxabs_1d_kernel(const float* __restrict_
     block_fold(m, bad, d_max, d_bad);
 }
 
-// Two contiguous matrices in one launch: blocks [0, gx) reduce X0 into d_max0, the rest X1.
+// Two contiguous matrices in one launch: blocks [0, gx) reduce X0, the rest X1.  Each block
+// writes its max (bits of |x|) to partials[blockIdx.x]; the last block to finish (ticket) folds
+// the partials into *d_max0 / *d_max1 and resets the ticket (threadfence-reduction pattern).
 __global__ void __launch_bounds__(256) maxabs2_1d_kernel(const float* __restrict__ X0, int64_t n0, float* d_max0,
                                                          const float* __restrict__ X1, int64_t n1, float* d_max1,
-                                                         int gx) {
+                                                         int gx, unsigned* partials, unsigned* ticket) {
     const bool first = (int)blockIdx.x < gx;
     const float* X = first ? X0 : X1;
     const int64_t n = first ? n0 : n1;
-    float* d_max = first ? d_max0 : d_max1;
     const int64_t b = first ? blockIdx.x : blockIdx.x - gx;
     const int64_t nb = first ? gx : gridDim.x - gx;
     unsigned m = 0;
@@ -121,7 +122,46 @@ __global__ void __launch_bounds__(256) maxabs2_1d_kernel(const float* __restrict
         fold1(v.x, 0, m, bad); fold1(v.y, 0, m, bad); fold1(v.z, 0, m, bad); fold1(v.w, 0, m, bad);
     }
     for (int64_t j = n4 * 4 + tid; j < n; j += nthr) fold1(__ldcs(X + j), 0, m, bad);
-    block_fold(m, LLONG_MAX, d_max, nullptr);
+    // block max -> partial
+    __shared__ unsigned sm[32];
+    __shared__ bool last;
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sm[w] = m;
+    __syncthreads();
+    if (w == 0) {
+        m = l < (int)(blockDim.x >> 5) ? sm[l] : 0u;
+        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (l == 0) {
+            partials[blockIdx.x] = m;
+            __threadfence();
+            last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        }
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    unsigned m0 = 0, m1 = 0;
+    for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) {
+        const unsigned v = __ldcg(partials + k);
+        if (k < gx) m0 = max(m0, v);
+        else m1 = max(m1, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        m0 = max(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+        m1 = max(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+    }
+    __shared__ unsigned s0[32], s1[32];
+    if (l == 0) { s0[w] = m0; s1[w] = m1; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < (int)(blockDim.x >> 5); k++) { m0 = max(m0, s0[k]); m1 = max(m1, s1[k]); }
+        m0 = max(m0, s0[0]);
+        m1 = max(m1, s1[0]);
+        *reinterpret_cast<unsigned*>(d_max0) = m0;
+        *reinterpret_cast<unsigned*>(d_max1) = m1;
+        *ticket = 0u;
+    }
 }
 
 // Strided matrix: grid-stride over rows, threads over columns.
@@ -399,17 +439,21 @@ int launch_maxabs(cudaStream_t st, int64_t rows, int64_t cols, const float* X, i
 }
 
 int launch_maxabs2(cudaStream_t st, int64_t rows0, int64_t cols0, const float* X0, int64_t ld0, float* d_max0,
-                   int64_t rows1, int64_t cols1, const float* X1, int64_t ld1, float* d_max1, int num_sms) {
+                   int64_t rows1, int64_t cols1, const float* X1, int64_t ld1, float* d_max1, int num_sms,
+                   float* partials, int max_parts, unsigned* ticket) {
     const bool ok = ld0 == cols0 && ld1 == cols1 && aligned16(X0) && aligned16(X1) && rows0 > 0 && cols0 > 0 &&
-                    rows1 > 0 && cols1 > 0;
+                    rows1 > 0 && cols1 > 0 && partials && ticket;
     if (!ok) {
+        if (cudaMemsetAsync(d_max0, 0, 4, st) != cudaSuccess || cudaMemsetAsync(d_max1, 0, 4, st) != cudaSuccess)
+            return -1;
         int a = launch_maxabs(st, rows0, cols0, X0, ld0, d_max0, nullptr, num_sms);
         if (a < 0) return -1;
         int b = launch_maxabs(st, rows1, cols1, X1, ld1, d_max1, nullptr, num_sms);
         return b < 0 ? -1 : a + b;
     }
     const int64_t n0 = rows0 * cols0, n1 = rows1 * cols1;
-    const int64_t total_blocks = (int64_t)num_sms * 8;
+    int64_t total_blocks = (int64_t)num_sms * 8;
+    if (total_blocks > max_parts) total_blocks = max_parts;
     int64_t g0 = (int64_t)((double)total_blocks * (double)n0 / (double)(n0 + n1));
     int64_t need0 = (n0 / 4 + 255) / 256, need1 = (n1 / 4 + 255) / 256;
     if (g0 > need0) g0 = need0;
@@ -417,7 +461,8 @@ int launch_maxabs2(cudaStream_t st, int64_t rows0, int64_t cols0, const float* X
     int64_t g1 = total_blocks - g0;
     if (g1 > need1) g1 = need1;
     if (g1 < 1) g1 = 1;
-    maxabs2_1d_kernel<<<(unsigned)(g0 + g1), 256, 0, st>>>(X0, n0, d_max0, X1, n1, d_max1, (int)g0);
+    maxabs2_1d_kernel<<<(unsigned)(g0 + g1), 256, 0, st>>>(X0, n0, d_max0, X1, n1, d_max1, (int)g0,
+                                                           reinterpret_cast<unsigned*>(partials), ticket);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
