@@ -23,6 +23,8 @@
  *    work is enqueued.  SPLIT3_ERR_CUDA reports a failed launch / CUDA API call.
  *  - C must not alias A, B or the workspace.  A handle is not thread-safe: use one per stream.
  *  - Requires an sm_100 device (B200); other devices -> SPLIT3_ERR_ARCH at create time.
+ *  - CUDA-graph capture: every asynchronous entry point may be captured (stream capture) and
+ *    replayed; SPLIT3_CHECK_FINITE synchronises and therefore cannot be captured.
  */
 #ifndef SPLIT3_H
 #define SPLIT3_H

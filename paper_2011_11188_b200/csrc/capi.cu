@@ -12,7 +12,8 @@
 #include "../../include/split3.h"
 #include "internal.h"
 
-// handle-owned device scratch: [0] wave counter, [4] max-abs ticket, [16] presplit max,
+// handle-owned device scratch: [0] wave counter, [4] max-abs ticket, [8] wave counter used under
+// CUDA-graph capture, [16] presplit max,
 // [64..] max-abs block partials (2 x kMaxPartials floats)
 constexpr size_t kMaxPartials = 2048;
 constexpr size_t kCounterBytes = 64 + 2 * kMaxPartials * 4;

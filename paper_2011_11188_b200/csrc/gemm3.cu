@@ -645,11 +645,20 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
     const int64_t tiles = plan.whole + plan.nsplit * plan.slices;   // work units
     const int64_t pairs = num_sms / 2;
     const int grid = 2 * (int)(tiles < pairs ? tiles : pairs);
-    const unsigned base = wave_base ? *wave_base : 0u;
+    // Under CUDA-graph capture the host cannot track the counter across replays: use the graph
+    // slot (wave_counter + 2), reset by a memset node captured before the kernel, base 0.
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) return -1;
+    const bool capturing = cap != cudaStreamCaptureStatusNone;
+    if (capturing && wave_counter) {
+        wave_counter += 2;
+        if (cudaMemsetAsync(wave_counter, 0, sizeof(unsigned), st) != cudaSuccess) return -1;
+    }
+    const unsigned base = (wave_base && !capturing) ? *wave_base : 0u;
     gemm3_kernel<TERMS, BN_><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(a1, a2, b1, b2, a3, b3, (int)M, (int)N, (int)K,
                                                                promo_kb, d_sA, d_sB, C, ldc, wave_counter, base,
                                                                tune, plan, partial);
-    if (wave_base && wave_counter) {   // arrivals of this launch: one per CTA per unit index >= 1
+    if (wave_base && wave_counter && !capturing) {   // arrivals: one per CTA per unit index >= 1
         const int64_t pairs_launched = grid / 2;
         const int64_t extra = tiles > pairs_launched ? tiles - pairs_launched : 0;
         *wave_base = base + 2u * (unsigned)extra;

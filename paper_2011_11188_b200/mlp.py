@@ -66,6 +66,11 @@ class DenseNet:
 
     def backward(self, X, y):
         """(loss, [dW], [db]) of the mean softmax cross-entropy."""
+        loss, dWs, dbs = self.backward_device(X, y)
+        return float(loss), dWs, dbs
+
+    def backward_device(self, X, y):
+        """As backward(), with the loss left on the device (no host synchronisation)."""
         acts = self.forward(X)
         _, dZ, loss = self.h.softmax_xent(acts[-1], y, want_probs=False, want_grad=True)
         dWs, dbs = [None] * len(self.W), [None] * len(self.W)
@@ -75,15 +80,33 @@ class DenseNet:
             if i > 0:
                 dH = self._mm(dZ, self.W[i], transB=True)         # dZ W^T
                 dZ = self.h.relu_backward(dH, acts[i], out=dH)
-        return float(loss), dWs, dbs
+        return loss, dWs, dbs
 
-    def step(self, X, y, lr: float):
-        loss, dWs, dbs = self.backward(X, y)
+    def step_device(self, X, y, lr: float):
+        """One SGD step; returns the loss as a 0-d device tensor (capturable in a CUDA graph)."""
+        loss, dWs, dbs = self.backward_device(X, y)
         for w, g in zip(self.W, dWs):
             self.h.sgd_update(w, g, lr)
         for b, g in zip(self.b, dbs):
             self.h.sgd_update(b, g, lr)
         return loss
+
+    def step(self, X, y, lr: float):
+        return float(self.step_device(X, y, lr))
+
+    def capture_step(self, X, y, lr: float):
+        """CUDA-graph the training step on the static batch buffers X, y (refill them in place
+        between replays).  Returns (replay, loss_tensor)."""
+        self.step_device(X, y, lr)          # warm-up: workspace and allocator pools
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                loss = self.step_device(X, y, lr)
+        torch.cuda.current_stream().wait_stream(s)
+        return g.replay, loss
 
     def accuracy(self, X, y):
         return float((self.forward(X)[-1].argmax(dim=1) == y).float().mean())

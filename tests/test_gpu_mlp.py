@@ -101,3 +101,22 @@ def test_training_trajectory_close_to_fp64(h):
     Wr, br = omlp.sgd_train(W0, b0, batches, 0.1)
     for w, r in zip(_np(net.W), Wr):
         assert np.linalg.norm(w - r) <= 1e-5 * np.linalg.norm(r)
+
+
+def test_graph_captured_step_matches_eager(h):
+    """The CUDA-graph training step produces the same weights as eager steps, bitwise."""
+    from paper_2011_11188_b200.mlp import DenseNet
+
+    sizes = (64, 128, 10)
+    X, y = make_blobs(256, 10, 64, 5.0, 41)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    a = DenseNet(sizes, seed=5, h=h)
+    b = DenseNet(sizes, seed=5, h=h)
+    replay, loss = b.capture_step(Xd, yd, 0.05)   # capture performs one warm-up step
+    a.step(Xd, yd, 0.05)
+    for _ in range(4):
+        a.step(Xd, yd, 0.05)
+        replay()
+    torch.cuda.synchronize()
+    for wa, wb in zip(a.W + a.b, b.W + b.b):
+        assert torch.equal(wa, wb)

@@ -424,3 +424,30 @@ def test_planes_exhaustive_fp32_range(h, orc):
             del X, hi, lo
             torch.cuda.empty_cache()
     assert checked == 2 * 0x47000000
+
+
+@pytest.mark.parametrize("shape,kw", [((2048, 2048, 1024), {}), ((256, 1024, 4096), {}),
+                                      ((700, 900, 1500), {"bf16x3": True})])
+def test_cuda_graph_capture_replay(h, shape, kw):
+    """split3_sgemm captured into a CUDA graph and replayed == eager, bitwise (wave-lockstep slot
+    and max-abs ticket are capture-safe); replays interleaved with eager calls stay correct."""
+    M, N, K = shape
+    A = torch_matrix("uniform", M, K, seed=1, device="cuda")
+    B = torch_matrix("uniform", K, N, seed=2, device="cuda")
+    ref = h.sgemm(A, B, **kw).clone()
+    C = torch.empty((M, N), device="cuda")
+    h.sgemm(A, B, out=C, **kw)           # allocate the workspace outside the capture
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            h.sgemm(A, B, out=C, **kw)
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(3):
+        C.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(C.view(torch.int32), ref.view(torch.int32))
+        eager = h.sgemm(A, B, **kw)
+        assert torch.equal(eager.view(torch.int32), ref.view(torch.int32))

@@ -14,12 +14,7 @@ import torch  # noqa: E402
 import paper_2011_11188_b200 as s3  # noqa: E402
 from paper_2011_11188_b200.mlp import DenseNet  # noqa: E402
 
-sizes = [4096, 4096, 4096, 4096, 1024]
-B = 4096
 h = s3.Handle(0)
-X = torch.randn((B, sizes[0]), device="cuda")
-y = torch.randint(0, sizes[-1], (B,), device="cuda", dtype=torch.int32)
-flops = sum(6.0 * B * a * b for a, b in zip(sizes[:-1], sizes[1:]))
 res = []
 
 
@@ -36,37 +31,51 @@ def timeit(fn, reps=20):
     return e0.elapsed_time(e1) / reps
 
 
-for mode in ("three", "one", "four"):
-    net = DenseNet(sizes, seed=0, mode=mode, h=h)
-    ms = timeit(lambda: net.step(X, y, 1e-3))
-    res.append({"impl": f"split3 {mode}-term", "ms_per_step": ms, "eff_tflops": flops / (ms / 1e3) / 1e12})
+def run(sizes, B, torch_ref=True):
+    X = torch.randn((B, sizes[0]), device="cuda")
+    y = torch.randint(0, sizes[-1], (B,), device="cuda", dtype=torch.int32)
+    flops = sum(6.0 * B * a * b for a, b in zip(sizes[:-1], sizes[1:]))
+    tag = f"{'x'.join(map(str, sizes))} batch {B}"
+    for mode in ("three", "one", "four"):
+        net = DenseNet(sizes, seed=0, mode=mode, h=h)
+        ms = timeit(lambda: net.step_device(X, y, 1e-3))
+        res.append({"net": tag, "impl": f"split3 {mode}-term", "ms_per_step": ms,
+                    "eff_tflops": flops / (ms / 1e3) / 1e12})
+        print(json.dumps(res[-1]), flush=True)
+        if mode == "three":
+            replay, _ = net.capture_step(X, y, 1e-3)
+            ms = timeit(replay)
+            res.append({"net": tag, "impl": "split3 three-term, CUDA graph", "ms_per_step": ms,
+                        "eff_tflops": flops / (ms / 1e3) / 1e12})
+            print(json.dumps(res[-1]), flush=True)
+    if not torch_ref:
+        return
+    torch.backends.cuda.matmul.allow_tf32 = False
+    Ws = [torch.randn((a, b), device="cuda") * (2.0 / (a + b)) ** 0.5 for a, b in zip(sizes[:-1], sizes[1:])]
+    bs = [torch.zeros(b, device="cuda") for b in sizes[1:]]
+    for t in Ws + bs:
+        t.requires_grad_(True)
+    yl = y.long()
+
+    def torch_step():
+        hcur = X
+        for i, (w, b) in enumerate(zip(Ws, bs)):
+            hcur = hcur @ w + b
+            if i < len(Ws) - 1:
+                hcur = torch.relu(hcur)
+        loss = torch.nn.functional.cross_entropy(hcur, yl)
+        gs = torch.autograd.grad(loss, Ws + bs)
+        with torch.no_grad():
+            for p, g in zip(Ws + bs, gs):
+                p -= 1e-3 * g
+
+    ms = timeit(torch_step, reps=5)
+    res.append({"net": tag, "impl": "torch fp32 (cuBLAS SGEMM, TF32 off)", "ms_per_step": ms,
+                "eff_tflops": flops / (ms / 1e3) / 1e12})
     print(json.dumps(res[-1]), flush=True)
 
-# context: plain torch fp32 (cuBLAS SGEMM) of the same step
-torch.backends.cuda.matmul.allow_tf32 = False
-Ws = [torch.randn((a, b), device="cuda") * (2.0 / (a + b)) ** 0.5 for a, b in zip(sizes[:-1], sizes[1:])]
-bs = [torch.zeros(b, device="cuda") for b in sizes[1:]]
-for t in Ws + bs:
-    t.requires_grad_(True)
-yl = y.long()
 
-
-def torch_step():
-    hcur = X
-    for i, (w, b) in enumerate(zip(Ws, bs)):
-        hcur = hcur @ w + b
-        if i < len(Ws) - 1:
-            hcur = torch.relu(hcur)
-    loss = torch.nn.functional.cross_entropy(hcur, yl)
-    gs = torch.autograd.grad(loss, Ws + bs)
-    with torch.no_grad():
-        for p, g in zip(Ws + bs, gs):
-            p -= 1e-3 * g
-
-
-ms = timeit(torch_step, reps=5)
-res.append({"impl": "torch fp32 (cuBLAS SGEMM, TF32 off)", "ms_per_step": ms, "eff_tflops": flops / (ms / 1e3) / 1e12})
-print(json.dumps(res[-1]), flush=True)
+run([4096, 4096, 4096, 4096, 1024], 4096)
+run([1024, 1024, 1024, 10], 512)
 os.makedirs("gpurun_out", exist_ok=True)
-json.dump({"sizes": sizes, "batch": B, "flops_per_step": flops, "results": res},
-          open("gpurun_out/mlp_bench.json", "w"), indent=1)
+json.dump({"results": res}, open("gpurun_out/mlp_bench.json", "w"), indent=1)
