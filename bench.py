@@ -41,6 +41,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-target-s", type=float, default=12.0)
+    p.add_argument("--sustained-s", type=float, default=4.0,
+                   help="extra back-to-back loop (s) reported as 'sustained' (0 = skip)")
     return p.parse_args()
 
 
@@ -353,6 +355,32 @@ def main():
                 "split_hbm_gbs": (12.0 * 2 * n * n / (split_ms / args.steps / 1e3) / 1e9)
                 if ncalls and split_ms > 0 and world == 1 else None}
 
+    # sustained: back to back for ~sustained_s seconds under the power cap (SURVEY §8d protocol);
+    # the contract's `value` above is the K-step timed region
+    sustained = None
+    if args.sustained_s > 0:
+        reps = max(args.steps, int(args.sustained_s * 1e3 / max(t_ms / args.steps, 1e-3)))
+        s2 = ClockSampler(gpu_idx)
+        s2.start()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        y0, y1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        y0.record(stream)
+        for _ in range(reps):
+            step()
+        y1.record(stream)
+        torch.cuda.synchronize()
+        ck = s2.stop()
+        ts = y0.elapsed_time(y1)
+        if world > 1:
+            tt = torch.tensor([ts], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            ts = float(tt.item())
+        sustained = {"value": flops_step * reps / (ts / 1e3) / 1e12, "unit": "TFLOPS", "steps": reps,
+                     "seconds": ts / 1e3, "sm_mhz": ck.get("sm_mhz"), "power_w_max": ck.get("power_w_max"),
+                     "reasons": ck.get("reasons")}
+
     # e2e through the C-ABI with HOST buffers (H2D of A, B and D2H of C inside the timed region)
     e2e = None
     if not args.no_e2e and world == 1:
@@ -421,6 +449,7 @@ def main():
             "frac_of_peak_over_3": value / world / (pk["tc_burst"] / n_prod),
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "sustained": sustained,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
