@@ -253,8 +253,10 @@ def encbf16(x) -> np.ndarray:
 
 
 def decbf16(h) -> np.ndarray:
+    """bfloat16 bit patterns -> exact fp64 values (bf16 is the top half of binary32)."""
     h = np.ascontiguousarray(h, dtype=np.uint16)
-    return (h.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    with np.errstate(invalid="ignore"):     # signalling-NaN patterns
+        return (h.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
 
 
 def split_bf16x3(X):
