@@ -712,7 +712,10 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
         return SPLIT3_ERR_CUDA;
     launches += n;
     // GEMM in row blocks (multiples of the 256-row pair tile); copy each block out as it completes
-    int nblk = M >= 8 * 1024 ? 4 : (M >= 2048 ? 2 : 1);
+    // more blocks shorten the exposed copy-out of the last one; each block keeps >= 2 waves of tiles
+    const int64_t tiles_n = (N + 255) / 256;
+    int nblk = 1;
+    while (nblk < 8 && ((M / (2 * nblk)) / 256) * tiles_n >= 2 * (h->num_sms / 2)) nblk *= 2;
     int64_t rows_per = ((M + nblk - 1) / nblk + 255) / 256 * 256;
     for (int b = 0; b < nblk; b++) {
         const int64_t r0 = b * rows_per;
