@@ -191,22 +191,31 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
 
 class TileGemm:
     """bench.py's multi-GPU step: each rank owns an n x n C tile of a (pr*n) x (pc*n) x n
-    problem (weak scaling), inputs sharded as above, generated on device from seeds."""
+    problem (weak scaling), inputs sharded as above, generated on the device from seeds
+    (A block of rank r: seed*1000 + 2r, B block: seed*1000 + 2r + 1).  `ops`/`device` are
+    injectable so the same workload runs on CPU / gloo in tests/test_dist_gloo.py."""
 
-    def __init__(self, h, n: int, world: int, rank: int, four_term=False, one_term=False, seed=0):
-        from workloads import torch_matrix
+    def __init__(self, h, n: int, world: int, rank: int, four_term=False, one_term=False, seed=0,
+                 ops=None, device=None):
+        from workloads import numpy_matrix, torch_matrix
 
         self.pr, self.pc = grid_for(world)
         self.M, self.N, self.K = self.pr * n, self.pc * n, n
         self.h = h
-        self.ops = CudaOps(h)
+        self.ops = ops if ops is not None else CudaOps(h)
         self.groups = make_groups(world)
         r0, r1 = a_block_rows(self.M, world, rank)
         c0, c1 = b_block_cols(self.N, world, rank)
-        dev = torch.device("cuda", torch.cuda.current_device())
-        self.A_blk = torch_matrix("uniform", r1 - r0, self.K, seed=seed * 1000 + 2 * rank, device=dev)
-        self.B_blk = torch_matrix("uniform", self.K, c1 - c0, seed=seed * 1000 + 2 * rank + 1, device=dev)
-        self.C = torch.empty((n, n), dtype=torch.float32, device=dev)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if dev.type == "cuda":
+            self.A_blk = torch_matrix("uniform", r1 - r0, self.K, seed=seed * 1000 + 2 * rank, device=dev)
+            self.B_blk = torch_matrix("uniform", self.K, c1 - c0, seed=seed * 1000 + 2 * rank + 1, device=dev)
+            dtype = torch.float32
+        else:
+            self.A_blk = torch.from_numpy(numpy_matrix("uniform", r1 - r0, self.K, seed * 1000 + 2 * rank))
+            self.B_blk = torch.from_numpy(numpy_matrix("uniform", self.K, c1 - c0, seed * 1000 + 2 * rank + 1))
+            dtype = torch.float64          # the oracle's tiles
+        self.C = torch.empty((n, n), dtype=dtype, device=dev)
         self.four, self.one = four_term, one_term
 
     def run(self):
@@ -214,4 +223,5 @@ class TileGemm:
                         four_term=self.four, one_term=self.one)
 
     def launches_per_step(self) -> int:
-        return 5   # 2 max-abs + 2 split + 1 GEMM (NCCL kernels not counted)
+        # 2 max-abs + 2 split + one GEMM per row block of the tile (NCCL kernels not counted)
+        return 4 + (self.pc if self.pc > 1 else 1)

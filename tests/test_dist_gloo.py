@@ -118,3 +118,45 @@ def test_sgemm_2d_matches_single_process(orc, world, terms, overlap):
     res = dict(q.get(timeout=5) for _ in range(world))
     assert all(p.exitcode == 0 for p in procs)
     assert res == {r: True for r in range(world)}
+
+
+def _tile_worker(rank, world, port, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+
+        tg = d2.TileGemm(None, n, world, rank, ops=OracleOps(oracle), device=torch.device("cpu"), seed=3)
+        tile = tg.run().numpy()
+        # assemble the global A and B from every rank's blocks, then the oracle's full product
+        As = [torch.empty_like(tg.A_blk) for _ in range(world)]
+        Bs = [torch.empty_like(tg.B_blk) for _ in range(world)]
+        dist.all_gather(As, tg.A_blk)
+        dist.all_gather(Bs, tg.B_blk)
+        A = torch.cat(As).numpy()                     # row blocks in rank order
+        B = np.empty((tg.K, tg.N), np.float32)
+        for r in range(world):
+            c0, c1 = d2.b_block_cols(tg.N, world, r)
+            B[:, c0:c1] = Bs[r].numpy()
+        full = oracle.sgemm(A, B, terms=3)
+        r0, r1, c0, c1 = d2.c_tile(tg.M, tg.N, world, rank)
+        q.put((rank, bool(np.array_equal(tile, full[r0:r1, c0:c1])), tg.launches_per_step()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_bench_tilegemm_workload(orc, world):
+    """bench.py's multi-rank workload (TileGemm: sharded seeded blocks, weak scaling) is the
+    exact 2-D partition of one global product."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tile_worker, args=(r, world, port, 24, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    res = {r: (ok, nl) for r, ok, nl in (q.get(timeout=5) for _ in range(world))}
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(ok for ok, _ in res.values()), res
