@@ -22,6 +22,6 @@ A = torch_matrix("uniform", M, K, seed=0)
 B = torch_matrix("uniform", K, a.n, seed=1)
 h = s3.Handle(0)
 for _ in range(a.reps):
-    C = h.sgemm(A, B, four_term=a.terms == 4, one_term=a.terms == 1)
+    C = h.sgemm(A, B, four_term=a.terms == 4, one_term=a.terms == 1, bf16x3=a.terms == 6)
 torch.cuda.synchronize()
 print("ok", float(C[0, 0]))
