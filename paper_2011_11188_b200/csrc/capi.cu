@@ -29,7 +29,7 @@ struct split3_ctx {
     int promo_kb = 0;   // 0 = library default
     int wave_sync = 1;  // GEMM wave lockstep hint (L2 locality)
     split3::GemmTuneIn tune;
-    unsigned wave_base = 0;           // running value of the device wave counter (d_counters[0])
+    unsigned wave_base[2] = {0, 0};   // running value of the device wave counter (d_counters[0]), launches
     unsigned* d_counters = nullptr;   // 256 B of device scratch owned by the handle
     // host-buffer entry: copy-in / copy-out streams and events, created on first use
     cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -188,7 +188,7 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
         delete c;
         return SPLIT3_ERR_CUDA;
     }
-    c->tune.wave_base = &c->wave_base;
+    c->tune.wave_base = c->wave_base;
     *h = c;
     return SPLIT3_OK;
 }

@@ -660,6 +660,12 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
         wave_counter += 2;
         if (cudaMemsetAsync(wave_counter, 0, sizeof(unsigned), st) != cudaSuccess) return -1;
     }
+    // Periodic resync of the eager counter (every 64 launches): bounds the cost of any drift
+    // between the device counter and the host-tracked base (e.g. after an aborted launch).
+    if (wave_counter && wave_base && !capturing && (wave_base[1]++ & 63u) == 0) {
+        if (cudaMemsetAsync(wave_counter, 0, sizeof(unsigned), st) != cudaSuccess) return -1;
+        wave_base[0] = 0;
+    }
     const unsigned base = (wave_base && !capturing) ? *wave_base : 0u;
     gemm3_kernel<TERMS, BN_><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(a1, a2, b1, b2, a3, b3, (int)M, (int)N, (int)K,
                                                                promo_kb, d_sA, d_sB, C, ldc, wave_counter, base,

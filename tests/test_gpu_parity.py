@@ -451,3 +451,22 @@ def test_cuda_graph_capture_replay(h, shape, kw):
         assert torch.equal(C.view(torch.int32), ref.view(torch.int32))
         eager = h.sgemm(A, B, **kw)
         assert torch.equal(eager.view(torch.int32), ref.view(torch.int32))
+
+
+def test_wave_counter_many_launches(h):
+    """100 back-to-back launches (the eager wave counter is resynchronised every 64) stay bitwise
+    identical and fast (no lockstep timeouts)."""
+    import time
+
+    A = torch_matrix("uniform", 4096, 2048, seed=1, device="cuda")
+    B = torch_matrix("uniform", 2048, 4096, seed=2, device="cuda")
+    ref = h.sgemm(A, B).clone()
+    C = torch.empty_like(ref)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(100):
+        h.sgemm(A, B, out=C)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / 100
+    assert torch.equal(C.view(torch.int32), ref.view(torch.int32))
+    assert dt < 2e-3, dt      # ~0.2 ms of work; a desynchronised counter would cost 0.2 ms per wave
