@@ -31,20 +31,24 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Build libsplit3.so (or, for experiments, `out` with extra -D `defines`)."""
+    target = out or LIB
+    if not force and out is None and not needs_build():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, "-shared", "-o", tmp, *sources(), "-I", os.path.join(ROOT, "include")]
+    tmp = target + f".tmp{os.getpid()}"
+    cmd = [NVCC, *NVCC_FLAGS, "-shared", "-o", tmp, *sources(), "-I", os.path.join(ROOT, "include"),
+           *[f"-D{d}" for d in defines]]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
     if verbose:
         print(res.stderr)
-    with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
-        f.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    if out is None:
+        with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
+            f.write(res.stderr)
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

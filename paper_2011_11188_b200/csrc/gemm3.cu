@@ -122,6 +122,20 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
         "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & PEER_MASK), "r"(x), "r"(y), "l"(policy)
         : "memory");
 }
+// TMA store of a shared-memory box to global (bulk async group of the issuing thread)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int32_t x, int32_t y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(x), "r"(y)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -235,7 +249,8 @@ struct Geo {
     static constexpr int TILE_B_BYTES = BNH * BK * 2;
     static constexpr int STAGE_BYTES = PL * TILE_A_BYTES + PL * TILE_B_BYTES;
     static constexpr int STAGES = (220 * 1024) / STAGE_BYTES > 6 ? 6 : (220 * 1024) / STAGE_BYTES;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int STAGING = 8 * 4096;   // epilogue: 4 KB (32 rows x 32 fp32) per warp
+    static constexpr int SMEM = STAGES * STAGE_BYTES + STAGING + 1024 + 256;
 };
 
 // Add this thread's row of NCOL TMEM columns into master[], 16 columns per tcgen05.ld.
@@ -256,6 +271,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapA2,
              const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
              const __grid_constant__ CUtensorMap mapA3, const __grid_constant__ CUtensorMap mapB3,
+             const __grid_constant__ CUtensorMap mapC, int tma_store,
              int M, int N, int K, int promo_kb, const int32_t* __restrict__ d_sA,
              const int32_t* __restrict__ d_sB, float* __restrict__ C, int64_t ldc,
              unsigned* __restrict__ wave_counter, unsigned wave_base, const GemmTune tune,
@@ -283,7 +299,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint8_t* staging = smem + STAGES * STAGE_BYTES;   // 1024-aligned (128-B swizzle atoms)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(staging + G::STAGING);
     uint64_t* full_bar = bars;                        // [STAGES]   leader: TMA bytes landed
     uint64_t* empty_bar = bars + STAGES;              // [STAGES]   both: stage consumed
     uint64_t* hfull_bar = bars + 2 * STAGES;          // [2]        both: D_hi chunk ready
@@ -409,7 +426,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     const uint64_t b1 = sdesc_sw128(smem_u32(st + B_OFF));
                     const uint64_t b2 = sdesc_sw128(smem_u32(st + B_OFF + TILE_B_BYTES));
                     const uint64_t b3 = sdesc_sw128(smem_u32(st + B_OFF + 2 * TILE_B_BYTES));
-                    const bool hi_first = kb == kb_begin;
+                    // D_hi first at both ends of a unit: at the start the epilogue frees D_hi before
+                    // D_mid; at the end the last D_hi drain overlaps the last D_mid MMAs
+                    const bool hi_first = kb == kb_begin || kb + 1 == kb_end;
                     auto issue_mid = [&]() {
                         if (!HAS_MID) return;
                         if (!mid_ready) {
@@ -434,6 +453,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                         }
                         __syncwarp();
                     };
+                    const bool chunk_end = ((kb + 1 - kb_begin) % promo_kb) == 0 || kb + 1 == kb_end;
                     auto issue_hi = [&]() {
                         if (chunk_start) {
                             mbar_wait(smem_u32(&hempty_bar[hb]), hphase ^ 1);
@@ -445,14 +465,15 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                                 const uint64_t dk = (uint64_t)(2 * k);
                                 mma_pair(t_hi, a1 + dk, b1 + dk, IDESC, (!chunk_start || k > 0) ? 1u : 0u);
                             }
+                            // D_hi chunk ready: the commit covers only MMAs issued so far, so with
+                            // D_hi first the drain starts while this k-block's D_mid MMAs run
+                            if (chunk_end) mma_commit_pair(smem_u32(&hfull_bar[hb]));
                         }
                         __syncwarp();
                     };
                     if (hi_first) { issue_hi(); issue_mid(); } else { issue_mid(); issue_hi(); }
                     if (elect_one()) {
                         mma_commit_pair(smem_u32(&empty_bar[stage]));        // stage free in both CTAs
-                        const bool chunk_end = ((kb + 1 - kb_begin) % promo_kb) == 0 || kb + 1 == kb_end;
-                        if (chunk_end) mma_commit_pair(smem_u32(&hfull_bar[hb]));   // D_hi chunk ready
                         if (HAS_MID && kb + 1 == kb_end) mma_commit_pair(smem_u32(&mfull_bar[0]));
                     }
                     __syncwarp();
@@ -543,7 +564,36 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             }
             const int64_t row = mb * 2 * BM + crank * BM + quad * 32 + lane;
             const int64_t col0 = nb * BN_ + half * NCOL;
-            if (row < M) {
+            if (tma_store) {
+                // stage 32 rows x 32 columns per step (row = lane, 16-B chunks XOR-swizzled by
+                // row % 8 as the map's SWIZZLE_128B expects: 4 wavefronts per warp store), then one
+                // lane stores the box with TMA (clipped at M, N); the buffer is reused once the
+                // previous store has read it
+                const uint32_t stg = smem_u32(staging + (warp - 2) * 4096);
+                const int32_t y = (int32_t)(mb * 2 * BM + crank * BM + quad * 32);
+#pragma unroll
+                for (int c = 0; c < NCOL / 32; c++) {
+                    if (lane == 0) bulk_wait_read0();
+                    __syncwarp();
+#pragma unroll
+                    for (int q = 0; q < 8; q++)
+                        st_shared_v4(stg + lane * 128 + ((q ^ (lane & 7)) * 16), master[c * 32 + 4 * q],
+                                     master[c * 32 + 4 * q + 1], master[c * 32 + 4 * q + 2], master[c * 32 + 4 * q + 3]);
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&mapC, stg, (int32_t)(col0 + c * 32), y);
+                        bulk_commit();
+                    }
+                }
+                continue;
+            }
+#ifdef SPLIT3_EXP_NO_STORE
+            if (row == -1)   // experiment only: time the kernel without the C stores
+#else
+            if (row < M)
+#endif
+            {
                 float* crow = C + row * ldc + col0;
                 if (vec_ok && col0 + NCOL <= N) {
 #pragma unroll
@@ -559,6 +609,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         }
     }
 
+    if (warp >= 2 && tma_store && lane == 0) bulk_wait0();   // the C stores have completed
     tc_fence_before();
     cluster_sync();
     if (warp == 1) {
@@ -614,6 +665,20 @@ EncodeTiledFn get_encode_fn() {
     return fn;
 }
 
+// 2-D map over C (fp32 row-major, M x N, ldc): 32 x 32 boxes, 128-B swizzle (the epilogue's
+// staging layout).  Requires C 16-byte aligned and ldc % 4 == 0.
+bool make_c_map(CUtensorMap* map, float* C, int64_t M, int64_t N, int64_t ldc) {
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+    cuuint64_t strides[1] = {(cuuint64_t)(ldc * 4)};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // 2-D map over a K-major FP16 plane: rows x K elements, leading dimension ld (elements).
 bool make_plane_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int64_t ld,
                     int box_rows) {
@@ -632,7 +697,7 @@ bool make_plane_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K,
 template <int TERMS, int BN_>
 int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap& a1,
              const CUtensorMap& a2, const CUtensorMap& b1, const CUtensorMap& b2, const CUtensorMap& a3,
-             const CUtensorMap& b3,
+             const CUtensorMap& b3, const CUtensorMap& mc, int tma_store,
              const int32_t* d_sA, const int32_t* d_sB, float* C, int64_t ldc, int num_sms,
              int promo_kb, unsigned* wave_counter, unsigned* wave_base, const GemmTune& tune, const SplitPlan& plan,
              float* partial) {
@@ -667,7 +732,7 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
         wave_base[0] = 0;
     }
     const unsigned base = (wave_base && !capturing) ? *wave_base : 0u;
-    gemm3_kernel<TERMS, BN_><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(a1, a2, b1, b2, a3, b3, (int)M, (int)N, (int)K,
+    gemm3_kernel<TERMS, BN_><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(a1, a2, b1, b2, a3, b3, mc, tma_store, (int)M, (int)N, (int)K,
                                                                promo_kb, d_sA, d_sB, C, ldc, wave_counter, base,
                                                                tune, plan, partial);
     if (wave_base && wave_counter && !capturing) {   // arrivals: one per CTA per unit index >= 1
@@ -733,6 +798,12 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
         return -1;
     }
     if (terms != 6) { ma3 = ma1; mb3 = mb1; }
+    // TMA-store epilogue when C allows it (else per-thread float4 / scalar stores)
+    CUtensorMap mc = ma1;
+    int tma_store = 0;
+#ifndef SPLIT3_EXP_NO_STORE
+    if ((ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(C) & 15u) == 0 && make_c_map(&mc, C, M, N, ldc)) tma_store = 1;
+#endif
     const int promo = promo_kb > 0 ? promo_kb : kDefaultPromoKb;
     GemmTune tune;
     tune.group_m = tin.group_m > 0 ? tin.group_m : kDefaultGroupM;
@@ -747,13 +818,13 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     }
     int r;
     if (terms == 1)
-        r = launch_t<1, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
+        r = launch_t<1, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
     else if (terms == 4)
-        r = launch_t<4, 128>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
+        r = launch_t<4, 128>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
     else if (terms == 6)
-        r = launch_t<6, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
+        r = launch_t<6, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
     else
-        r = launch_t<3, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
+        r = launch_t<3, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
     if (r < 0) { *err = 4; return -1; }
     if (plan.slices > 1) {
         const int bn = terms == 4 ? 128 : 256;

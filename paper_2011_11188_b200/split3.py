@@ -15,7 +15,9 @@ import torch
 
 from . import _build
 
-LIB_PATH = _build.LIB
+# SPLIT3_EXPERIMENT_LIB: load an experimental build of the same sources (tools/exp_ab.py) instead
+# of the in-tree library — for A/B timing experiments only.
+LIB_PATH = os.environ.get("SPLIT3_EXPERIMENT_LIB") or _build.LIB
 
 OK = 0
 ERR_INVALID_VALUE = 1

@@ -1,0 +1,54 @@
+"""A/B timing of experimental builds (extra -D flags) of the same sources.
+
+  python tools/exp_ab.py build TAG DEFINE...     (here: nvcc -> tools/exp/libsplit3_TAG.so)
+  python tools/exp_ab.py time  M N K [TAG...]    (on the GPU: GEMM-kernel time per library)
+"""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+if sys.argv[1] == "build":
+    from paper_2011_11188_b200 import _build
+
+    tag = sys.argv[2]
+    out = os.path.join(ROOT, "tools", "exp", f"libsplit3_{tag}.so")
+    print(_build.build(force=True, out=out, defines=sys.argv[3:]))
+    sys.exit(0)
+
+M, N, K = (int(x) for x in sys.argv[2:5])
+tags = sys.argv[5:] or ["base"]
+if len(tags) > 1 or os.environ.get("EXP_CHILD") is None:
+    for tag in tags:
+        env = dict(os.environ, EXP_CHILD="1")
+        if tag != "base":
+            env["SPLIT3_EXPERIMENT_LIB"] = os.path.join(ROOT, "tools", "exp", f"libsplit3_{tag}.so")
+        out = subprocess.run([sys.executable, __file__, "time", str(M), str(N), str(K), tag], env=env,
+                             capture_output=True, text=True)
+        print(out.stdout.strip() or out.stderr[-2000:])
+    sys.exit(0)
+
+import torch  # noqa: E402
+
+import paper_2011_11188_b200 as s3  # noqa: E402
+from workloads import torch_matrix  # noqa: E402
+
+h = s3.Handle(0)
+A = torch_matrix("uniform", M, K, seed=0)
+B = torch_matrix("uniform", K, N, seed=1)
+C = torch.empty((M, N), device="cuda")
+for _ in range(3):
+    h.sgemm(A, B, out=C)
+torch.cuda.synchronize()
+h.timing_enable(True)
+h.timing_read()
+reps = 20
+for _ in range(reps):
+    h.sgemm(A, B, out=C)
+torch.cuda.synchronize()
+sp, gm, n = h.timing_read()
+print(json.dumps({"tag": tags[0], "lib": s3.split3.LIB_PATH, "M": M, "N": N, "K": K,
+                  "gemm_ms": gm / n, "fp16_tflops": 3 * 2.0 * M * N * K / (gm / n / 1e3) / 1e12}))
