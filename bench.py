@@ -157,8 +157,10 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- cpu oracle -----
-def cpu_oracle_sample(A_host: np.ndarray, B_host: np.ndarray, terms: int, target_s: float):
-    """Time oracle.sgemm_sampled on R x R sampled outputs of the full-size problem."""
+def cpu_oracle_sample(A_host: np.ndarray, B_host: np.ndarray, terms: int, target_s: float, C_gpu=None):
+    """Time oracle.sgemm_sampled on R x R sampled outputs of the full-size problem.  With the
+    GPU result C_gpu (a torch tensor), also report its error on exactly those samples: E_or vs
+    the oracle's emulation, E64rel / E64 vs fp64 products of the sampled rows and columns."""
     import oracle
 
     N = A_host.shape[0]
@@ -166,12 +168,16 @@ def cpu_oracle_sample(A_host: np.ndarray, B_host: np.ndarray, terms: int, target
     Nc = B_host.shape[1]
     rng = np.random.Generator(np.random.PCG64(1234))
 
+    last = {}
+
     def run(R):
         rows = np.sort(rng.choice(A_host.shape[0], R, replace=False))
         cols = np.sort(rng.choice(Nc, R, replace=False))
         t = time.perf_counter()
-        oracle.sgemm_sampled(A_host, B_host, rows, cols, terms=terms)
-        return time.perf_counter() - t
+        Cs, _, _ = oracle.sgemm_sampled(A_host, B_host, rows, cols, terms=terms)
+        dt = time.perf_counter() - t
+        last.update(rows=rows, cols=cols, Cs=Cs)
+        return dt
 
     r0 = min(32, N, Nc)
     t0 = run(r0)
@@ -183,8 +189,24 @@ def cpu_oracle_sample(A_host: np.ndarray, B_host: np.ndarray, terms: int, target
     R = int(max(r1, min(R, 1024, N, Nc)))
     dt = run(R)
     flops = 2.0 * R * R * K
+    acc = None
+    if C_gpu is not None:
+        import torch
+
+        rows, cols, Cs = last["rows"], last["cols"], last["Cs"]
+        Cg = C_gpu[torch.from_numpy(rows).to(C_gpu.device)][:, torch.from_numpy(cols).to(C_gpu.device)]
+        Cg = Cg.cpu().numpy().astype(np.float64)
+        C64 = A_host[rows].astype(np.float64) @ B_host[:, cols].astype(np.float64)
+        nA = float(np.linalg.norm(A_host.astype(np.float64)))
+        nB = float(np.linalg.norm(B_host.astype(np.float64)))
+        scale = (A_host.shape[0] * Nc) / (len(rows) * len(cols))
+        acc = {"E_or": float(np.linalg.norm(Cg - Cs) / np.linalg.norm(Cs)),
+               "E64rel": float(np.linalg.norm(Cg - C64) / np.linalg.norm(C64)),
+               "E64": float(np.sqrt(scale) * np.linalg.norm(Cg - C64) / (nA * nB)),
+               "samples": f"{len(rows)}x{len(cols)} outputs of the timed run's C",
+               "tolerances": {"E_or": 1e-6, "E64": 2e-6}}
     return {"value": flops / dt / 1e12, "unit": "TFLOPS", "cores": oracle.num_threads(),
-            "kind": "oracle", "seconds": dt,
+            "kind": "oracle", "seconds": dt, "accuracy": acc,
             "sample": f"{R}x{R} sampled outputs of the {A_host.shape[0]}x{Nc}x{K} product "
                       f"(fp64 oracle: full-matrix max-abs, split of the sampled rows/cols, "
                       f"{terms}-term Eq. A_2); value = 2*R*R*K / time"}
@@ -355,6 +377,13 @@ def main():
                 "split_hbm_gbs": (12.0 * 2 * n * n / (split_ms / args.steps / 1e3) / 1e9)
                 if ncalls and split_ms > 0 and world == 1 else None}
 
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_oracle_sample(A.cpu().numpy(), B.cpu().numpy(), args.terms, args.cpu_target_s, C_gpu=C)
+        except Exception as ex:   # reported, never silently replaced
+            cpu = {"value": None, "error": repr(ex)}
+
     # sustained: back to back for ~sustained_s seconds under the power cap (SURVEY §8d protocol);
     # the contract's `value` above is the K-step timed region
     sustained = None
@@ -432,13 +461,6 @@ def main():
                "d2h_bytes_per_step": int(Ch.numel()) * 4 * world, "ms_per_step": te,
                "api": "paper_2011_11188_b200.dist.sgemm_2d (pinned host blocks, max over ranks)"}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        try:
-            cpu = cpu_oracle_sample(A.cpu().numpy(), B.cpu().numpy(), args.terms, args.cpu_target_s)
-        except Exception as ex:   # reported, never silently replaced
-            cpu = {"value": None, "error": repr(ex)}
-
     if rank == 0:
         line = {
             "metric": "split-FP16 SGEMM effective TFLOPS (2MNK/t)",
@@ -450,6 +472,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "sustained": sustained,
+            "accuracy": (cpu or {}).get("accuracy"),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
