@@ -153,3 +153,42 @@ def test_canaries_around_output_and_workspace(h, M, N, K, kw):
     finally:
         h._ws = None
         h._ensure_ws(256)
+
+
+def test_ex_error_paths(h):
+    import ctypes
+
+    import paper_2011_11188_b200.split3 as s3
+
+    A = torch.ones((64, 32), device="cuda")
+    B = torch.ones((32, 48), device="cuda")
+    PB = h.presplit(B, role=1)
+    PA = h.presplit(A, role=0)
+    with pytest.raises(ValueError):                      # planes split for the other role
+        h.sgemm_ex(PB, B)
+    with pytest.raises(s3.Split3Error) as ei:            # bf16x3 takes fp32 operands only
+        h.sgemm_ex(A, PB, bf16x3=True)
+    assert ei.value.status == s3.ERR_NOT_IMPLEMENTED
+    with pytest.raises(s3.Split3Error) as ei:            # exclusive flags
+        h.sgemm_ex(A, B, bf16x3=True, four_term=True)
+    assert ei.value.status == s3.ERR_INVALID_VALUE
+    lib = s3.load()
+    hi = torch.empty((48, 32), dtype=torch.int16, device="cuda")
+    sx = torch.zeros(1, dtype=torch.int32, device="cuda")
+    # ldp not a multiple of 8 / smaller than K / bad role
+    assert lib.split3_presplit(h._h, 1, 32, 48, B.data_ptr(), 48, 0, hi.data_ptr(), hi.data_ptr(), 30, sx.data_ptr()) \
+        == s3.ERR_INVALID_VALUE
+    assert lib.split3_presplit(h._h, 2, 32, 48, B.data_ptr(), 48, 0, hi.data_ptr(), hi.data_ptr(), 32, sx.data_ptr()) \
+        == s3.ERR_INVALID_VALUE
+    assert lib.split3_presplit(h._h, 1, 32, 48, B.data_ptr(), 47, 0, hi.data_ptr(), hi.data_ptr(), 32, sx.data_ptr()) \
+        == s3.ERR_INVALID_VALUE
+    # a pre-split A with pre-split B works and equals the fp32 call
+    C = h.sgemm_ex(PA, PB)
+    assert torch.equal(C, h.sgemm(A, B))
+    # check-finite under bf16x3 reports the index in the stored matrix
+    A2 = A.clone()
+    A2[5, 7] = float("nan")
+    with pytest.raises(s3.NotFiniteError) as ei:
+        h.sgemm_ex(A2, B, bf16x3=True, check_finite=True)
+    assert ei.value.index == 5 * 32 + 7
+    del ctypes
