@@ -48,6 +48,16 @@ constexpr uint64_t kPolicyNormal = 0x1000000000000000ull;
 constexpr uint64_t kPolicyFirst = 0x12F0000000000000ull;
 constexpr uint64_t kPolicyLast = 0x14F0000000000000ull;
 
+#ifdef SPLIT3_EXP_TRACE
+// experiment only (tools/exp_ab.py trace): per-CTA cycle counters of the barrier waits
+__device__ unsigned long long g_trace[160][16];
+#define TRACE_T0() const long long _t0 = clock64()
+#define TRACE_ADD(slot) atomicAdd(&g_trace[blockIdx.x][slot], (unsigned long long)(clock64() - _t0))
+#else
+#define TRACE_T0()
+#define TRACE_ADD(slot)
+#endif
+
 // ------------------------------------------------------------------ PTX wrappers -------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -350,6 +360,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+#ifdef SPLIT3_EXP_TRACE
+    const long long _tkernel = clock64();
+#endif
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs; warp-uniform, one elected lane) =====
@@ -364,8 +377,18 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             if (wave_counter && idx > 0) {
                 int64_t active = num_units - idx * num_pairs;   // pairs with an idx-th unit
                 if (active > num_pairs) active = num_pairs;
+#ifdef SPLIT3_EXP_WAVE_SLACK
+                const unsigned wait_target = wave_target;   // everyone started the previous unit
+#endif
                 wave_target += 2u * (unsigned)active;
-                if (elect_one()) wave_sync(wave_counter, wave_target);
+#ifndef SPLIT3_EXP_WAVE_SLACK
+                const unsigned wait_target = wave_target;
+#endif
+                if (elect_one()) {
+                    TRACE_T0();
+                    wave_sync(wave_counter, wait_target);
+                    TRACE_ADD(8);
+                }
                 __syncwarp();
             }
             int64_t mb, nb;
@@ -373,7 +396,11 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             const int32_t y_a = (int32_t)(mb * 2 * BM + crank * BM);
             const int32_t y_b = (int32_t)(nb * BN_ + crank * BNH);
             for (int kb = kb_begin; kb < kb_end; kb++) {
-                mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+                {
+                    TRACE_T0();
+                    mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+                    if (lane == 0) TRACE_ADD(9);
+                }
                 const uint32_t fb = smem_u32(&full_bar[stage]);
                 uint8_t* st = smem + stage * STAGE_BYTES;
                 const int32_t x = kb * BK;
@@ -412,12 +439,17 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                 const uint32_t t_lo = tmem_base + COL_LO;
                 bool mid_ready = false;
                 for (int kb = kb_begin; kb < kb_end; kb++) {
-                    const bool chunk_start = ((kb - kb_begin) % promo_kb) == 0;
+                    const int rel = kb - kb_begin;
+                    const bool chunk_start = rel == 0 || (rel >= tune.first_kb && (rel - tune.first_kb) % promo_kb == 0);
                     if (chunk_start && kb > kb_begin) cc++;
                     const uint32_t hb = HB == 2 ? (cc & 1) : 0;
                     const uint32_t hphase = HB == 2 ? ((cc >> 1) & 1) : (cc & 1);
                     const uint32_t t_hi = tmem_base + hb * BN_;
-                    mbar_wait(smem_u32(&full_bar[stage]), phase);
+                    {
+                        TRACE_T0();
+                        mbar_wait(smem_u32(&full_bar[stage]), phase);
+                        TRACE_ADD(0);
+                    }
                     tc_fence_after();
                     uint8_t* st = smem + stage * STAGE_BYTES;
                     const uint64_t a1 = sdesc_sw128(smem_u32(st));
@@ -432,7 +464,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     auto issue_mid = [&]() {
                         if (!HAS_MID) return;
                         if (!mid_ready) {
+                            TRACE_T0();
                             mbar_wait(smem_u32(&mempty_bar[0]), (tc & 1) ^ 1);
+                            TRACE_ADD(1);
                             tc_fence_after();
                             mid_ready = true;
                         }
@@ -453,10 +487,13 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                         }
                         __syncwarp();
                     };
-                    const bool chunk_end = ((kb + 1 - kb_begin) % promo_kb) == 0 || kb + 1 == kb_end;
+                    const bool chunk_end = kb + 1 == kb_end ||
+                                           (rel + 1 >= tune.first_kb && (rel + 1 - tune.first_kb) % promo_kb == 0);
                     auto issue_hi = [&]() {
                         if (chunk_start) {
+                            TRACE_T0();
                             mbar_wait(smem_u32(&hempty_bar[hb]), hphase ^ 1);
+                            TRACE_ADD(2);
                             tc_fence_after();
                         }
                         if (elect_one()) {
@@ -502,16 +539,27 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             float master[NCOL];
 #pragma unroll
             for (int j = 0; j < NCOL; j++) master[j] = 0.0f;
-            for (int kb0 = kb_begin; kb0 < kb_end; kb0 += promo_kb, cc++) {
+            for (int kb0 = kb_begin; kb0 < kb_end; kb0 += (kb0 == kb_begin ? tune.first_kb : promo_kb), cc++) {
                 const uint32_t hb = HB == 2 ? (cc & 1) : 0;
                 const uint32_t hphase = HB == 2 ? ((cc >> 1) & 1) : (cc & 1);
-                mbar_wait(smem_u32(&hfull_bar[hb]), hphase);
+                {
+                    TRACE_T0();
+                    mbar_wait(smem_u32(&hfull_bar[hb]), hphase);
+                    if (warp == 2 && lane == 0) TRACE_ADD(3);
+                }
                 tc_fence_after();
-                promote_all<NCOL>(lane_base + hb * BN_, master);
+                {
+                    TRACE_T0();
+                    promote_all<NCOL>(lane_base + hb * BN_, master);
+                    if (warp == 2 && lane == 0) TRACE_ADD(4);
+                }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_leader(smem_u32(&hempty_bar[hb]));
             }
+#ifdef SPLIT3_EXP_TRACE
+            const long long _tend = clock64();
+#endif
             if (HAS_MID) {
                 mbar_wait(smem_u32(&mfull_bar[0]), tc & 1);
                 tc_fence_after();
@@ -564,6 +612,10 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             }
             const int64_t row = mb * 2 * BM + crank * BM + quad * 32 + lane;
             const int64_t col0 = nb * BN_ + half * NCOL;
+#ifdef SPLIT3_EXP_TRACE
+            if (warp == 2 && lane == 0) atomicAdd(&g_trace[blockIdx.x][5], (unsigned long long)(clock64() - _tend));
+            const long long _tst = clock64();
+#endif
             if (tma_store) {
                 // stage 32 rows x 32 columns per step (row = lane, 16-B chunks XOR-swizzled by
                 // row % 8 as the map's SWIZZLE_128B expects: 4 wavefronts per warp store), then one
@@ -586,6 +638,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                         bulk_commit();
                     }
                 }
+#ifdef SPLIT3_EXP_TRACE
+                if (warp == 2 && lane == 0) atomicAdd(&g_trace[blockIdx.x][6], (unsigned long long)(clock64() - _tst));
+#endif
                 continue;
             }
 #ifdef SPLIT3_EXP_NO_STORE
@@ -610,6 +665,16 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     }
 
     if (warp >= 2 && tma_store && lane == 0) bulk_wait0();   // the C stores have completed
+#ifdef SPLIT3_EXP_TRACE
+    if (threadIdx.x == 0) {
+        atomicAdd(&g_trace[blockIdx.x][7], (unsigned long long)(clock64() - _tkernel));
+        unsigned smid, nsmid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        asm volatile("mov.u32 %0, %%nsmid;" : "=r"(nsmid));
+        g_trace[blockIdx.x][10] = smid;
+        g_trace[blockIdx.x][11] = nsmid;
+    }
+#endif
     tc_fence_before();
     cluster_sync();
     if (warp == 1) {
@@ -673,9 +738,10 @@ bool make_c_map(CUtensorMap* map, float* C, int64_t M, int64_t N, int64_t ldc) {
     cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
     cuuint64_t strides[1] = {(cuuint64_t)(ldc * 4)};
     cuuint32_t box[2] = {32, 32};
+    const CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B;
     cuuint32_t estr[2] = {1, 1};
     return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -807,6 +873,7 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     const int promo = promo_kb > 0 ? promo_kb : kDefaultPromoKb;
     GemmTune tune;
     tune.group_m = tin.group_m > 0 ? tin.group_m : kDefaultGroupM;
+    tune.first_kb = kDefaultFirstKb > promo ? kDefaultFirstKb : promo;
     auto pol = [](int p) { return p == 1 ? kPolicyFirst : (p == 2 ? kPolicyLast : kPolicyNormal); };
     tune.pol_a = pol(tin.pol_a);
     tune.pol_b = pol(tin.pol_b);
@@ -838,3 +905,14 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
 }
 
 }  // namespace split3
+
+#ifdef SPLIT3_EXP_TRACE
+extern "C" int split3_exp_trace(unsigned long long* host, int reset) {
+    if (cudaMemcpyFromSymbol(host, split3::g_trace, sizeof(split3::g_trace)) != cudaSuccess) return 4;
+    if (reset) {
+        static unsigned long long zeros[160][16];
+        cudaMemcpyToSymbol(split3::g_trace, zeros, sizeof(zeros));
+    }
+    return 0;
+}
+#endif

@@ -37,6 +37,8 @@ import paper_2011_11188_b200 as s3  # noqa: E402
 from workloads import torch_matrix  # noqa: E402
 
 h = s3.Handle(0)
+if os.environ.get("EXP_WAVE") == "0":
+    h.set_wave_sync(False)
 A = torch_matrix("uniform", M, K, seed=0)
 B = torch_matrix("uniform", K, N, seed=1)
 C = torch.empty((M, N), device="cuda")
@@ -45,10 +47,42 @@ for _ in range(3):
 torch.cuda.synchronize()
 h.timing_enable(True)
 h.timing_read()
-reps = 20
+reps = int(os.environ.get("EXP_REPS", "20"))
 for _ in range(reps):
     h.sgemm(A, B, out=C)
 torch.cuda.synchronize()
 sp, gm, n = h.timing_read()
-print(json.dumps({"tag": tags[0], "lib": s3.split3.LIB_PATH, "M": M, "N": N, "K": K,
-                  "gemm_ms": gm / n, "fp16_tflops": 3 * 2.0 * M * N * K / (gm / n / 1e3) / 1e12}))
+rec = {"tag": tags[0], "lib": s3.split3.LIB_PATH, "M": M, "N": N, "K": K,
+       "gemm_ms": gm / n, "fp16_tflops": 3 * 2.0 * M * N * K / (gm / n / 1e3) / 1e12}
+if os.environ.get("EXP_ACC"):               # accuracy of this build vs fp64 (measurement only)
+    C64 = A.double() @ B.double()
+    rec["e64rel"] = float((C.double() - C64).norm() / C64.norm())
+    del C64
+lib = s3.load()
+if hasattr(lib, "split3_exp_trace"):           # experiment build with -DSPLIT3_EXP_TRACE
+    import ctypes
+
+    import numpy as np
+
+    buf = np.zeros((160, 16), np.uint64)
+    lib.split3_exp_trace(ctypes.c_void_p(buf.ctypes.data), 1)
+    h.sgemm(A, B, out=C)
+    torch.cuda.synchronize()
+    lib.split3_exp_trace(ctypes.c_void_p(buf.ctypes.data), 0)
+    leaders = buf[0:148:2].astype(np.float64)            # leader CTAs (MMA waits are recorded there)
+    tot = leaders[:, 7].mean()
+    names = ["mma_wait_full", "mma_wait_mempty", "mma_wait_hempty", "epi_wait_hfull", "epi_promote",
+             "epi_unit_end_combine", "epi_store_issue", "kernel", "prod_wave_sync", "prod_wait_empty"]
+    lanes = [32, 32, 32, 1, 1, 1, 1, 1, 1, 1]          # MMA-warp waits are counted by every lane
+    rec["trace_fraction_of_kernel_cycles"] = {nm: round(leaders[:, i].mean() / tot / lanes[i], 4)
+                                              for i, nm in enumerate(names) if nm != "kernel"}
+    rec["trace_wave_sync_max_cta"] = round(float((buf[:148, 8] / buf[:148, 7]).max()), 4)
+    rec["kernel_cycles"] = tot
+    if os.environ.get("EXP_DUMP"):
+        np.save(os.environ["EXP_DUMP"], buf)
+        h.sgemm(A, B, out=C)          # a second launch: is the per-CTA pattern systematic?
+        torch.cuda.synchronize()
+        lib.split3_exp_trace(ctypes.c_void_p(buf.ctypes.data), 1)
+        lib.split3_exp_trace(ctypes.c_void_p(buf.ctypes.data), 0)
+        np.save(os.environ["EXP_DUMP"].replace(".npy", "_b.npy"), buf)
+print(json.dumps(rec))
