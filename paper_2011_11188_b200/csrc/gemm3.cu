@@ -687,6 +687,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
 
 // Split-tile reduction: for each split tile t and element (r, c) of its 256 x BN block,
 // C = 2^(sA+sB) * sum_{s=0}^{S-1} P[s*nsplit + t][r][c]  (fixed slice order -> deterministic).
+// Launch: grid (2*BM / kReduceRows, nsplit), 256 threads; block (x, t) handles rows
+// [x*kReduceRows, +kReduceRows) of split tile t, one float4 column group per thread per row.
+constexpr int kReduceRows = 16;
 __global__ void __launch_bounds__(256) ksplit_reduce_kernel(const float* __restrict__ P, SplitPlan plan, int bn,
                                                             int64_t M, int64_t N, int group_m,
                                                             float* __restrict__ C, int64_t ldc,
@@ -696,19 +699,35 @@ __global__ void __launch_bounds__(256) ksplit_reduce_kernel(const float* __restr
     const bool fast = sAB >= -126 && sAB <= 127;
     const float f = fast ? __uint_as_float((unsigned)(sAB + 127) << 23) : 1.0f;
     const double fd = __longlong_as_double((long long)(sAB + 1023) << 52);
+    auto scale = [&](float a) { return fast ? a * f : __double2float_rn(__dmul_rn((double)a, fd)); };
     const int64_t blk = (int64_t)(2 * BM) * bn;
-    const int64_t total = plan.nsplit * blk;
+    const int64_t t = blockIdx.y;
     const int64_t num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + bn - 1) / bn;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t t = i / blk, e = i - t * blk;
-        const int64_t r = e / bn, c = e - r * bn;
-        int64_t mb, nb;
-        tile_coords(plan.whole + t, num_m, num_n, group_m, mb, nb);
-        const int64_t row = mb * 2 * BM + r, col = nb * bn + c;
+    int64_t mb, nb;
+    tile_coords(plan.whole + t, num_m, num_n, group_m, mb, nb);
+    const int groups = bn / 4;                       // float4 column groups per row
+    const int rows_per_pass = 256 / groups;
+    const int g = threadIdx.x % groups;
+    const int64_t col = nb * bn + 4 * g;
+    const bool vec = (ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(C) & 15u) == 0 && col + 4 <= N;
+    for (int r = blockIdx.x * kReduceRows + threadIdx.x / groups; r < (int)(blockIdx.x + 1) * kReduceRows;
+         r += rows_per_pass) {
+        const int64_t row = mb * 2 * BM + r;
         if (row >= M || col >= N) continue;
-        float acc = P[t * blk + e];
-        for (int s = 1; s < plan.slices; s++) acc = __fadd_rn(acc, P[((int64_t)s * plan.nsplit + t) * blk + e]);
-        C[row * ldc + col] = fast ? acc * f : __double2float_rn(__dmul_rn((double)acc, fd));
+        const int64_t e = (int64_t)r * bn + 4 * g;
+        float4 acc = *reinterpret_cast<const float4*>(P + t * blk + e);
+        for (int sl = 1; sl < plan.slices; sl++) {     // fixed slice order -> deterministic
+            const float4 v = *reinterpret_cast<const float4*>(P + ((int64_t)sl * plan.nsplit + t) * blk + e);
+            acc.x = __fadd_rn(acc.x, v.x); acc.y = __fadd_rn(acc.y, v.y);
+            acc.z = __fadd_rn(acc.z, v.z); acc.w = __fadd_rn(acc.w, v.w);
+        }
+        float* dst = C + row * ldc + col;
+        if (vec) {
+            *reinterpret_cast<float4*>(dst) = make_float4(scale(acc.x), scale(acc.y), scale(acc.z), scale(acc.w));
+        } else {
+            const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+            for (int j = 0; j < 4 && col + j < N; j++) dst[j] = scale(a[j]);
+        }
     }
 }
 
@@ -895,9 +914,8 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     if (r < 0) { *err = 4; return -1; }
     if (plan.slices > 1) {
         const int bn = terms == 4 ? 128 : 256;
-        int64_t blocks = (plan.nsplit * 256 * bn + 255) / 256;
-        if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
-        ksplit_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(partial, plan, bn, M, N, tune.group_m, C, ldc, d_sA, d_sB);
+        const dim3 grid((unsigned)(2 * BM / kReduceRows), (unsigned)plan.nsplit);
+        ksplit_reduce_kernel<<<grid, 256, 0, st>>>(partial, plan, bn, M, N, tune.group_m, C, ldc, d_sA, d_sB);
         if (cudaPeekAtLastError() != cudaSuccess) { *err = 4; return -1; }
         r += 1;
     }
