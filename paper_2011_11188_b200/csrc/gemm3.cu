@@ -360,6 +360,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();   // prologue above overlaps the predecessor's tail; no global access before here
 #ifdef SPLIT3_EXP_TRACE
     const long long _tkernel = clock64();
 #endif
@@ -695,6 +696,7 @@ __global__ void __launch_bounds__(256) ksplit_reduce_kernel(const float* __restr
                                                             float* __restrict__ C, int64_t ldc,
                                                             const int32_t* __restrict__ d_sA,
                                                             const int32_t* __restrict__ d_sB) {
+    pdl_enter();
     const int sAB = *d_sA + *d_sB;
     const bool fast = sAB >= -126 && sAB <= 127;
     const float f = fast ? __uint_as_float((unsigned)(sAB + 127) << 23) : 1.0f;
@@ -817,9 +819,10 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
         wave_base[0] = 0;
     }
     const unsigned base = (wave_base && !capturing) ? *wave_base : 0u;
-    gemm3_kernel<TERMS, BN_><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(a1, a2, b1, b2, a3, b3, mc, tma_store, (int)M, (int)N, (int)K,
-                                                               promo_kb, d_sA, d_sB, C, ldc, wave_counter, base,
-                                                               tune, plan, partial);
+    if (launch_k(gemm3_kernel<TERMS, BN_>, dim3((unsigned)grid), dim3(NUM_THREADS), SMEM_BYTES, st, a1, a2, b1, b2, a3,
+                 b3, mc, tma_store, (int)M, (int)N, (int)K, promo_kb, d_sA, d_sB, C, ldc, wave_counter, base, tune,
+                 plan, partial) != cudaSuccess)
+        return -1;
     if (wave_base && wave_counter && !capturing) {   // arrivals: one per CTA per unit index >= 1
         const int64_t pairs_launched = grid / 2;
         const int64_t extra = tiles > pairs_launched ? tiles - pairs_launched : 0;
@@ -915,7 +918,7 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     if (plan.slices > 1) {
         const int bn = terms == 4 ? 128 : 256;
         const dim3 grid((unsigned)(2 * BM / kReduceRows), (unsigned)plan.nsplit);
-        ksplit_reduce_kernel<<<grid, 256, 0, st>>>(partial, plan, bn, M, N, tune.group_m, C, ldc, d_sA, d_sB);
+        launch_k(ksplit_reduce_kernel, grid, dim3(256), 0, st, partial, plan, bn, M, N, tune.group_m, C, ldc, d_sA, d_sB);
         if (cudaPeekAtLastError() != cudaSuccess) { *err = 4; return -1; }
         r += 1;
     }

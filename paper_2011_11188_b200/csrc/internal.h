@@ -6,6 +6,45 @@
 
 namespace split3 {
 
+// ---- programmatic dependent launch ------------------------------------------------------
+// Every kernel of the split3_sgemm path is launched with programmatic stream serialization:
+// it may be scheduled while its predecessor in the stream drains, runs its prologue, and waits
+// in griddepcontrol.wait (full completion + memory flush of the predecessor) before its first
+// global-memory access.  Hides the launch gap between the 4-5 kernels of a call.
+#ifndef SPLIT3_PDL
+#define SPLIT3_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if SPLIT3_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#if SPLIT3_PDL
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+// wait for the predecessor, then let the successor be scheduled (small kernels)
+__device__ __forceinline__ void pdl_enter() {
+    pdl_wait();
+    pdl_trigger();
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = SPLIT3_PDL ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...);
+}
+
 // Padded plane leading dimension: a multiple of 8 elements (16 bytes, the TMA stride unit).
 inline int64_t plane_ld(int64_t k) { return ((k + 7) / 8) * 8; }
 

@@ -57,6 +57,7 @@ __device__ __forceinline__ void fold1(float x, long long idx, unsigned& m, long 
 template <bool VEC>
 __global__ void __launch_bounds__(256) maxabs_1d_kernel(const float* __restrict__ X, int64_t n,
                                                         float* d_max, long long* d_bad) {
+    pdl_enter();
     unsigned m = 0;
     long long bad = LLONG_MAX;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(256) maxabs_1d_kernel(const float* __restrict_
 __global__ void __launch_bounds__(256) maxabs2_1d_kernel(const float* __restrict__ X0, int64_t n0, float* d_max0,
                                                          const float* __restrict__ X1, int64_t n1, float* d_max1,
                                                          int gx, unsigned* partials, unsigned* ticket) {
+    pdl_enter();
     const bool first = (int)blockIdx.x < gx;
     const float* X = first ? X0 : X1;
     const int64_t n = first ? n0 : n1;
@@ -168,6 +170,7 @@ __global__ void __launch_bounds__(256) maxabs2_1d_kernel(const float* __restrict
 __global__ void __launch_bounds__(256) maxabs_2d_kernel(const float* __restrict__ X, int64_t rows,
                                                         int64_t cols, int64_t ld, float* d_max,
                                                         long long* d_bad) {
+    pdl_enter();
     unsigned m = 0;
     long long bad = LLONG_MAX;
     for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
@@ -207,6 +210,7 @@ __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ X,
                                                     uint16_t* __restrict__ hi,
                                                     uint16_t* __restrict__ lo, int64_t ldp,
                                                     int32_t* d_sexp) {
+    pdl_enter();
     const int s = scale_exp_dev(*d_max);
     const float f = pow2_neg(s);
     if (d_sexp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *d_sexp = s;
@@ -263,6 +267,7 @@ __global__ void __launch_bounds__(256) split_t_kernel(const float* __restrict__ 
                                                       uint16_t* __restrict__ hi,
                                                       uint16_t* __restrict__ lo, int64_t ldp,
                                                       int32_t* d_sexp) {
+    pdl_enter();
     constexpr int TK = 64, TN = 64;   // X rows (K) x X columns (N) per tile
     constexpr int TKP = TK + 2;       // halves per smem row (132 B: 4-B aligned, breaks the bank stride)
     __shared__ __align__(16) unsigned short s1[TN][TKP];
@@ -355,6 +360,7 @@ __global__ void __launch_bounds__(256) split_bf3_kernel(const float* __restrict_
                                                         int64_t ld, uint16_t* __restrict__ p1,
                                                         uint16_t* __restrict__ p2, uint16_t* __restrict__ p3,
                                                         int64_t ldp) {
+    pdl_enter();
     for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
         for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x) {
             unsigned short a, b, d;
@@ -370,6 +376,7 @@ __global__ void __launch_bounds__(256) split_bf3_t_kernel(const float* __restric
                                                           int64_t ld, uint16_t* __restrict__ p1,
                                                           uint16_t* __restrict__ p2, uint16_t* __restrict__ p3,
                                                           int64_t ldp) {
+    pdl_enter();
     __shared__ __align__(16) unsigned short sm[3][64][66];
     const int t = threadIdx.x;
     const int64_t ntr = (rows + 63) / 64, ntc = (cols + 63) / 64;
@@ -427,13 +434,13 @@ int launch_maxabs(cudaStream_t st, int64_t rows, int64_t cols, const float* X, i
         int64_t blocks = (n / 4 + 255) / 256;
         int64_t cap = (int64_t)num_sms * 8;
         int g = (int)(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
-        if (aligned16(X)) maxabs_1d_kernel<true><<<g, 256, 0, st>>>(X, n, d_max, d_bad);
-        else maxabs_1d_kernel<false><<<g, 256, 0, st>>>(X, n, d_max, d_bad);
+        if (aligned16(X)) launch_k(maxabs_1d_kernel<true>, dim3(g), dim3(256), 0, st, X, n, d_max, d_bad);
+        else launch_k(maxabs_1d_kernel<false>, dim3(g), dim3(256), 0, st, X, n, d_max, d_bad);
     } else {
         int64_t bx = (cols + 255) / 256;
         if (bx > 64) bx = 64;
         dim3 grid((unsigned)bx, (unsigned)grid_rows(rows, num_sms, bx));
-        maxabs_2d_kernel<<<grid, 256, 0, st>>>(X, rows, cols, ld, d_max, d_bad);
+        launch_k(maxabs_2d_kernel, grid, dim3(256), 0, st, X, rows, cols, ld, d_max, d_bad);
     }
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
@@ -461,8 +468,8 @@ int launch_maxabs2(cudaStream_t st, int64_t rows0, int64_t cols0, const float* X
     int64_t g1 = total_blocks - g0;
     if (g1 > need1) g1 = need1;
     if (g1 < 1) g1 = 1;
-    maxabs2_1d_kernel<<<(unsigned)(g0 + g1), 256, 0, st>>>(X0, n0, d_max0, X1, n1, d_max1, (int)g0,
-                                                           reinterpret_cast<unsigned*>(partials), ticket);
+    launch_k(maxabs2_1d_kernel, dim3((unsigned)(g0 + g1)), dim3(256), 0, st, X0, n0, d_max0, X1, n1, d_max1, (int)g0,
+             reinterpret_cast<unsigned*>(partials), ticket);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -475,8 +482,8 @@ int launch_split(cudaStream_t st, int64_t rows, int64_t cols, const float* X, in
     int64_t bx = (units + 255) / 256;
     if (bx > 64) bx = 64;
     dim3 grid((unsigned)bx, (unsigned)grid_rows(rows, num_sms, bx));
-    if (vec) split_kernel<true><<<grid, 256, 0, st>>>(X, rows, cols, ld, d_max, hi, lo, ldp, d_sexp);
-    else split_kernel<false><<<grid, 256, 0, st>>>(X, rows, cols, ld, d_max, hi, lo, ldp, d_sexp);
+    if (vec) launch_k(split_kernel<true>, grid, dim3(256), 0, st, X, rows, cols, ld, d_max, hi, lo, ldp, d_sexp);
+    else launch_k(split_kernel<false>, grid, dim3(256), 0, st, X, rows, cols, ld, d_max, hi, lo, ldp, d_sexp);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -486,12 +493,12 @@ int launch_split_bf16x3(cudaStream_t st, int64_t rows, int64_t cols, const float
     if (transpose) {
         int64_t tiles = ((rows + 63) / 64) * ((cols + 63) / 64);
         int64_t cap = (int64_t)num_sms * 8;
-        split_bf3_t_kernel<<<(unsigned)(tiles < cap ? tiles : cap), 256, 0, st>>>(X, rows, cols, ld, p1, p2, p3, ldp);
+        launch_k(split_bf3_t_kernel, dim3((unsigned)(tiles < cap ? tiles : cap)), dim3(256), 0, st, X, rows, cols, ld, p1, p2, p3, ldp);
     } else {
         int64_t bx = (cols + 255) / 256;
         if (bx > 64) bx = 64;
         dim3 grid((unsigned)bx, (unsigned)grid_rows(rows, num_sms, bx));
-        split_bf3_kernel<<<grid, 256, 0, st>>>(X, rows, cols, ld, p1, p2, p3, ldp);
+        launch_k(split_bf3_kernel, grid, dim3(256), 0, st, X, rows, cols, ld, p1, p2, p3, ldp);
     }
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
@@ -504,8 +511,8 @@ int launch_split_t(cudaStream_t st, int64_t rows, int64_t cols, const float* X, 
     int64_t tiles = ((rows + 63) / 64) * ((cols + 63) / 64);
     int64_t cap = (int64_t)num_sms * 8;
     int g = (int)(tiles < cap ? tiles : cap);
-    if (vec) split_t_kernel<true><<<g, 256, 0, st>>>(X, rows, cols, ld, d_max, hi, lo, ldp, d_sexp);
-    else split_t_kernel<false><<<g, 256, 0, st>>>(X, rows, cols, ld, d_max, hi, lo, ldp, d_sexp);
+    if (vec) launch_k(split_t_kernel<true>, dim3(g), dim3(256), 0, st, X, rows, cols, ld, d_max, hi, lo, ldp, d_sexp);
+    else launch_k(split_t_kernel<false>, dim3(g), dim3(256), 0, st, X, rows, cols, ld, d_max, hi, lo, ldp, d_sexp);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

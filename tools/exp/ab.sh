@@ -1,5 +1,5 @@
-for r in 1 2 3; do
-python tools/exp_ab.py time 4096 4096 4096 base pf4 pf8 pf16
-python tools/exp_ab.py time 16384 16384 4096 base pf4 pf8 pf16
-python tools/exp_ab.py time 16384 16384 16384 base pf8
+python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+for r in 1 2; do
+python tools/call_breakdown.py 1024 2048 4096 8192 2>&1 | grep "{" | sed 's/^/pdl /'
+SPLIT3_EXPERIMENT_LIB=tools/exp/libsplit3_nopdl.so python tools/call_breakdown.py 1024 2048 4096 8192 2>&1 | grep "{" | sed 's/^/nopdl /'
 done
