@@ -439,9 +439,11 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                 const uint32_t t_mid = tmem_base + COL_MID;
                 const uint32_t t_lo = tmem_base + COL_LO;
                 bool mid_ready = false;
+                int cpos = 0;      // k-block position inside the current D_hi chunk (no % on this path)
                 for (int kb = kb_begin; kb < kb_end; kb++) {
-                    const int rel = kb - kb_begin;
-                    const bool chunk_start = rel == 0 || (rel >= tune.first_kb && (rel - tune.first_kb) % promo_kb == 0);
+                    const bool chunk_start = cpos == 0;
+                    const bool chunk_end = cpos + 1 == promo_kb || kb + 1 == kb_end;
+                    cpos = cpos + 1 == promo_kb ? 0 : cpos + 1;
                     if (chunk_start && kb > kb_begin) cc++;
                     const uint32_t hb = HB == 2 ? (cc & 1) : 0;
                     const uint32_t hphase = HB == 2 ? ((cc >> 1) & 1) : (cc & 1);
@@ -488,8 +490,6 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                         }
                         __syncwarp();
                     };
-                    const bool chunk_end = kb + 1 == kb_end ||
-                                           (rel + 1 >= tune.first_kb && (rel + 1 - tune.first_kb) % promo_kb == 0);
                     auto issue_hi = [&]() {
                         if (chunk_start) {
                             TRACE_T0();
@@ -540,7 +540,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             float master[NCOL];
 #pragma unroll
             for (int j = 0; j < NCOL; j++) master[j] = 0.0f;
-            for (int kb0 = kb_begin; kb0 < kb_end; kb0 += (kb0 == kb_begin ? tune.first_kb : promo_kb), cc++) {
+            for (int kb0 = kb_begin; kb0 < kb_end; kb0 += promo_kb, cc++) {
                 const uint32_t hb = HB == 2 ? (cc & 1) : 0;
                 const uint32_t hphase = HB == 2 ? ((cc >> 1) & 1) : (cc & 1);
                 {
@@ -895,7 +895,6 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     const int promo = promo_kb > 0 ? promo_kb : kDefaultPromoKb;
     GemmTune tune;
     tune.group_m = tin.group_m > 0 ? tin.group_m : kDefaultGroupM;
-    tune.first_kb = kDefaultFirstKb > promo ? kDefaultFirstKb : promo;
     auto pol = [](int p) { return p == 1 ? kPolicyFirst : (p == 2 ? kPolicyLast : kPolicyNormal); };
     tune.pol_a = pol(tin.pol_a);
     tune.pol_b = pol(tin.pol_b);

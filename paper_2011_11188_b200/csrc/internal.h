@@ -73,16 +73,6 @@ int launch_split_t(cudaStream_t s, int64_t rows, int64_t cols, const float* X, i
 // D_hi promotion period in 64-wide k-blocks (4 MMAs each) when the handle sets none
 // (DESIGN.md §3 R9: measured truncating accumulation, promote every 8 MMAs).
 constexpr int kDefaultPromoKb = 2;
-// Length of the FIRST D_hi chunk of every unit, in k-blocks (>= the period): while the MMAs of
-// that chunk run, the epilogue finishes the previous unit's combine and C stores, which would
-// otherwise stall the second chunk on the single 256-column D_hi buffer.  A function of the
-// k-block index within the unit only, so results stay schedule-independent.
-// 0 = the promotion period (measured trade-off: a first chunk of 8 is 4 % faster
-// at K = 4096 but raises the error by 45 %, so the default keeps uniform chunks).
-#ifndef SPLIT3_FIRST_KB
-#define SPLIT3_FIRST_KB 0
-#endif
-constexpr int kDefaultFirstKb = SPLIT3_FIRST_KB;
 
 // GEMM scheduling knobs (results never depend on them).
 constexpr int kDefaultGroupM = 8;     // raster group, in pair m-blocks
@@ -93,7 +83,6 @@ struct GemmTuneIn {
 };
 struct GemmTune {
     int group_m;
-    int first_kb;                     // first D_hi chunk length (>= promo_kb)
     uint64_t pol_a, pol_b;
 };
 

@@ -1,2 +1,5 @@
-python tools/call_breakdown.py 4096 16384 2>&1 | grep "{" | sed 's/^/fused /'
-SPLIT3_FUSED_SCALE=0 python tools/call_breakdown.py 4096 16384 2>&1 | grep "{" | sed 's/^/twopass /'
+for r in 1 2 3; do
+python tools/exp_ab.py time 16384 16384 16384 base nofk old
+python tools/exp_ab.py time 16384 16384 4096 base nofk old
+python tools/exp_ab.py time 4096 4096 4096 base nofk old
+done
