@@ -1,7 +1,7 @@
 """Per-kernel breakdown of one split3_sgemm call (device durations via the torch profiler / CUPTI)
 next to the call's own event-timed duration, so launch gaps between the kernels show up.
 
-  python tools/call_breakdown.py 4096 8192 ...
+  python tools/call_breakdown.py 4096 8192 256x1024x1024 ...   (N or MxNxK)
 """
 import json
 import os
@@ -17,13 +17,15 @@ from workloads import torch_matrix  # noqa: E402
 
 h = s3.Handle(0)
 flush = torch.empty(256 * 2**20, dtype=torch.uint8, device="cuda")    # 256 MiB > L2
-for n in [int(x) for x in sys.argv[1:]] or [4096]:
-    A = torch_matrix("uniform", n, n, seed=0)
-    B = torch_matrix("uniform", n, n, seed=1)
-    C = torch.empty((n, n), device="cuda")
+for arg in sys.argv[1:] or ["4096"]:
+    M, N, K = (int(v) for v in arg.split("x")) if "x" in arg else (int(arg),) * 3
+    n = arg
+    A = torch_matrix("uniform", M, K, seed=0)
+    B = torch_matrix("uniform", K, N, seed=1)
+    C = torch.empty((M, N), device="cuda")
     for _ in range(5):
         h.sgemm(A, B, out=C)
-    reps = 20
+    reps = 50
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
     torch.cuda.synchronize()
     for i in range(reps):
@@ -46,4 +48,4 @@ for n in [int(x) for x in sys.argv[1:]] or [4096]:
     tot = sum(kern.values())
     print(json.dumps({"n": n, "call_ms_median": call_ms, "kernels_ms_per_call": {k[:60]: round(v, 4) for k, v in kern.items()},
                       "sum_kernels_ms": round(tot, 4), "gaps_ms": round(call_ms - tot, 4),
-                      "tflops_effective": 2.0 * n**3 / (call_ms / 1e3) / 1e12}))
+                      "tflops_effective": 2.0 * M * N * K / (call_ms / 1e3) / 1e12}))

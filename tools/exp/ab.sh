@@ -1,6 +1,5 @@
-for r in 1 2 3; do
-python tools/exp_ab.py time 16384 16384 16384 base mma1
-python tools/exp_ab.py time 16384 16384 4096 base mma1
-python tools/exp_ab.py time 4096 4096 4096 base mma1
+for r in 1 2; do
+python tools/call_breakdown.py 64 256x1024x1024 256x4096x4096 256x8192x8192 1024 1024x4096x4096 4096 2>&1 | grep "{" | sed 's/^/new /'
+SPLIT3_EXPERIMENT_LIB=tools/exp/libsplit3_prev.so python tools/call_breakdown.py 64 256x1024x1024 256x4096x4096 256x8192x8192 1024 1024x4096x4096 4096 2>&1 | grep "{" | sed 's/^/prev /'
+SPLIT3_EXPERIMENT_LIB=tools/exp/libsplit3_nosplit.so python tools/call_breakdown.py 64 256x1024x1024 256x4096x4096 256x8192x8192 1024 1024x4096x4096 4096 2>&1 | grep "{" | sed 's/^/nosplit /'
 done
-EXP_ACC=1 EXP_REPS=3 python tools/exp_ab.py time 4096 4096 4096 base mma1
