@@ -1,5 +1,7 @@
 for r in 1 2; do
-python tools/call_breakdown.py 64 256x1024x1024 256x4096x4096 256x8192x8192 1024 1024x4096x4096 4096 2>&1 | grep "{" | sed 's/^/new /'
-SPLIT3_EXPERIMENT_LIB=tools/exp/libsplit3_prev.so python tools/call_breakdown.py 64 256x1024x1024 256x4096x4096 256x8192x8192 1024 1024x4096x4096 4096 2>&1 | grep "{" | sed 's/^/prev /'
-SPLIT3_EXPERIMENT_LIB=tools/exp/libsplit3_nosplit.so python tools/call_breakdown.py 64 256x1024x1024 256x4096x4096 256x8192x8192 1024 1024x4096x4096 4096 2>&1 | grep "{" | sed 's/^/nosplit /'
+python tools/split_bench.py 16384 | sed 's/^/base /'
+SPLIT3_EXPERIMENT_LIB=tools/exp/libsplit3_rot.so python tools/split_bench.py 16384 | sed 's/^/rot /'
+python tools/split_bench.py 4096 | sed 's/^/base /'
+SPLIT3_EXPERIMENT_LIB=tools/exp/libsplit3_rot.so python tools/split_bench.py 4096 | sed 's/^/rot /'
 done
+SPLIT3_EXPERIMENT_LIB=tools/exp/libsplit3_rot.so python -m pytest tests -x -q -m gpu -k "plane or split or transpose or presplit" 2>&1 | tail -2
