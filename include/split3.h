@@ -72,7 +72,9 @@ int split3_set_stream(split3_handle_t h, void *cuda_stream);
 int split3_sgemm_destroy(split3_handle_t h);
 
 /* Bytes of device workspace split3_sgemm / split3_sgemm_ex need for (M, N, K): 256 bytes of
- * scalars, the four FP16 planes with padded leading dimensions (a multiple of 8 elements) and,
+ * scalars, the four FP16 planes with padded leading dimensions (a multiple of 8 elements; B's
+ * region fits either its K-major N x K planes or the MN-major K x N planes a row-major B is split
+ * into) and,
  * when the problem has fewer 256-wide C tiles than CTA pairs, S*M*N floats of split-K partials
  * (S <= 16 slices of K, reduced in a fixed order: results are deterministic). */
 size_t split3_sgemm_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags);

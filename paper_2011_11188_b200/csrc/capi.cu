@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <new>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/split3.h"
@@ -28,6 +29,7 @@ struct split3_ctx {
     int last_launches = 0;
     int promo_kb = 0;   // 0 = library default
     int wave_sync = 1;  // GEMM wave lockstep hint (L2 locality)
+    int b_mn = 1;       // split a row-major fp32 B without a transpose (MN-major planes); env SPLIT3_B_MN=0: off
     split3::GemmTuneIn tune;
     unsigned wave_base[2] = {0, 0};   // running value of the device wave counter (d_counters[0]), launches
     unsigned* d_counters = nullptr;   // 256 B of device scratch owned by the handle
@@ -74,7 +76,7 @@ struct Carve {
     uint16_t* A2;
     uint16_t* B1t;
     uint16_t* B2t;
-    int64_t ldpa, ldpb;
+    int64_t ldpa, ldpb, ldpb_mn;
     size_t end;   // bytes used
 };
 
@@ -93,7 +95,9 @@ Carve carve(void* ws, int64_t M, int64_t N, int64_t K) {
     c.ldpb = plane_ld(K);
     size_t off = kScalarBytes;
     const size_t pa = align256((size_t)M * (size_t)c.ldpa * 2);
-    const size_t pb = align256((size_t)N * (size_t)c.ldpb * 2);
+    // B planes: K-major N x plane_ld(K), or MN-major K x plane_ld(N) (plain split of a row-major B)
+    c.ldpb_mn = plane_ld(N);
+    const size_t pb = align256(std::max((size_t)N * (size_t)c.ldpb, (size_t)K * (size_t)c.ldpb_mn) * 2);
     c.A1 = reinterpret_cast<uint16_t*>(b + off); off += pa;
     c.A2 = reinterpret_cast<uint16_t*>(b + off); off += pa;
     c.B1t = reinterpret_cast<uint16_t*>(b + off); off += pb;
@@ -106,7 +110,7 @@ size_t ws_bytes_for(int64_t M, int64_t N, int64_t K, bool planesA, bool planesB,
     if (M < 0 || N < 0 || K < 0) return 0;
     (void)planesA; (void)planesB;   // plane regions are always carved (fixed layout)
     size_t b = kScalarBytes + 2 * align256((size_t)M * (size_t)plane_ld(K) * 2) +
-               2 * align256((size_t)N * (size_t)plane_ld(K) * 2);
+               2 * align256(std::max((size_t)N * (size_t)plane_ld(K), (size_t)K * (size_t)plane_ld(N)) * 2);
     if (terms_for_partials) {
         const split3::SplitPlan p = split3::gemm3_split_plan(M, N, K, terms_for_partials, 148, 0);
         b += align256((size_t)split3::gemm3_partial_elems(p, terms_for_partials) * 4);
@@ -189,6 +193,7 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
         return SPLIT3_ERR_CUDA;
     }
     c->tune.wave_base = c->wave_base;
+    if (const char* e = getenv("SPLIT3_B_MN")) c->b_mn = atoi(e) != 0;
     *h = c;
     return SPLIT3_OK;
 }
@@ -488,7 +493,14 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
         if (st) return st;
         A1 = w.A1; A2 = w.A2; sA = w.sA; ldpa = w.ldpa;
     }
-    if (needB) {
+    const bool b_mn = needB && !B->trans && h->b_mn;   // MN-major B planes: no transposing split
+    if (b_mn) {
+        if ((n = split3::launch_split(h->stream, K, N, B->data, B->ld, w.maxB, w.B1t, w.B2t, w.ldpb_mn, w.sB,
+                                      h->num_sms)) < 0)
+            return SPLIT3_ERR_CUDA;
+        launches += n;
+        B1t = w.B1t; B2t = w.B2t; sB = w.sB; ldpb = w.ldpb_mn;
+    } else if (needB) {
         int st = split_operand(h, 1, K, N, B, w.maxB, w.B1t, w.B2t, w.ldpb, w.sB, &launches);
         if (st) return st;
         B1t = w.B1t; B2t = w.B2t; sB = w.sB; ldpb = w.ldpb;
@@ -504,7 +516,7 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     int err = 0;
     n = split3::launch_gemm3(h->stream, M, N, K, A1, A2, ldpa, sA, B1t, B2t, ldpb, sB, C, ldc, terms,
                              h->num_sms, h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune, partial,
-                             partial_elems, &err);
+                             partial_elems, &err, nullptr, nullptr, b_mn ? 1 : 0);
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
     launches += n;
@@ -708,7 +720,10 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
     if (cudaStreamWaitEvent(s0, h->ev_b, 0) != cudaSuccess) return SPLIT3_ERR_CUDA;
     if ((n = split3::launch_maxabs(s0, K, N, dB, N, w.maxB, nullptr, h->num_sms)) < 0) return SPLIT3_ERR_CUDA;
     launches += n;
-    if ((n = split3::launch_split_t(s0, K, N, dB, N, w.maxB, w.B1t, w.B2t, w.ldpb, w.sB, h->num_sms)) < 0)
+    const bool b_mn = h->b_mn != 0;      // MN-major B planes (plain split) unless disabled
+    const int64_t ldpb = b_mn ? w.ldpb_mn : w.ldpb;
+    if ((n = b_mn ? split3::launch_split(s0, K, N, dB, N, w.maxB, w.B1t, w.B2t, ldpb, w.sB, h->num_sms)
+                  : split3::launch_split_t(s0, K, N, dB, N, w.maxB, w.B1t, w.B2t, ldpb, w.sB, h->num_sms)) < 0)
         return SPLIT3_ERR_CUDA;
     launches += n;
     // GEMM in row blocks (multiples of the 256-row pair tile); copy each block out as it completes
@@ -723,8 +738,9 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
         const int64_t mr = (M - r0 < rows_per) ? M - r0 : rows_per;
         int err = 0;
         n = split3::launch_gemm3(s0, mr, N, K, w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa, w.ldpa, w.sA, w.B1t, w.B2t,
-                                 w.ldpb, w.sB, dC + r0 * N, N, terms_of(flags), h->num_sms, h->promo_kb,
-                                 h->wave_sync ? h->d_counters : nullptr, h->tune, nullptr, 0, &err);
+                                 ldpb, w.sB, dC + r0 * N, N, terms_of(flags), h->num_sms, h->promo_kb,
+                                 h->wave_sync ? h->d_counters : nullptr, h->tune, nullptr, 0, &err, nullptr, nullptr,
+                                 b_mn ? 1 : 0);
         if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
         launches += n;
         if (cudaEventRecord(h->ev_rows[b], s0) != cudaSuccess || cudaStreamWaitEvent(h->s_out, h->ev_rows[b], 0) != cudaSuccess ||

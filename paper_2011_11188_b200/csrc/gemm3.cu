@@ -211,6 +211,19 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
     return d;
 }
 
+// Smem descriptor of an MN-major (N-contiguous) SW128 operand: 64-element (128-B) rows along N,
+// 8 k-rows per 1024-B swizzle atom; SBO = 1024 B between 8-k groups, LBO = `lbo` bytes between
+// 64-wide N atoms (here: consecutive 64 x 64 TMA boxes).  One K = 16 MMA step = +2048 B.
+__device__ __forceinline__ uint64_t sdesc_mn_sw128(uint32_t saddr, uint32_t lbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);   // start address      [0,14)
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;  // LBO                [16,30)
+    d |= (uint64_t)(1024 >> 4) << 32;             // SBO = 1024 B       [32,46)
+    d |= (uint64_t)1 << 46;                       // descriptor version [46,48) = 1 (sm_100)
+    d |= (uint64_t)2 << 61;                       // layout: SWIZZLE_128B
+    return d;
+}
+
 // Instruction descriptor, kind::f16: A = B = F16, D = F32, both K-major, M x N.
 __host__ __device__ constexpr uint32_t make_idesc(int m, int n, bool bf16 = false) {
     return (1u << 4)                              // D format F32
@@ -276,7 +289,9 @@ __device__ __forceinline__ void promote_all(uint32_t taddr, float (&master)[NCOL
     }
 }
 
-template <int TERMS, int BN_>
+// BMN: the B planes are MN-major (K x N row-major, as split from a row-major K x N fp32 B without
+// a transpose); else K-major (N x K).
+template <int TERMS, int BN_, bool BMN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapA2,
              const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
@@ -301,7 +316,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     constexpr uint32_t COL_LO = COL_MID + BN_;
     static_assert(HB * BN_ + (HAS_MID ? BN_ : 0) + (TERMS == 4 ? BN_ : 0) <= 512, "TMEM budget");
     constexpr uint32_t TX_BYTES = 2u * (LOAD_LO ? STAGE_BYTES : TILE_A_BYTES + TILE_B_BYTES);
-    constexpr uint32_t IDESC = make_idesc(2 * BM, BN_, BF3);
+    constexpr uint32_t IDESC = make_idesc(2 * BM, BN_, BF3) | (BMN ? (1u << 16) : 0u);   // b_major
+    constexpr uint64_t DKB = BMN ? (2048 >> 4) : (32 >> 4);   // B descriptor step per K = 16
+    constexpr int MN_BOX_BYTES = 64 * BK * 2;                 // one 64 (N) x 64 (K) box
     constexpr int B_OFF = PL * TILE_A_BYTES;         // B planes follow the A planes in a stage
     constexpr int NCOL = BN_ / 2;                    // columns per epilogue warp (2 warps per quadrant)
     constexpr uint32_t EPI_ARRIVALS = 2 * NUM_EPI_WARPS;
@@ -406,16 +423,27 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                 uint8_t* st = smem + stage * STAGE_BYTES;
                 const int32_t x = kb * BK;
                 if (elect_one()) {
+                    // K-major B: one 64 (K) x BNH (N) box; MN-major B: BNH/64 boxes of 64 (N) x 64 (K)
+                    auto load_b = [&](int off, const CUtensorMap* map) {
+                        if (BMN) {
+#pragma unroll
+                            for (int h = 0; h < BNH / 64; h++)
+                                tma_load_2d_pair(smem_u32(st + off + h * MN_BOX_BYTES), map, fb, y_b + 64 * h, x,
+                                                 tune.pol_b);
+                        } else {
+                            tma_load_2d_pair(smem_u32(st + off), map, fb, x, y_b, tune.pol_b);
+                        }
+                    };
                     if (leader) mbar_expect_tx(fb, TX_BYTES);
                     tma_load_2d_pair(smem_u32(st), &mapA1, fb, x, y_a, tune.pol_a);
-                    tma_load_2d_pair(smem_u32(st + B_OFF), &mapB1, fb, x, y_b, tune.pol_b);
+                    load_b(B_OFF, &mapB1);
                     if (LOAD_LO) {
                         tma_load_2d_pair(smem_u32(st + TILE_A_BYTES), &mapA2, fb, x, y_a, tune.pol_a);
-                        tma_load_2d_pair(smem_u32(st + B_OFF + TILE_B_BYTES), &mapB2, fb, x, y_b, tune.pol_b);
+                        load_b(B_OFF + TILE_B_BYTES, &mapB2);
                     }
                     if (BF3) {
                         tma_load_2d_pair(smem_u32(st + 2 * TILE_A_BYTES), &mapA3, fb, x, y_a, tune.pol_a);
-                        tma_load_2d_pair(smem_u32(st + B_OFF + 2 * TILE_B_BYTES), &mapB3, fb, x, y_b, tune.pol_b);
+                        load_b(B_OFF + 2 * TILE_B_BYTES, &mapB3);
                     }
                 }
                 __syncwarp();
@@ -458,9 +486,12 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     const uint64_t a1 = sdesc_sw128(smem_u32(st));
                     const uint64_t a2 = sdesc_sw128(smem_u32(st + TILE_A_BYTES));
                     const uint64_t a3 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES));
-                    const uint64_t b1 = sdesc_sw128(smem_u32(st + B_OFF));
-                    const uint64_t b2 = sdesc_sw128(smem_u32(st + B_OFF + TILE_B_BYTES));
-                    const uint64_t b3 = sdesc_sw128(smem_u32(st + B_OFF + 2 * TILE_B_BYTES));
+                    auto bdesc = [&](int off) {
+                        return BMN ? sdesc_mn_sw128(smem_u32(st + off), MN_BOX_BYTES) : sdesc_sw128(smem_u32(st + off));
+                    };
+                    const uint64_t b1 = bdesc(B_OFF);
+                    const uint64_t b2 = bdesc(B_OFF + TILE_B_BYTES);
+                    const uint64_t b3 = bdesc(B_OFF + 2 * TILE_B_BYTES);
                     // D_hi first at both ends of a unit: at the start the epilogue frees D_hi before
                     // D_mid; at the end the last D_hi drain overlaps the last D_mid MMAs
                     const bool hi_first = kb == kb_begin || kb + 1 == kb_end;
@@ -476,15 +507,15 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                         if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < BK / 16; k++) {
-                                const uint64_t dk = (uint64_t)(2 * k);
+                                const uint64_t dk = (uint64_t)(2 * k), dkb = DKB * k;
                                 const uint32_t acc = (kb > kb_begin || k > 0) ? 1u : 0u;
-                                mma_pair(t_mid, a1 + dk, b2 + dk, IDESC, acc);
-                                mma_pair(t_mid, a2 + dk, b1 + dk, IDESC, 1u);
-                                if (TERMS == 4) mma_pair(t_lo, a2 + dk, b2 + dk, IDESC, acc);
+                                mma_pair(t_mid, a1 + dk, b2 + dkb, IDESC, acc);
+                                mma_pair(t_mid, a2 + dk, b1 + dkb, IDESC, 1u);
+                                if (TERMS == 4) mma_pair(t_lo, a2 + dk, b2 + dkb, IDESC, acc);
                                 if (BF3) {          // the 2^-16-weighted products share D_mid
-                                    mma_pair(t_mid, a1 + dk, b3 + dk, IDESC, 1u);
-                                    mma_pair(t_mid, a2 + dk, b2 + dk, IDESC, 1u);
-                                    mma_pair(t_mid, a3 + dk, b1 + dk, IDESC, 1u);
+                                    mma_pair(t_mid, a1 + dk, b3 + dkb, IDESC, 1u);
+                                    mma_pair(t_mid, a2 + dk, b2 + dkb, IDESC, 1u);
+                                    mma_pair(t_mid, a3 + dk, b1 + dkb, IDESC, 1u);
                                 }
                             }
                         }
@@ -500,8 +531,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                         if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < BK / 16; k++) {
-                                const uint64_t dk = (uint64_t)(2 * k);
-                                mma_pair(t_hi, a1 + dk, b1 + dk, IDESC, (!chunk_start || k > 0) ? 1u : 0u);
+                                const uint64_t dk = (uint64_t)(2 * k), dkb = DKB * k;
+                                mma_pair(t_hi, a1 + dk, b1 + dkb, IDESC, (!chunk_start || k > 0) ? 1u : 0u);
                             }
                             // D_hi chunk ready: the commit covers only MMAs issued so far, so with
                             // D_hi first the drain starts while this k-block's D_mid MMAs run
@@ -781,7 +812,7 @@ bool make_plane_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K,
     return r == CUDA_SUCCESS;
 }
 
-template <int TERMS, int BN_>
+template <int TERMS, int BN_, bool BMN>
 int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap& a1,
              const CUtensorMap& a2, const CUtensorMap& b1, const CUtensorMap& b2, const CUtensorMap& a3,
              const CUtensorMap& b3, const CUtensorMap& mc, int tma_store,
@@ -795,7 +826,7 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
     if (cudaGetDevice(&dev) != cudaSuccess) return -1;
     const uint64_t bit = 1ull << (dev & 63);
     if (!(attr_set.load() & bit)) {
-        if (cudaFuncSetAttribute(gemm3_kernel<TERMS, BN_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(gemm3_kernel<TERMS, BN_, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  SMEM_BYTES) != cudaSuccess)
             return -1;
         attr_set.fetch_or(bit);
@@ -819,7 +850,7 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
         wave_base[0] = 0;
     }
     const unsigned base = (wave_base && !capturing) ? *wave_base : 0u;
-    if (launch_k(gemm3_kernel<TERMS, BN_>, dim3((unsigned)grid), dim3(NUM_THREADS), SMEM_BYTES, st, a1, a2, b1, b2, a3,
+    if (launch_k(gemm3_kernel<TERMS, BN_, BMN>, dim3((unsigned)grid), dim3(NUM_THREADS), SMEM_BYTES, st, a1, a2, b1, b2, a3,
                  b3, mc, tma_store, (int)M, (int)N, (int)K, promo_kb, d_sA, d_sB, C, ldc, wave_counter, base, tune,
                  plan, partial) != cudaSuccess)
         return -1;
@@ -870,14 +901,20 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
                  const uint16_t* A2, int64_t ldpa, const int32_t* d_sA, const uint16_t* B1t,
                  const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB, float* C, int64_t ldc,
                  int terms, int num_sms, int promo_kb, unsigned* wave_counter, const GemmTuneIn& tin,
-                 float* partial, int64_t partial_elems, int* err, const uint16_t* A3, const uint16_t* B3t) {
+                 float* partial, int64_t partial_elems, int* err, const uint16_t* A3, const uint16_t* B3t,
+                 int b_mn) {
     unsigned* wave_base = wave_counter ? tin.wave_base : nullptr;
     CUtensorMap ma1, ma2, mb1, mb2, ma3, mb3;
     const uint16_t* A2e = terms == 1 ? A1 : A2;
     const uint16_t* B2e = terms == 1 ? B1t : B2t;
     const int bnh = (terms == 4 ? 128 : 256) / 2;
+    // B planes: K-major N x K (box 64 K x bnh N), or MN-major K x N (box 64 N x 64 K, bnh/64 per plane)
+    auto map_b = [&](CUtensorMap* m, const uint16_t* p) {
+        return b_mn ? make_plane_map(m, p, K, N, ldpb, BK) : make_plane_map(m, p, N, K, ldpb, bnh);
+    };
+    if (b_mn && terms == 6) { *err = 1; return -1; }   // not instantiated: bf16 x 3 uses K-major B
     if (!make_plane_map(&ma1, A1, M, K, ldpa, BM) || !make_plane_map(&ma2, A2e, M, K, ldpa, BM) ||
-        !make_plane_map(&mb1, B1t, N, K, ldpb, bnh) || !make_plane_map(&mb2, B2e, N, K, ldpb, bnh)) {
+        !map_b(&mb1, B1t) || !map_b(&mb2, B2e)) {
         *err = 4;   // SPLIT3_ERR_CUDA
         return -1;
     }
@@ -906,13 +943,13 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     }
     int r;
     if (terms == 1)
-        r = launch_t<1, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
+        r = b_mn ? launch_t<1, 256, true>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial) : launch_t<1, 256, false>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
     else if (terms == 4)
-        r = launch_t<4, 128>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
+        r = b_mn ? launch_t<4, 128, true>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial) : launch_t<4, 128, false>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
     else if (terms == 6)
-        r = launch_t<6, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
+        r = launch_t<6, 256, false>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
     else
-        r = launch_t<3, 256>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
+        r = b_mn ? launch_t<3, 256, true>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial) : launch_t<3, 256, false>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
     if (r < 0) { *err = 4; return -1; }
     if (plan.slices > 1) {
         const int bn = terms == 4 ? 128 : 256;
