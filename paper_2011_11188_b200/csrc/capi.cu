@@ -123,22 +123,25 @@ size_t ws_size(int64_t M, int64_t N, int64_t K) { return ws_bytes_for(M, N, K, t
 // bf16 x 3: three planes per operand (scalars block as usual; sA = sB stay 0: no scale)
 struct CarveBF3 {
     uint16_t *A[3], *B[3];
-    int64_t ldp;
+    int64_t ldp, ldpb_mn;
     size_t end;
 };
 CarveBF3 carve_bf3(void* ws, int64_t M, int64_t N, int64_t K) {
     CarveBF3 c;
     uint8_t* b = static_cast<uint8_t*>(ws);
     c.ldp = plane_ld(K);
+    c.ldpb_mn = plane_ld(N);
     size_t off = kScalarBytes;
-    const size_t pa = align256((size_t)M * (size_t)c.ldp * 2), pb = align256((size_t)N * (size_t)c.ldp * 2);
+    const size_t pa = align256((size_t)M * (size_t)c.ldp * 2);
+    const size_t pb = align256(std::max((size_t)N * (size_t)c.ldp, (size_t)K * (size_t)c.ldpb_mn) * 2);
     for (int i = 0; i < 3; i++) { c.A[i] = reinterpret_cast<uint16_t*>(b + off); off += pa; }
     for (int i = 0; i < 3; i++) { c.B[i] = reinterpret_cast<uint16_t*>(b + off); off += pb; }
     c.end = off;
     return c;
 }
 size_t ws_bytes_bf3(int64_t M, int64_t N, int64_t K, bool partials) {
-    size_t b = kScalarBytes + 3 * align256((size_t)M * (size_t)plane_ld(K) * 2) + 3 * align256((size_t)N * (size_t)plane_ld(K) * 2);
+    size_t b = kScalarBytes + 3 * align256((size_t)M * (size_t)plane_ld(K) * 2) +
+               3 * align256(std::max((size_t)N * (size_t)plane_ld(K), (size_t)K * (size_t)plane_ld(N)) * 2);
     if (partials) b += align256((size_t)split3::gemm3_partial_elems(split3::gemm3_split_plan(M, N, K, 6, 148, 0), 6) * 4);
     return b;
 }
@@ -382,6 +385,7 @@ static int sgemm_bf16x3(split3_ctx* h, int64_t M, int64_t N, int64_t K, const sp
         if (!ev0 || !ev1 || !ev2) return SPLIT3_ERR_CUDA;
         record(h, ev0);
     }
+    const bool b_mn = !B->trans && h->b_mn;
     {   // role A: planes M x K (transposing split iff transA); role B: planes N x K (iff !transB)
         const int64_t ra = A->trans ? K : M, ca = A->trans ? M : K;
         if ((n = split3::launch_split_bf16x3(h->stream, ra, ca, A->data, A->ld, w.A[0], w.A[1], w.A[2], w.ldp,
@@ -389,8 +393,9 @@ static int sgemm_bf16x3(split3_ctx* h, int64_t M, int64_t N, int64_t K, const sp
             return SPLIT3_ERR_CUDA;
         launches += n;
         const int64_t rb = B->trans ? N : K, cb = B->trans ? K : N;
-        if ((n = split3::launch_split_bf16x3(h->stream, rb, cb, B->data, B->ld, w.B[0], w.B[1], w.B[2], w.ldp,
-                                             !B->trans, h->num_sms)) < 0)
+        // a row-major K x N B: MN-major K x N planes without a transpose (as in the FP16 path)
+        if ((n = split3::launch_split_bf16x3(h->stream, rb, cb, B->data, B->ld, w.B[0], w.B[1], w.B[2],
+                                             b_mn ? w.ldpb_mn : w.ldp, b_mn ? 0 : !B->trans, h->num_sms)) < 0)
             return SPLIT3_ERR_CUDA;
         launches += n;
     }
@@ -399,9 +404,10 @@ static int sgemm_bf16x3(split3_ctx* h, int64_t M, int64_t N, int64_t K, const sp
     size_t reserved = ws_bytes_bf3(M, N, K, true) - w.end;
     if (reserved > h->ws_bytes - w.end) reserved = h->ws_bytes - w.end;
     int err = 0;
-    n = split3::launch_gemm3(h->stream, M, N, K, w.A[0], w.A[1], w.ldp, sc.sA, w.B[0], w.B[1], w.ldp, sc.sB, C, ldc,
-                             6, h->num_sms, h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune, partial,
-                             (int64_t)(reserved / 4), &err, w.A[2], w.B[2]);
+    n = split3::launch_gemm3(h->stream, M, N, K, w.A[0], w.A[1], w.ldp, sc.sA, w.B[0], w.B[1],
+                             b_mn ? w.ldpb_mn : w.ldp, sc.sB, C, ldc, 6, h->num_sms, h->promo_kb,
+                             h->wave_sync ? h->d_counters : nullptr, h->tune, partial, (int64_t)(reserved / 4), &err,
+                             w.A[2], w.B[2], b_mn ? 1 : 0);
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
     h->last_launches = launches + n;

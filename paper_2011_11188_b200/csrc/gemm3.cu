@@ -912,13 +912,12 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     auto map_b = [&](CUtensorMap* m, const uint16_t* p) {
         return b_mn ? make_plane_map(m, p, K, N, ldpb, BK) : make_plane_map(m, p, N, K, ldpb, bnh);
     };
-    if (b_mn && terms == 6) { *err = 1; return -1; }   // not instantiated: bf16 x 3 uses K-major B
     if (!make_plane_map(&ma1, A1, M, K, ldpa, BM) || !make_plane_map(&ma2, A2e, M, K, ldpa, BM) ||
         !map_b(&mb1, B1t) || !map_b(&mb2, B2e)) {
         *err = 4;   // SPLIT3_ERR_CUDA
         return -1;
     }
-    if (terms == 6 && (!A3 || !B3t || !make_plane_map(&ma3, A3, M, K, ldpa, BM) || !make_plane_map(&mb3, B3t, N, K, ldpb, bnh))) {
+    if (terms == 6 && (!A3 || !B3t || !make_plane_map(&ma3, A3, M, K, ldpa, BM) || !map_b(&mb3, B3t))) {
         *err = 4;
         return -1;
     }
@@ -947,7 +946,7 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     else if (terms == 4)
         r = b_mn ? launch_t<4, 128, true>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial) : launch_t<4, 128, false>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
     else if (terms == 6)
-        r = launch_t<6, 256, false>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
+        r = b_mn ? launch_t<6, 256, true>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial) : launch_t<6, 256, false>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
     else
         r = b_mn ? launch_t<3, 256, true>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial) : launch_t<3, 256, false>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
     if (r < 0) { *err = 4; return -1; }

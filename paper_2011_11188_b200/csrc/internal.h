@@ -99,7 +99,7 @@ int64_t gemm3_partial_elems(const SplitPlan& p, int terms);   // floats of parti
 
 // terms: 1, 3, 4, or 6 (= bf16 x 3: planes A1..A3, B1t..B3t, 6 products, no scale).
 // b_mn: the B planes are MN-major, K x N row-major with leading dimension ldpb >= N (the plain
-// split of a row-major K x N B); else K-major N x K with ldpb >= K.  Not for terms == 6.  `partial` (may be NULL: no split-K) holds partial_elems floats.
+// split of a row-major K x N B); else K-major N x K with ldpb >= K.  `partial` (may be NULL: no split-K) holds partial_elems floats.
 // Returns kernels launched (1, or 2 with the split-K reduction) or -1 (*err set to a status).
 int launch_gemm3(cudaStream_t s, int64_t M, int64_t N, int64_t K,
                  const uint16_t* A1, const uint16_t* A2, int64_t ldpa, const int32_t* d_sA,

@@ -37,7 +37,7 @@ def hk():
 
 @pytest.mark.parametrize("M,N,K", [(512, 512, 512), (300, 200, 500), (1000, 1030, 129), (257, 72, 4100),
                                    (64, 8, 64), (2048, 2048, 2048), (256, 8192, 1024)])
-@pytest.mark.parametrize("kw", [{}, {"four_term": True}, {"one_term": True}])
+@pytest.mark.parametrize("kw", [{}, {"four_term": True}, {"one_term": True}, {"bf16x3": True}])
 def test_b_mn_equals_k_major(hm, hk, M, N, K, kw):
     A = torch_matrix("uniform", M, K, seed=3)
     B = torch_matrix("loguni", K, N, seed=4)
