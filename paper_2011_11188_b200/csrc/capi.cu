@@ -29,7 +29,8 @@ struct split3_ctx {
     int last_launches = 0;
     int promo_kb = 0;   // 0 = library default
     int wave_sync = 1;  // GEMM wave lockstep hint (L2 locality)
-    int b_mn = 1;       // split a row-major fp32 B without a transpose (MN-major planes); env SPLIT3_B_MN=0: off
+    int mn_major = 1;   // MN-major planes for a row-major B / a transposed A (no transposing split);
+                        // env SPLIT3_MN_MAJOR=0: off (K-major planes, transposing split)
     split3::GemmTuneIn tune;
     unsigned wave_base[2] = {0, 0};   // running value of the device wave counter (d_counters[0]), launches
     unsigned* d_counters = nullptr;   // 256 B of device scratch owned by the handle
@@ -76,7 +77,7 @@ struct Carve {
     uint16_t* A2;
     uint16_t* B1t;
     uint16_t* B2t;
-    int64_t ldpa, ldpb, ldpb_mn;
+    int64_t ldpa, ldpb, ldpa_mn, ldpb_mn;
     size_t end;   // bytes used
 };
 
@@ -94,8 +95,10 @@ Carve carve(void* ws, int64_t M, int64_t N, int64_t K) {
     c.ldpa = plane_ld(K);
     c.ldpb = plane_ld(K);
     size_t off = kScalarBytes;
-    const size_t pa = align256((size_t)M * (size_t)c.ldpa * 2);
-    // B planes: K-major N x plane_ld(K), or MN-major K x plane_ld(N) (plain split of a row-major B)
+    // planes K-major (A: M x plane_ld(K), B: N x plane_ld(K)) or MN-major (A: K x plane_ld(M),
+    // B: K x plane_ld(N): the plain split of a stored A^T / row-major B); regions fit either
+    c.ldpa_mn = plane_ld(M);
+    const size_t pa = align256(std::max((size_t)M * (size_t)c.ldpa, (size_t)K * (size_t)c.ldpa_mn) * 2);
     c.ldpb_mn = plane_ld(N);
     const size_t pb = align256(std::max((size_t)N * (size_t)c.ldpb, (size_t)K * (size_t)c.ldpb_mn) * 2);
     c.A1 = reinterpret_cast<uint16_t*>(b + off); off += pa;
@@ -109,7 +112,7 @@ Carve carve(void* ws, int64_t M, int64_t N, int64_t K) {
 size_t ws_bytes_for(int64_t M, int64_t N, int64_t K, bool planesA, bool planesB, int terms_for_partials) {
     if (M < 0 || N < 0 || K < 0) return 0;
     (void)planesA; (void)planesB;   // plane regions are always carved (fixed layout)
-    size_t b = kScalarBytes + 2 * align256((size_t)M * (size_t)plane_ld(K) * 2) +
+    size_t b = kScalarBytes + 2 * align256(std::max((size_t)M * (size_t)plane_ld(K), (size_t)K * (size_t)plane_ld(M)) * 2) +
                2 * align256(std::max((size_t)N * (size_t)plane_ld(K), (size_t)K * (size_t)plane_ld(N)) * 2);
     if (terms_for_partials) {
         const split3::SplitPlan p = split3::gemm3_split_plan(M, N, K, terms_for_partials, 148, 0);
@@ -123,16 +126,17 @@ size_t ws_size(int64_t M, int64_t N, int64_t K) { return ws_bytes_for(M, N, K, t
 // bf16 x 3: three planes per operand (scalars block as usual; sA = sB stay 0: no scale)
 struct CarveBF3 {
     uint16_t *A[3], *B[3];
-    int64_t ldp, ldpb_mn;
+    int64_t ldp, ldpa_mn, ldpb_mn;
     size_t end;
 };
 CarveBF3 carve_bf3(void* ws, int64_t M, int64_t N, int64_t K) {
     CarveBF3 c;
     uint8_t* b = static_cast<uint8_t*>(ws);
     c.ldp = plane_ld(K);
+    c.ldpa_mn = plane_ld(M);
     c.ldpb_mn = plane_ld(N);
     size_t off = kScalarBytes;
-    const size_t pa = align256((size_t)M * (size_t)c.ldp * 2);
+    const size_t pa = align256(std::max((size_t)M * (size_t)c.ldp, (size_t)K * (size_t)c.ldpa_mn) * 2);
     const size_t pb = align256(std::max((size_t)N * (size_t)c.ldp, (size_t)K * (size_t)c.ldpb_mn) * 2);
     for (int i = 0; i < 3; i++) { c.A[i] = reinterpret_cast<uint16_t*>(b + off); off += pa; }
     for (int i = 0; i < 3; i++) { c.B[i] = reinterpret_cast<uint16_t*>(b + off); off += pb; }
@@ -140,7 +144,7 @@ CarveBF3 carve_bf3(void* ws, int64_t M, int64_t N, int64_t K) {
     return c;
 }
 size_t ws_bytes_bf3(int64_t M, int64_t N, int64_t K, bool partials) {
-    size_t b = kScalarBytes + 3 * align256((size_t)M * (size_t)plane_ld(K) * 2) +
+    size_t b = kScalarBytes + 3 * align256(std::max((size_t)M * (size_t)plane_ld(K), (size_t)K * (size_t)plane_ld(M)) * 2) +
                3 * align256(std::max((size_t)N * (size_t)plane_ld(K), (size_t)K * (size_t)plane_ld(N)) * 2);
     if (partials) b += align256((size_t)split3::gemm3_partial_elems(split3::gemm3_split_plan(M, N, K, 6, 148, 0), 6) * 4);
     return b;
@@ -196,7 +200,7 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
         return SPLIT3_ERR_CUDA;
     }
     c->tune.wave_base = c->wave_base;
-    if (const char* e = getenv("SPLIT3_B_MN")) c->b_mn = atoi(e) != 0;
+    if (const char* e = getenv("SPLIT3_MN_MAJOR")) c->mn_major = atoi(e) != 0;
     *h = c;
     return SPLIT3_OK;
 }
@@ -385,11 +389,12 @@ static int sgemm_bf16x3(split3_ctx* h, int64_t M, int64_t N, int64_t K, const sp
         if (!ev0 || !ev1 || !ev2) return SPLIT3_ERR_CUDA;
         record(h, ev0);
     }
-    const bool b_mn = !B->trans && h->b_mn;
-    {   // role A: planes M x K (transposing split iff transA); role B: planes N x K (iff !transB)
+    const bool b_mn = !B->trans && h->mn_major, a_mn = A->trans && h->mn_major;
+    {   // K-major planes (A: M x K, transposing split iff transA; B: N x K, iff !transB), or
+        // MN-major planes (no transpose) for a stored A^T / a row-major B
         const int64_t ra = A->trans ? K : M, ca = A->trans ? M : K;
-        if ((n = split3::launch_split_bf16x3(h->stream, ra, ca, A->data, A->ld, w.A[0], w.A[1], w.A[2], w.ldp,
-                                             A->trans, h->num_sms)) < 0)
+        if ((n = split3::launch_split_bf16x3(h->stream, ra, ca, A->data, A->ld, w.A[0], w.A[1], w.A[2],
+                                             a_mn ? w.ldpa_mn : w.ldp, a_mn ? 0 : A->trans, h->num_sms)) < 0)
             return SPLIT3_ERR_CUDA;
         launches += n;
         const int64_t rb = B->trans ? N : K, cb = B->trans ? K : N;
@@ -404,10 +409,10 @@ static int sgemm_bf16x3(split3_ctx* h, int64_t M, int64_t N, int64_t K, const sp
     size_t reserved = ws_bytes_bf3(M, N, K, true) - w.end;
     if (reserved > h->ws_bytes - w.end) reserved = h->ws_bytes - w.end;
     int err = 0;
-    n = split3::launch_gemm3(h->stream, M, N, K, w.A[0], w.A[1], w.ldp, sc.sA, w.B[0], w.B[1],
+    n = split3::launch_gemm3(h->stream, M, N, K, w.A[0], w.A[1], a_mn ? w.ldpa_mn : w.ldp, sc.sA, w.B[0], w.B[1],
                              b_mn ? w.ldpb_mn : w.ldp, sc.sB, C, ldc, 6, h->num_sms, h->promo_kb,
                              h->wave_sync ? h->d_counters : nullptr, h->tune, partial, (int64_t)(reserved / 4), &err,
-                             w.A[2], w.B[2], b_mn ? 1 : 0);
+                             w.A[2], w.B[2], (b_mn ? 1 : 0) | (a_mn ? 2 : 0));
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
     h->last_launches = launches + n;
@@ -494,12 +499,19 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     const uint16_t *A1 = A->hi, *A2 = A->lo, *B1t = B->hi, *B2t = B->lo;
     const int32_t *sA = A->d_sexp, *sB = B->d_sexp;
     int64_t ldpa = A->ldp, ldpb = B->ldp;
-    if (needA) {
+    const bool a_mn = needA && A->trans && h->mn_major;   // MN-major A planes: no transposing split
+    if (a_mn) {
+        if ((n = split3::launch_split(h->stream, K, M, A->data, A->ld, w.maxA, w.A1, w.A2, w.ldpa_mn, w.sA,
+                                      h->num_sms)) < 0)
+            return SPLIT3_ERR_CUDA;
+        launches += n;
+        A1 = w.A1; A2 = w.A2; sA = w.sA; ldpa = w.ldpa_mn;
+    } else if (needA) {
         int st = split_operand(h, 0, M, K, A, w.maxA, w.A1, w.A2, w.ldpa, w.sA, &launches);
         if (st) return st;
         A1 = w.A1; A2 = w.A2; sA = w.sA; ldpa = w.ldpa;
     }
-    const bool b_mn = needB && !B->trans && h->b_mn;   // MN-major B planes: no transposing split
+    const bool b_mn = needB && !B->trans && h->mn_major;   // MN-major B planes: no transposing split
     if (b_mn) {
         if ((n = split3::launch_split(h->stream, K, N, B->data, B->ld, w.maxB, w.B1t, w.B2t, w.ldpb_mn, w.sB,
                                       h->num_sms)) < 0)
@@ -522,7 +534,7 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     int err = 0;
     n = split3::launch_gemm3(h->stream, M, N, K, A1, A2, ldpa, sA, B1t, B2t, ldpb, sB, C, ldc, terms,
                              h->num_sms, h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune, partial,
-                             partial_elems, &err, nullptr, nullptr, b_mn ? 1 : 0);
+                             partial_elems, &err, nullptr, nullptr, (b_mn ? 1 : 0) | (a_mn ? 2 : 0));
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
     launches += n;
@@ -726,7 +738,7 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
     if (cudaStreamWaitEvent(s0, h->ev_b, 0) != cudaSuccess) return SPLIT3_ERR_CUDA;
     if ((n = split3::launch_maxabs(s0, K, N, dB, N, w.maxB, nullptr, h->num_sms)) < 0) return SPLIT3_ERR_CUDA;
     launches += n;
-    const bool b_mn = h->b_mn != 0;      // MN-major B planes (plain split) unless disabled
+    const bool b_mn = h->mn_major != 0;  // MN-major B planes (plain split) unless disabled
     const int64_t ldpb = b_mn ? w.ldpb_mn : w.ldpb;
     if ((n = b_mn ? split3::launch_split(s0, K, N, dB, N, w.maxB, w.B1t, w.B2t, ldpb, w.sB, h->num_sms)
                   : split3::launch_split_t(s0, K, N, dB, N, w.maxB, w.B1t, w.B2t, ldpb, w.sB, h->num_sms)) < 0)

@@ -289,9 +289,10 @@ __device__ __forceinline__ void promote_all(uint32_t taddr, float (&master)[NCOL
     }
 }
 
-// BMN: the B planes are MN-major (K x N row-major, as split from a row-major K x N fp32 B without
-// a transpose); else K-major (N x K).
-template <int TERMS, int BN_, bool BMN>
+// LAY bit 0 (BMN): the B planes are MN-major (K x N row-major, as split from a row-major K x N fp32
+// B without a transpose), else K-major (N x K); bit 1 (AMN): likewise A (K x M planes of a stored
+// K x M fp32 A = op(A)^T), else K-major (M x K).
+template <int TERMS, int BN_, int LAY>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapA2,
              const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
@@ -316,8 +317,10 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     constexpr uint32_t COL_LO = COL_MID + BN_;
     static_assert(HB * BN_ + (HAS_MID ? BN_ : 0) + (TERMS == 4 ? BN_ : 0) <= 512, "TMEM budget");
     constexpr uint32_t TX_BYTES = 2u * (LOAD_LO ? STAGE_BYTES : TILE_A_BYTES + TILE_B_BYTES);
-    constexpr uint32_t IDESC = make_idesc(2 * BM, BN_, BF3) | (BMN ? (1u << 16) : 0u);   // b_major
+    constexpr bool BMN = (LAY & 1) != 0, AMN = (LAY & 2) != 0;
+    constexpr uint32_t IDESC = make_idesc(2 * BM, BN_, BF3) | (AMN ? (1u << 15) : 0u) | (BMN ? (1u << 16) : 0u);
     constexpr uint64_t DKB = BMN ? (2048 >> 4) : (32 >> 4);   // B descriptor step per K = 16
+    constexpr uint64_t DKA = AMN ? (2048 >> 4) : (32 >> 4);   // A descriptor step per K = 16
     constexpr int MN_BOX_BYTES = 64 * BK * 2;                 // one 64 (N) x 64 (K) box
     constexpr int B_OFF = PL * TILE_A_BYTES;         // B planes follow the A planes in a stage
     constexpr int NCOL = BN_ / 2;                    // columns per epilogue warp (2 warps per quadrant)
@@ -434,15 +437,25 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                             tma_load_2d_pair(smem_u32(st + off), map, fb, x, y_b, tune.pol_b);
                         }
                     };
+                    auto load_a = [&](int off, const CUtensorMap* map) {
+                        if (AMN) {
+#pragma unroll
+                            for (int h = 0; h < BM / 64; h++)
+                                tma_load_2d_pair(smem_u32(st + off + h * MN_BOX_BYTES), map, fb, y_a + 64 * h, x,
+                                                 tune.pol_a);
+                        } else {
+                            tma_load_2d_pair(smem_u32(st + off), map, fb, x, y_a, tune.pol_a);
+                        }
+                    };
                     if (leader) mbar_expect_tx(fb, TX_BYTES);
-                    tma_load_2d_pair(smem_u32(st), &mapA1, fb, x, y_a, tune.pol_a);
+                    load_a(0, &mapA1);
                     load_b(B_OFF, &mapB1);
                     if (LOAD_LO) {
-                        tma_load_2d_pair(smem_u32(st + TILE_A_BYTES), &mapA2, fb, x, y_a, tune.pol_a);
+                        load_a(TILE_A_BYTES, &mapA2);
                         load_b(B_OFF + TILE_B_BYTES, &mapB2);
                     }
                     if (BF3) {
-                        tma_load_2d_pair(smem_u32(st + 2 * TILE_A_BYTES), &mapA3, fb, x, y_a, tune.pol_a);
+                        load_a(2 * TILE_A_BYTES, &mapA3);
                         load_b(B_OFF + 2 * TILE_B_BYTES, &mapB3);
                     }
                 }
@@ -483,9 +496,12 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     }
                     tc_fence_after();
                     uint8_t* st = smem + stage * STAGE_BYTES;
-                    const uint64_t a1 = sdesc_sw128(smem_u32(st));
-                    const uint64_t a2 = sdesc_sw128(smem_u32(st + TILE_A_BYTES));
-                    const uint64_t a3 = sdesc_sw128(smem_u32(st + 2 * TILE_A_BYTES));
+                    auto adesc = [&](int off) {
+                        return AMN ? sdesc_mn_sw128(smem_u32(st + off), MN_BOX_BYTES) : sdesc_sw128(smem_u32(st + off));
+                    };
+                    const uint64_t a1 = adesc(0);
+                    const uint64_t a2 = adesc(TILE_A_BYTES);
+                    const uint64_t a3 = adesc(2 * TILE_A_BYTES);
                     auto bdesc = [&](int off) {
                         return BMN ? sdesc_mn_sw128(smem_u32(st + off), MN_BOX_BYTES) : sdesc_sw128(smem_u32(st + off));
                     };
@@ -507,7 +523,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                         if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < BK / 16; k++) {
-                                const uint64_t dk = (uint64_t)(2 * k), dkb = DKB * k;
+                                const uint64_t dk = DKA * k, dkb = DKB * k;
                                 const uint32_t acc = (kb > kb_begin || k > 0) ? 1u : 0u;
                                 mma_pair(t_mid, a1 + dk, b2 + dkb, IDESC, acc);
                                 mma_pair(t_mid, a2 + dk, b1 + dkb, IDESC, 1u);
@@ -531,7 +547,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                         if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < BK / 16; k++) {
-                                const uint64_t dk = (uint64_t)(2 * k), dkb = DKB * k;
+                                const uint64_t dk = DKA * k, dkb = DKB * k;
                                 mma_pair(t_hi, a1 + dk, b1 + dkb, IDESC, (!chunk_start || k > 0) ? 1u : 0u);
                             }
                             // D_hi chunk ready: the commit covers only MMAs issued so far, so with
@@ -812,7 +828,7 @@ bool make_plane_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K,
     return r == CUDA_SUCCESS;
 }
 
-template <int TERMS, int BN_, bool BMN>
+template <int TERMS, int BN_, int LAY>
 int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap& a1,
              const CUtensorMap& a2, const CUtensorMap& b1, const CUtensorMap& b2, const CUtensorMap& a3,
              const CUtensorMap& b3, const CUtensorMap& mc, int tma_store,
@@ -826,7 +842,7 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
     if (cudaGetDevice(&dev) != cudaSuccess) return -1;
     const uint64_t bit = 1ull << (dev & 63);
     if (!(attr_set.load() & bit)) {
-        if (cudaFuncSetAttribute(gemm3_kernel<TERMS, BN_, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(gemm3_kernel<TERMS, BN_, LAY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  SMEM_BYTES) != cudaSuccess)
             return -1;
         attr_set.fetch_or(bit);
@@ -850,7 +866,7 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
         wave_base[0] = 0;
     }
     const unsigned base = (wave_base && !capturing) ? *wave_base : 0u;
-    if (launch_k(gemm3_kernel<TERMS, BN_, BMN>, dim3((unsigned)grid), dim3(NUM_THREADS), SMEM_BYTES, st, a1, a2, b1, b2, a3,
+    if (launch_k(gemm3_kernel<TERMS, BN_, LAY>, dim3((unsigned)grid), dim3(NUM_THREADS), SMEM_BYTES, st, a1, a2, b1, b2, a3,
                  b3, mc, tma_store, (int)M, (int)N, (int)K, promo_kb, d_sA, d_sB, C, ldc, wave_counter, base, tune,
                  plan, partial) != cudaSuccess)
         return -1;
@@ -902,8 +918,9 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
                  const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB, float* C, int64_t ldc,
                  int terms, int num_sms, int promo_kb, unsigned* wave_counter, const GemmTuneIn& tin,
                  float* partial, int64_t partial_elems, int* err, const uint16_t* A3, const uint16_t* B3t,
-                 int b_mn) {
+                 int mn) {
     unsigned* wave_base = wave_counter ? tin.wave_base : nullptr;
+    const bool b_mn = (mn & 1) != 0, a_mn = (mn & 2) != 0;
     CUtensorMap ma1, ma2, mb1, mb2, ma3, mb3;
     const uint16_t* A2e = terms == 1 ? A1 : A2;
     const uint16_t* B2e = terms == 1 ? B1t : B2t;
@@ -912,12 +929,14 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     auto map_b = [&](CUtensorMap* m, const uint16_t* p) {
         return b_mn ? make_plane_map(m, p, K, N, ldpb, BK) : make_plane_map(m, p, N, K, ldpb, bnh);
     };
-    if (!make_plane_map(&ma1, A1, M, K, ldpa, BM) || !make_plane_map(&ma2, A2e, M, K, ldpa, BM) ||
-        !map_b(&mb1, B1t) || !map_b(&mb2, B2e)) {
+    auto map_a = [&](CUtensorMap* m, const uint16_t* p) {
+        return a_mn ? make_plane_map(m, p, K, M, ldpa, BK) : make_plane_map(m, p, M, K, ldpa, BM);
+    };
+    if (!map_a(&ma1, A1) || !map_a(&ma2, A2e) || !map_b(&mb1, B1t) || !map_b(&mb2, B2e)) {
         *err = 4;   // SPLIT3_ERR_CUDA
         return -1;
     }
-    if (terms == 6 && (!A3 || !B3t || !make_plane_map(&ma3, A3, M, K, ldpa, BM) || !map_b(&mb3, B3t))) {
+    if (terms == 6 && (!A3 || !B3t || !map_a(&ma3, A3) || !map_b(&mb3, B3t))) {
         *err = 4;
         return -1;
     }
@@ -941,14 +960,15 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
         plan.slices = 1;
     }
     int r;
-    if (terms == 1)
-        r = b_mn ? launch_t<1, 256, true>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial) : launch_t<1, 256, false>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
-    else if (terms == 4)
-        r = b_mn ? launch_t<4, 128, true>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial) : launch_t<4, 128, false>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
-    else if (terms == 6)
-        r = b_mn ? launch_t<6, 256, true>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial) : launch_t<6, 256, false>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
-    else
-        r = b_mn ? launch_t<3, 256, true>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial) : launch_t<3, 256, false>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial);
+    if (terms == 1) {
+        switch (mn & 3) { case 1: r = launch_t<1, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 2: r = launch_t<1, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 3: r = launch_t<1, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; default: r = launch_t<1, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); }
+    } else if (terms == 4) {
+        switch (mn & 3) { case 1: r = launch_t<4, 128, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 2: r = launch_t<4, 128, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 3: r = launch_t<4, 128, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; default: r = launch_t<4, 128, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); }
+    } else if (terms == 6) {
+        switch (mn & 3) { case 1: r = launch_t<6, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 2: r = launch_t<6, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 3: r = launch_t<6, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; default: r = launch_t<6, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); }
+    } else {
+        switch (mn & 3) { case 1: r = launch_t<3, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 2: r = launch_t<3, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 3: r = launch_t<3, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; default: r = launch_t<3, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); }
+    }
     if (r < 0) { *err = 4; return -1; }
     if (plan.slices > 1) {
         const int bn = terms == 4 ? 128 : 256;

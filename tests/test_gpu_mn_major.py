@@ -1,6 +1,7 @@
-"""MN-major B planes (default: a row-major fp32 B is split without a transpose, the GEMM reads
-K x N planes with MN-major smem descriptors) against the K-major path (SPLIT3_B_MN=0: transposing
-split into N x K planes).  Same planes, same MMA K order -> C must be BIT-identical."""
+"""MN-major operand planes (default: a row-major fp32 B and a transposed fp32 A are split without
+a transpose, and the GEMM reads K x N / K x M planes with MN-major smem descriptors) against the
+K-major path (SPLIT3_MN_MAJOR=0: transposing splits into N x K / M x K planes).  Same plane values,
+same MMA K order -> C must be BIT-identical."""
 import os
 
 import numpy as np
@@ -14,15 +15,15 @@ pytestmark = pytest.mark.gpu
 
 
 def _handle(b_mn: bool):
-    old = os.environ.get("SPLIT3_B_MN")
-    os.environ["SPLIT3_B_MN"] = "1" if b_mn else "0"
+    old = os.environ.get("SPLIT3_MN_MAJOR")
+    os.environ["SPLIT3_MN_MAJOR"] = "1" if b_mn else "0"
     try:
         return s3.Handle(0)
     finally:
         if old is None:
-            os.environ.pop("SPLIT3_B_MN", None)
+            os.environ.pop("SPLIT3_MN_MAJOR", None)
         else:
-            os.environ["SPLIT3_B_MN"] = old
+            os.environ["SPLIT3_MN_MAJOR"] = old
 
 
 @pytest.fixture(scope="module")
@@ -43,6 +44,17 @@ def test_b_mn_equals_k_major(hm, hk, M, N, K, kw):
     B = torch_matrix("loguni", K, N, seed=4)
     Cm = hm.sgemm(A, B, **kw).clone()
     Ck = hk.sgemm(A, B, **kw)
+    assert torch.equal(Cm.view(torch.int32), Ck.view(torch.int32))
+
+
+@pytest.mark.parametrize("transA,transB", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("kw", [{}, {"four_term": True}, {"one_term": True}, {"bf16x3": True}])
+@pytest.mark.parametrize("M,N,K", [(300, 200, 500), (1000, 1030, 129), (2048, 1024, 1024)])
+def test_mn_major_all_transposes(hm, hk, transA, transB, kw, M, N, K):
+    A = torch_matrix("uniform", K if transA else M, M if transA else K, seed=13)
+    B = torch_matrix("glorot", N if transB else K, K if transB else N, seed=14)
+    Cm = hm.sgemm_ex(A, B, transA=bool(transA), transB=bool(transB), **kw).clone()
+    Ck = hk.sgemm_ex(A, B, transA=bool(transA), transB=bool(transB), **kw)
     assert torch.equal(Cm.view(torch.int32), Ck.view(torch.int32))
 
 
