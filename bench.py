@@ -40,6 +40,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--force-dist", action="store_true",
+                   help="test only: run the 2-D tile path (NCCL) even with one rank")
     p.add_argument("--cpu-target-s", type=float, default=12.0)
     p.add_argument("--sustained-s", type=float, default=4.0,
                    help="extra back-to-back loop (s) reported as 'sustained' (0 = skip)")
@@ -279,6 +281,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    use_dist = world > 1 or args.force_dist
 
     import torch
 
@@ -287,7 +290,7 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if use_dist:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
@@ -295,7 +298,7 @@ def main():
     h = s3.Handle(local)
     four, one = args.terms == 4, args.terms == 1
 
-    if world == 1:
+    if not use_dist:
         A = torch_matrix("uniform", n, n, seed=0, device=dev)
         B = torch_matrix("uniform", n, n, seed=1, device=dev)
         C = torch.empty((n, n), dtype=torch.float32, device=dev)
@@ -313,7 +316,7 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    launches_per_step = h.last_launch_count() if world == 1 else tg.launches_per_step()
+    launches_per_step = h.last_launch_count() if not use_dist else tg.launches_per_step()
 
     gpu_idx = local
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
@@ -327,7 +330,7 @@ def main():
     h.timing_read()
     sampler.start()
     time.sleep(0.05)
-    if world > 1:
+    if use_dist:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream(dev)
@@ -337,13 +340,13 @@ def main():
         step()
     e1.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         torch.distributed.barrier()
     clocks = sampler.stop()
     h.timing_enable(False)
     split_ms, gemm_ms, ncalls = h.timing_read()
     t_ms = e0.elapsed_time(e1)
-    if world > 1:
+    if use_dist:
         t = torch.tensor([t_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t_ms = float(t.item())
@@ -373,12 +376,12 @@ def main():
                 "frac_of_burst": (achieved / pk["tc_burst"]) if achieved else None,
                 "gemm_share_of_step": gemm_ms / max(t_ms, 1e-9) if ncalls else None,
                 "gemm_launches_per_step": ncalls / args.steps,
-                "split_ms_per_step": split_ms / args.steps if world == 1 else None,
+                "split_ms_per_step": split_ms / args.steps if not use_dist else None,
                 "split_hbm_gbs": (12.0 * 2 * n * n / (split_ms / args.steps / 1e3) / 1e9)
-                if ncalls and split_ms > 0 and world == 1 else None}
+                if ncalls and split_ms > 0 and not use_dist else None}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not use_dist and not args.no_cpu:
         try:
             cpu = cpu_oracle_sample(A.cpu().numpy(), B.cpu().numpy(), args.terms, args.cpu_target_s, C_gpu=C)
         except Exception as ex:   # reported, never silently replaced
@@ -391,7 +394,7 @@ def main():
         reps = max(args.steps, int(args.sustained_s * 1e3 / max(t_ms / args.steps, 1e-3)))
         s2 = ClockSampler(gpu_idx)
         s2.start()
-        if world > 1:
+        if use_dist:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         y0, y1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -402,7 +405,7 @@ def main():
         torch.cuda.synchronize()
         ck = s2.stop()
         ts = y0.elapsed_time(y1)
-        if world > 1:
+        if use_dist:
             tt = torch.tensor([ts], device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             ts = float(tt.item())
@@ -412,7 +415,7 @@ def main():
 
     # e2e through the C-ABI with HOST buffers (H2D of A, B and D2H of C inside the timed region)
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and not use_dist:
         Ah = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
         Bh = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
         Ch = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
@@ -475,7 +478,7 @@ def main():
             "accuracy": (cpu or {}).get("accuracy"),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         torch.distributed.destroy_process_group()
 
 
