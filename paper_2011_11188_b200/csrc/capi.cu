@@ -13,8 +13,9 @@
 #include "../../include/split3.h"
 #include "internal.h"
 
-// handle-owned device scratch: [0] wave counter, [4] max-abs ticket, [8] wave counter used under
-// CUDA-graph capture, [16] presplit max,
+// handle-owned device scratch (byte offsets): [0] wave counter, [4] max-abs ticket, [8] wave counter
+// used under CUDA-graph capture, [16] presplit max, [48..55] grid barrier (arrival count, sense)
+// of the one-launch front end,
 // [64..] max-abs block partials (2 x kMaxPartials floats)
 constexpr size_t kMaxPartials = 2048;
 constexpr size_t kCounterBytes = 64 + 2 * kMaxPartials * 4;
@@ -29,6 +30,8 @@ struct split3_ctx {
     int last_launches = 0;
     int promo_kb = 0;   // 0 = library default
     int wave_sync = 1;  // GEMM wave lockstep hint (L2 locality)
+    int prep_ok = 1;    // the cooperative one-launch front end is accepted (cleared on rejection)
+    int64_t prep_max = split3::kPrepMaxElems;   // elements of A + B up to which it is used (env SPLIT3_PREP_MAX)
     int mn_major = 1;   // MN-major planes for a row-major B / a transposed A (no transposing split);
                         // env SPLIT3_MN_MAJOR=0: off (K-major planes, transposing split)
     split3::GemmTuneIn tune;
@@ -201,6 +204,7 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
     }
     c->tune.wave_base = c->wave_base;
     if (const char* e = getenv("SPLIT3_MN_MAJOR")) c->mn_major = atoi(e) != 0;
+    if (const char* e = getenv("SPLIT3_PREP_MAX")) c->prep_max = atoll(e);
     *h = c;
     return SPLIT3_OK;
 }
@@ -462,8 +466,28 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
         if (!ev0 || !ev1 || !ev2) return SPLIT3_ERR_CUDA;
         record(h, ev0);
     }
+    // small problems: a1 + a2 of both operands in ONE cooperative launch (all splits are plain
+    // with MN-major planes); a rejected cooperative launch switches the handle to the 3 kernels
+    bool prepped = false;
+    if (fast_max && h->mn_major && h->prep_ok && h->prep_max >= M * K + K * N) {
+        const split3::PrepOperand pa{A->data, A->trans ? K : M, A->trans ? M : K, A->ld, w.A1, w.A2,
+                                     A->trans ? w.ldpa_mn : w.ldpa, w.maxA, w.sA};
+        const split3::PrepOperand pb{B->data, B->trans ? N : K, B->trans ? K : N, B->ld, w.B1t, w.B2t,
+                                     B->trans ? w.ldpb : w.ldpb_mn, w.maxB, w.sB};
+        unsigned* parts_u = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(h->d_counters) + 64);
+        n = split3::launch_prep2(h->stream, pa, pb, parts_u, h->d_counters + 12, h->num_sms);
+        if (n == -2) {
+            h->prep_ok = 0;
+        } else if (n < 0) {
+            return SPLIT3_ERR_CUDA;
+        } else {
+            launches += n;
+            prepped = true;
+        }
+    }
     // a1: per-matrix max-abs (reading R1) of the fp32 operands (max|op(X)| = max|X|)
-    if (fast_max) {
+    if (prepped) {
+    } else if (fast_max) {
         const int64_t ra = A->trans ? K : M, ca = A->trans ? M : K;
         const int64_t rb = B->trans ? N : K, cb = B->trans ? K : N;
         float* parts = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(h->d_counters) + 64);
@@ -478,7 +502,7 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
             return SPLIT3_ERR_CUDA;
         launches += n;
     }
-    if (needB && !(needA && !check)) {
+    if (needB && !(needA && !check) && !prepped) {
         const int64_t r = B->trans ? N : K, c = B->trans ? K : N;
         if ((n = split3::launch_maxabs(h->stream, r, c, B->data, B->ld, w.maxB, check ? w.badB : nullptr, h->num_sms)) < 0)
             return SPLIT3_ERR_CUDA;
@@ -500,7 +524,9 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     const int32_t *sA = A->d_sexp, *sB = B->d_sexp;
     int64_t ldpa = A->ldp, ldpb = B->ldp;
     const bool a_mn = needA && A->trans && h->mn_major;   // MN-major A planes: no transposing split
-    if (a_mn) {
+    if (prepped) {
+        A1 = w.A1; A2 = w.A2; sA = w.sA; ldpa = a_mn ? w.ldpa_mn : w.ldpa;
+    } else if (a_mn) {
         if ((n = split3::launch_split(h->stream, K, M, A->data, A->ld, w.maxA, w.A1, w.A2, w.ldpa_mn, w.sA,
                                       h->num_sms)) < 0)
             return SPLIT3_ERR_CUDA;
@@ -512,7 +538,9 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
         A1 = w.A1; A2 = w.A2; sA = w.sA; ldpa = w.ldpa;
     }
     const bool b_mn = needB && !B->trans && h->mn_major;   // MN-major B planes: no transposing split
-    if (b_mn) {
+    if (prepped) {
+        B1t = w.B1t; B2t = w.B2t; sB = w.sB; ldpb = b_mn ? w.ldpb_mn : w.ldpb;
+    } else if (b_mn) {
         if ((n = split3::launch_split(h->stream, K, N, B->data, B->ld, w.maxB, w.B1t, w.B2t, w.ldpb_mn, w.sB,
                                       h->num_sms)) < 0)
             return SPLIT3_ERR_CUDA;

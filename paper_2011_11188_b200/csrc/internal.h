@@ -44,12 +44,45 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
     cfg.numAttrs = SPLIT3_PDL ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...);
 }
+// cooperative (all blocks co-resident: the kernel has a grid-wide barrier) + programmatic
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k_coop(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                 Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = SPLIT3_PDL ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...);
+}
 
 // Padded plane leading dimension: a multiple of 8 elements (16 bytes, the TMA stride unit).
 inline int64_t plane_ld(int64_t k) { return ((k + 7) / 8) * 8; }
 
 // ---- split_kernels.cu ------------------------------------------------------------------
 // Each launcher returns the number of kernels it launched (>= 0) or -1 on a launch error.
+// One-launch front end for small problems (both operands fp32, plain splits): max-abs of both,
+// a grid-wide barrier (cooperative launch), then both non-transposing splits.  `sync` points to
+// 2 zeroed words (arrival count, sense flag) left reusable; partials holds >= 2 * grid words.
+struct PrepOperand {
+    const float* X;
+    int64_t rows, cols, ld;     // the STORED matrix
+    uint16_t *hi, *lo;
+    int64_t ldp;
+    float* d_max;
+    int32_t* d_sexp;
+};
+constexpr int64_t kPrepMaxElems = 4 << 20;   // both operands together; larger: separate kernels
+int launch_prep2(cudaStream_t s, const PrepOperand& a, const PrepOperand& b, unsigned* partials,
+                 unsigned* sync, int num_sms);
+
 int launch_maxabs(cudaStream_t s, int64_t rows, int64_t cols, const float* X, int64_t ld,
                   float* d_max, long long* d_bad, int num_sms);
 // max-abs of two matrices in one launch (no bad-index tracking): block partials (<= max_parts

@@ -47,6 +47,11 @@ __device__ __forceinline__ void block_fold(unsigned m, long long bad, float* d_m
     }
 }
 
+__device__ __forceinline__ void fold_finite(float x, unsigned& m) {
+    const unsigned u = __float_as_uint(x) & 0x7FFFFFFFu;
+    if (u < kFiniteLimit) m = max(m, u);
+}
+
 __device__ __forceinline__ void fold1(float x, long long idx, unsigned& m, long long& bad) {
     unsigned u = __float_as_uint(x) & 0x7FFFFFFFu;
     if (u < kFiniteLimit) m = max(m, u);
@@ -342,6 +347,114 @@ __global__ void __launch_bounds__(256) split_t_kernel(const float* __restrict__ 
     }
 }
 
+// ---- one-launch front end for small problems (launch_prep2) -------------------------------
+// Work item w of an operand = (row w / nseg, 1024-column segment w % nseg): 256 threads x float4.
+__device__ __forceinline__ void prep_max(const PrepOperand& p, int64_t w0, int64_t wstep, unsigned& m) {
+    const int64_t nseg = (p.cols + 1023) / 1024, items = p.rows * nseg;
+    const bool vec = (p.cols % 4 == 0) && (p.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(p.X) & 15u) == 0);
+    for (int64_t w = w0; w < items; w += wstep) {
+        const int64_t r = w / nseg, c = (w - r * nseg) * 1024 + 4 * threadIdx.x;
+        const float* row = p.X + r * p.ld;
+        if (vec && c + 3 < p.cols) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(row + c));
+            fold_finite(v.x, m); fold_finite(v.y, m); fold_finite(v.z, m); fold_finite(v.w, m);
+        } else {
+            for (int j = 0; j < 4 && c + j < p.cols; j++) fold_finite(row[c + j], m);
+        }
+    }
+}
+__device__ __forceinline__ void prep_split(const PrepOperand& p, float f, int64_t w0, int64_t wstep) {
+    const int64_t nseg = (p.cols + 1023) / 1024, items = p.rows * nseg;
+    const bool vec = (p.cols % 4 == 0) && (p.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(p.X) & 15u) == 0);
+    for (int64_t w = w0; w < items; w += wstep) {
+        const int64_t r = w / nseg, c = (w - r * nseg) * 1024 + 4 * threadIdx.x;
+        const float* row = p.X + r * p.ld;
+        if (vec && c + 3 < p.cols) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(row + c));
+            unsigned short a[4], b[4];
+            split1(v.x, f, a[0], b[0]); split1(v.y, f, a[1], b[1]);
+            split1(v.z, f, a[2], b[2]); split1(v.w, f, a[3], b[3]);
+            *reinterpret_cast<uint2*>(p.hi + r * p.ldp + c) = make_uint2(a[0] | ((unsigned)a[1] << 16), a[2] | ((unsigned)a[3] << 16));
+            *reinterpret_cast<uint2*>(p.lo + r * p.ldp + c) = make_uint2(b[0] | ((unsigned)b[1] << 16), b[2] | ((unsigned)b[3] << 16));
+        } else {
+            for (int j = 0; j < 4 && c + j < p.cols; j++) {
+                unsigned short a, b;
+                split1(row[c + j], f, a, b);
+                p.hi[r * p.ldp + c + j] = a;
+                p.lo[r * p.ldp + c + j] = b;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) prep2_kernel(const PrepOperand pa, const PrepOperand pb,
+                                                    unsigned* partials, unsigned* sync) {
+    pdl_wait();
+    __shared__ unsigned sm0[8], sm1[8];
+    __shared__ bool last;
+    unsigned* count = sync;
+    unsigned* sense = sync + 1;
+    unsigned my_sense = 0;
+    if (threadIdx.x == 0) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(my_sense) : "l"(sense) : "memory");
+    // phase 1 (a1): max-abs of both operands
+    unsigned m0 = 0, m1 = 0;
+    prep_max(pa, blockIdx.x, gridDim.x, m0);
+    prep_max(pb, blockIdx.x, gridDim.x, m1);
+    for (int o = 16; o > 0; o >>= 1) {
+        m0 = max(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+        m1 = max(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { sm0[w] = m0; sm1[w] = m1; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < 8; k++) { m0 = max(m0, sm0[k]); m1 = max(m1, sm1[k]); }
+        partials[2 * blockIdx.x] = m0;
+        partials[2 * blockIdx.x + 1] = m1;
+        __threadfence();
+        last = atomicAdd(count, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {   // fold the partials, publish max and scale of both, release the barrier
+        __threadfence();
+        unsigned t0 = 0, t1 = 0;
+        for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x) {
+            t0 = max(t0, __ldcg(partials + 2 * k));
+            t1 = max(t1, __ldcg(partials + 2 * k + 1));
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            t0 = max(t0, __shfl_xor_sync(0xffffffffu, t0, o));
+            t1 = max(t1, __shfl_xor_sync(0xffffffffu, t1, o));
+        }
+        __syncthreads();
+        if (l == 0) { sm0[w] = t0; sm1[w] = t1; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int k = 0; k < 8; k++) { t0 = max(t0, sm0[k]); t1 = max(t1, sm1[k]); }
+            *reinterpret_cast<unsigned*>(pa.d_max) = t0;
+            *reinterpret_cast<unsigned*>(pb.d_max) = t1;
+            *pa.d_sexp = scale_exp_dev(__uint_as_float(t0));
+            *pb.d_sexp = scale_exp_dev(__uint_as_float(t1));
+            *count = 0u;
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(sense), "r"(my_sense ^ 1u) : "memory");
+        }
+    } else if (threadIdx.x == 0) {   // grid-wide barrier (all blocks co-resident: cooperative launch)
+        unsigned v;
+        do {
+            __nanosleep(32);
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(sense) : "memory");
+        } while (v == my_sense);
+    }
+    __syncthreads();
+    pdl_trigger();
+    // phase 2 (a2): both splits with the exact scales
+    const float fa = pow2_neg(scale_exp_dev(__ldcg(pa.d_max)));
+    const float fb = pow2_neg(scale_exp_dev(__ldcg(pb.d_max)));
+    prep_split(pa, fa, blockIdx.x, gridDim.x);
+    prep_split(pb, fb, blockIdx.x, gridDim.x);
+}
+
 // ---- bf16 x 3 split: x = X1 + X2 + X3, X_i = RN_bf16 of the running
 // residual (exact in fp32); no scale (bfloat16 has the range of fp32).
 __device__ __forceinline__ void split_bf3(float x, unsigned short& h1, unsigned short& h2, unsigned short& h3) {
@@ -425,6 +538,21 @@ inline int grid_rows(int64_t rows, int num_sms, int64_t blocks_x) {
 }
 
 }  // namespace
+
+int launch_prep2(cudaStream_t st, const PrepOperand& a, const PrepOperand& b, unsigned* partials,
+                 unsigned* sync, int num_sms) {
+    auto items = [](const PrepOperand& p) { return p.rows * ((p.cols + 1023) / 1024); };
+    int64_t g = items(a) > items(b) ? items(a) : items(b);
+    const int64_t cap = (int64_t)num_sms * 2;   // far below the co-residency limit (8 blocks / SM)
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    const cudaError_t e = launch_k_coop(prep2_kernel, dim3((unsigned)g), dim3(256), 0, st, a, b, partials, sync);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();   // launch-configuration error (not sticky): caller falls back
+        return -2;
+    }
+    return 1;
+}
 
 int launch_maxabs(cudaStream_t st, int64_t rows, int64_t cols, const float* X, int64_t ld,
                   float* d_max, long long* d_bad, int num_sms) {
