@@ -468,8 +468,12 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     }
     // small problems: a1 + a2 of both operands in ONE cooperative launch (all splits are plain
     // with MN-major planes); a rejected cooperative launch switches the handle to the 3 kernels
+    // (eager calls only: under CUDA-graph capture the separate kernels' programmatic edges
+    // replay faster than one cooperative node: 0.361 vs 0.403 ms per small-MLP step)
     bool prepped = false;
-    if (fast_max && h->mn_major && h->prep_ok && h->prep_max >= M * K + K * N) {
+    cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+    if (fast_max && h->mn_major && h->prep_ok && h->prep_max >= M * K + K * N &&
+        cudaStreamIsCapturing(h->stream, &cap_st) == cudaSuccess && cap_st == cudaStreamCaptureStatusNone) {
         const split3::PrepOperand pa{A->data, A->trans ? K : M, A->trans ? M : K, A->ld, w.A1, w.A2,
                                      A->trans ? w.ldpa_mn : w.ldpa, w.maxA, w.sA};
         const split3::PrepOperand pb{B->data, B->trans ? N : K, B->trans ? K : N, B->ld, w.B1t, w.B2t,

@@ -61,8 +61,9 @@ def test_prep_strided_and_misaligned(hp, hs):
 
 
 def test_prep_graph_replays_track_new_inputs(hp, hs):
-    """The barrier is sense-reversing (no host state): captured once, replayed with inputs whose
-    scales change, each replay equals a fresh two-pass call."""
+    """Under capture the library takes the separate front-end kernels (faster replays); the graph,
+    replayed with inputs whose scales change, matches fresh eager calls (which take the one-launch
+    front end) bitwise."""
     M, N, K = 512, 384, 640
     A = torch_matrix("uniform", M, K, seed=25)
     B = torch_matrix("uniform", K, N, seed=26)
