@@ -62,7 +62,13 @@ typedef enum split3_status {
 /* ---- handle ------------------------------------------------------------------------ */
 
 /* Create a handle bound to CUDA device `device` and stream `cuda_stream` (a cudaStream_t;
- * NULL = the legacy default stream).  Fails with SPLIT3_ERR_ARCH unless the device is sm_100. */
+ * NULL = the legacy default stream).  Fails with SPLIT3_ERR_ARCH unless the device is sm_100.
+ * Environment variables read here select internal paths for A/B measurements; none changes a
+ * bit of any result (tests compare the paths bitwise):
+ *   SPLIT3_MN_MAJOR=0     K-major planes for every operand (transposing splits) instead of
+ *                         MN-major planes for a row-major B / a transposed A;
+ *   SPLIT3_PREP_MAX=<n>   use the one-launch max-abs + split front end for eager calls whose
+ *                         fp32 operands hold <= n elements together (default 4 Mi; 0 = never). */
 int split3_sgemm_create(split3_handle_t *h, int device, void *cuda_stream);
 
 /* Rebind the handle to another stream of the same device. */
