@@ -124,7 +124,6 @@ size_t ws_bytes_for(int64_t M, int64_t N, int64_t K, bool planesA, bool planesB,
     return b;
 }
 
-size_t ws_size(int64_t M, int64_t N, int64_t K) { return ws_bytes_for(M, N, K, true, true, 3); }
 
 // bf16 x 3: three planes per operand (scalars block as usual; sA = sB stay 0: no scale)
 struct CarveBF3 {
