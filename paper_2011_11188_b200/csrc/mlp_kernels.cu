@@ -63,13 +63,28 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(int64_t M, int64_t N,
     if (lane == 0 && row_loss) row_loss[row] = (y >= 0) ? -((double)(l[y] - mx) - log(s)) : 0.0;
 }
 
-// db[c] = sum_r dZ[r, c] in row order (deterministic): one thread per column, coalesced rows.
+// db[c] = sum_r dZ[r, c] in a fixed order (deterministic): a block owns 32 columns; warp g sums the
+// rows r = g, g + 8, g + 16, ... in increasing order (lane = column: 128-B coalesced loads), then
+// the 8 group sums are added in group order.
 __global__ void __launch_bounds__(256) col_sum_kernel(int64_t M, int64_t N, const float* __restrict__ dZ,
                                                       float* __restrict__ db) {
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < N; c += (int64_t)gridDim.x * blockDim.x) {
+    __shared__ float part[8][33];
+    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+    for (int64_t c0 = (int64_t)blockIdx.x * 32; c0 < N; c0 += (int64_t)gridDim.x * 32) {
+        const int64_t c = c0 + lane;
         float acc = 0.0f;
-        for (int64_t r = 0; r < M; r++) acc = __fadd_rn(acc, dZ[r * N + c]);
-        db[c] = acc;
+        if (c < N) {
+#pragma unroll 8
+            for (int64_t r = g; r < M; r += 8) acc = __fadd_rn(acc, dZ[r * N + c]);
+        }
+        part[g][lane] = acc;
+        __syncthreads();
+        if (g == 0 && c < N) {
+            float t = part[0][lane];
+            for (int k = 1; k < 8; k++) t = __fadd_rn(t, part[k][lane]);
+            db[c] = t;
+        }
+        __syncthreads();
     }
 }
 
@@ -128,7 +143,8 @@ int launch_softmax_xent(cudaStream_t st, int64_t M, int64_t N, const float* L, c
     return 1;
 }
 int launch_col_sum(cudaStream_t st, int64_t M, int64_t N, const float* dZ, float* db, int num_sms) {
-    col_sum_kernel<<<grid_for(N, num_sms), 256, 0, st>>>(M, N, dZ, db);
+    const int64_t tiles = (N + 31) / 32, cap = (int64_t)num_sms * 8;
+    col_sum_kernel<<<(unsigned)(tiles < cap ? tiles : cap), 256, 0, st>>>(M, N, dZ, db);
     return ok();
 }
 int launch_sgd(cudaStream_t st, int64_t n, float* w, const float* g, float lr, int num_sms) {
