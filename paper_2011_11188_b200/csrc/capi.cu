@@ -13,8 +13,8 @@
 #include "../../include/split3.h"
 #include "internal.h"
 
-// handle-owned device scratch (byte offsets): [0] wave counter, [4] max-abs ticket, [8] wave counter
-// used under CUDA-graph capture, [16] presplit max, [48..55] grid barrier (arrival count, sense)
+// handle-owned device scratch (byte offsets): [0] GEMM wave-lockstep counter, [4] max-abs ticket,
+// [12] GEMM exit ticket (the last CTA zeroes [0] and [12]), [16] presplit max, [48..55] grid barrier (arrival count, sense)
 // of the one-launch front end,
 // [64..] max-abs block partials (2 x kMaxPartials floats)
 constexpr size_t kMaxPartials = 2048;
@@ -35,7 +35,6 @@ struct split3_ctx {
     int mn_major = 1;   // MN-major planes for a row-major B / a transposed A (no transposing split);
                         // env SPLIT3_MN_MAJOR=0: off (K-major planes, transposing split)
     split3::GemmTuneIn tune;
-    unsigned wave_base[2] = {0, 0};   // running value of the device wave counter (d_counters[0]), launches
     unsigned* d_counters = nullptr;   // 256 B of device scratch owned by the handle
     // host-buffer entry: copy-in / copy-out streams and events, created on first use
     cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -201,7 +200,6 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
         delete c;
         return SPLIT3_ERR_CUDA;
     }
-    c->tune.wave_base = c->wave_base;
     if (const char* e = getenv("SPLIT3_MN_MAJOR")) c->mn_major = atoi(e) != 0;
     if (const char* e = getenv("SPLIT3_PREP_MAX")) c->prep_max = atoll(e);
     *h = c;

@@ -86,7 +86,7 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // i-th tile, then waits — at most kWaveWaitNs — until all CTAs that have an i-th tile did.  A
 // performance hint only: the bounded wait can never deadlock (e.g. if not all CTAs are resident).
 constexpr uint64_t kWaveWaitNs = 200000;
-// The counter is never reset: launches continue from the base the host tracks (wrap-safe).
+// The counter starts every launch at 0: the last CTA to exit zeroes it (see the kernel's end).
 __device__ __forceinline__ void wave_sync(unsigned* counter, unsigned target) {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
     const uint64_t t0 = globaltimer_ns();
@@ -286,7 +286,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
              const __grid_constant__ CUtensorMap mapC, int tma_store,
              int M, int N, int K, int promo_kb, const int32_t* __restrict__ d_sA,
              const int32_t* __restrict__ d_sB, float* __restrict__ C, int64_t ldc,
-             unsigned* __restrict__ wave_counter, unsigned wave_base, const GemmTune tune,
+             unsigned* __restrict__ wave_counter, const GemmTune tune,
              const SplitPlan plan, float* __restrict__ partial) {
     constexpr bool BF3 = TERMS == 6;                 // bf16 x 3 split (NEXT #4): 3 planes, 6 products
     constexpr int PL = BF3 ? 3 : 2;
@@ -374,7 +374,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         // ===================== TMA producer (both CTAs; warp-uniform, one elected lane) =====
         int stage = 0;
         uint32_t phase = 0;
-        unsigned wave_target = wave_base;   // cumulative arrivals expected up to this unit index
+        unsigned wave_target = 0;   // cumulative arrivals expected up to this unit index (counter starts at 0)
         int64_t idx = 0;
         for (int64_t unit = pair; unit < num_units; unit += num_pairs, idx++) {
             int64_t tile;
@@ -710,6 +710,15 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
 #endif
     tc_fence_before();
     cluster_sync();
+    // Wave-lockstep counter reset: the last CTA to get here (exit ticket, word 3) zeroes the
+    // counter, so every launch — eager or a CUDA-graph replay — starts from 0 with no memset.
+    if (wave_counter && threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(wave_counter + 3, 1u) == gridDim.x - 1) {
+            atomicExch(wave_counter, 0u);
+            atomicExch(wave_counter + 3, 0u);
+        }
+    }
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -818,7 +827,7 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
              const CUtensorMap& a2, const CUtensorMap& b1, const CUtensorMap& b2, const CUtensorMap& a3,
              const CUtensorMap& b3, const CUtensorMap& mc, int tma_store,
              const int32_t* d_sA, const int32_t* d_sB, float* C, int64_t ldc, int num_sms,
-             int promo_kb, unsigned* wave_counter, unsigned* wave_base, const GemmTune& tune, const SplitPlan& plan,
+             int promo_kb, unsigned* wave_counter, const GemmTune& tune, const SplitPlan& plan,
              float* partial) {
     constexpr int SMEM_BYTES = Geo<BN_, TERMS == 6 ? 3 : 2>::SMEM;
     // the dynamic-smem opt-in is per device: remember it per device ordinal
@@ -835,31 +844,10 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
     const int64_t tiles = plan.whole + plan.nsplit * plan.slices;   // work units
     const int64_t pairs = num_sms / 2;
     const int grid = 2 * (int)(tiles < pairs ? tiles : pairs);
-    // Under CUDA-graph capture the host cannot track the counter across replays: use the graph
-    // slot (wave_counter + 2), reset by a memset node captured before the kernel, base 0.
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) return -1;
-    const bool capturing = cap != cudaStreamCaptureStatusNone;
-    if (capturing && wave_counter) {
-        wave_counter += 2;
-        if (cudaMemsetAsync(wave_counter, 0, sizeof(unsigned), st) != cudaSuccess) return -1;
-    }
-    // Periodic resync of the eager counter (every 64 launches): bounds the cost of any drift
-    // between the device counter and the host-tracked base (e.g. after an aborted launch).
-    if (wave_counter && wave_base && !capturing && (wave_base[1]++ & 63u) == 0) {
-        if (cudaMemsetAsync(wave_counter, 0, sizeof(unsigned), st) != cudaSuccess) return -1;
-        wave_base[0] = 0;
-    }
-    const unsigned base = (wave_base && !capturing) ? *wave_base : 0u;
     if (launch_k(gemm3_kernel<TERMS, BN_, LAY>, dim3((unsigned)grid), dim3(NUM_THREADS), SMEM_BYTES, st, a1, a2, b1, b2, a3,
-                 b3, mc, tma_store, (int)M, (int)N, (int)K, promo_kb, d_sA, d_sB, C, ldc, wave_counter, base, tune,
+                 b3, mc, tma_store, (int)M, (int)N, (int)K, promo_kb, d_sA, d_sB, C, ldc, wave_counter, tune,
                  plan, partial) != cudaSuccess)
         return -1;
-    if (wave_base && wave_counter && !capturing) {   // arrivals: one per CTA per unit index >= 1
-        const int64_t pairs_launched = grid / 2;
-        const int64_t extra = tiles > pairs_launched ? tiles - pairs_launched : 0;
-        *wave_base = base + 2u * (unsigned)extra;
-    }
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -904,7 +892,6 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
                  int terms, int num_sms, int promo_kb, unsigned* wave_counter, const GemmTuneIn& tin,
                  float* partial, int64_t partial_elems, int* err, const uint16_t* A3, const uint16_t* B3t,
                  int mn) {
-    unsigned* wave_base = wave_counter ? tin.wave_base : nullptr;
     const bool b_mn = (mn & 1) != 0, a_mn = (mn & 2) != 0;
     CUtensorMap ma1, ma2, mb1, mb2, ma3, mb3;
     const uint16_t* A2e = terms == 1 ? A1 : A2;
@@ -946,13 +933,13 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     }
     int r;
     if (terms == 1) {
-        switch (mn & 3) { case 1: r = launch_t<1, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 2: r = launch_t<1, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 3: r = launch_t<1, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; default: r = launch_t<1, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); }
+        switch (mn & 3) { case 1: r = launch_t<1, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 2: r = launch_t<1, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 3: r = launch_t<1, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; default: r = launch_t<1, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); }
     } else if (terms == 4) {
-        switch (mn & 3) { case 1: r = launch_t<4, 128, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 2: r = launch_t<4, 128, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 3: r = launch_t<4, 128, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; default: r = launch_t<4, 128, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); }
+        switch (mn & 3) { case 1: r = launch_t<4, 128, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 2: r = launch_t<4, 128, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 3: r = launch_t<4, 128, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; default: r = launch_t<4, 128, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); }
     } else if (terms == 6) {
-        switch (mn & 3) { case 1: r = launch_t<6, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 2: r = launch_t<6, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 3: r = launch_t<6, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; default: r = launch_t<6, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); }
+        switch (mn & 3) { case 1: r = launch_t<6, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 2: r = launch_t<6, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 3: r = launch_t<6, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; default: r = launch_t<6, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); }
     } else {
-        switch (mn & 3) { case 1: r = launch_t<3, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 2: r = launch_t<3, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; case 3: r = launch_t<3, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); break; default: r = launch_t<3, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, wave_base, tune, plan, partial); }
+        switch (mn & 3) { case 1: r = launch_t<3, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 2: r = launch_t<3, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 3: r = launch_t<3, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; default: r = launch_t<3, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); }
     }
     if (r < 0) { *err = 4; return -1; }
     if (plan.slices > 1) {

@@ -112,7 +112,6 @@ constexpr int kDefaultGroupM = 8;     // raster group, in pair m-blocks
 struct GemmTuneIn {
     int group_m = 0;                  // 0 = default
     int pol_a = 0, pol_b = 0;         // L2 policy for A / B plane loads: 0 normal, 1 evict_first, 2 evict_last
-    unsigned* wave_base = nullptr;    // host-side [0] running base of the wave counter, [1] launch count
 };
 struct GemmTune {
     int group_m;
