@@ -208,8 +208,11 @@ int split3_relu_backward(split3_handle_t h, int64_t M, int64_t N, const float *d
 int split3_softmax_xent(split3_handle_t h, int64_t M, int64_t N, const float *L, const int32_t *labels,
                         float *P, float *dL, double *row_scratch, double *d_loss_sum);
 
-/* db[c] = sum_r dZ[r, c], dZ packed M x N, in a fixed order (deterministic): 8 interleaved row
- * groups (r mod 8) each summed in row order, then the group sums in group order. */
+/* db[c] = sum_r dZ[r, c], dZ packed M x N, in a fixed order (deterministic): with an attached
+ * workspace of >= chunks * N floats (chunks = min(ceil(M / 256), 64) >= 2) the rows are cut into
+ * `chunks` contiguous chunks, each summed as 8 interleaved row groups (row order inside a group,
+ * groups in order) and the chunk sums added in chunk order; otherwise 32 interleaved row groups,
+ * then the group sums in order.  Uses the handle's workspace as scratch (dead between calls). */
 int split3_bias_grad(split3_handle_t h, int64_t M, int64_t N, const float *dZ, float *db);
 
 /* w -= lr * g over n elements. */

@@ -641,7 +641,10 @@ int split3_bias_grad(split3_handle_t h, int64_t M, int64_t N, const float* dZ, f
     if (N == 0) return SPLIT3_OK;
     if (!dZ || !db) return SPLIT3_ERR_INVALID_VALUE;
     if (set_dev(h)) return SPLIT3_ERR_CUDA;
-    return split3::launch_col_sum(h->stream, M, N, dZ, db, h->num_sms) < 0 ? SPLIT3_ERR_CUDA : SPLIT3_OK;
+    // the attached workspace is scratch between calls on this stream: the two-stage form uses it
+    return split3::launch_col_sum(h->stream, M, N, dZ, db, h->num_sms, static_cast<float*>(h->ws), h->ws_bytes) < 0
+               ? SPLIT3_ERR_CUDA
+               : SPLIT3_OK;
 }
 
 int split3_sgd_update(split3_handle_t h, int64_t n, float* w, const float* g, float lr) {

@@ -147,7 +147,9 @@ int launch_bias_act(cudaStream_t s, int64_t M, int64_t N, const float* Z, int64_
 int launch_relu_bwd(cudaStream_t s, int64_t M, int64_t N, const float* dH, const float* H, float* dZ, int num_sms);
 int launch_softmax_xent(cudaStream_t s, int64_t M, int64_t N, const float* L, const int32_t* labels, float* P,
                         float* dL, double* row_loss, double* loss_sum);
-int launch_col_sum(cudaStream_t s, int64_t M, int64_t N, const float* dZ, float* db, int num_sms);
+// scratch (may be NULL): chunks * N floats for the two-stage fixed-order form
+int launch_col_sum(cudaStream_t s, int64_t M, int64_t N, const float* dZ, float* db, int num_sms,
+                   float* scratch = nullptr, size_t scratch_bytes = 0);
 int launch_sgd(cudaStream_t s, int64_t n, float* w, const float* g, float lr, int num_sms);
 
 }  // namespace split3

@@ -7,7 +7,7 @@ from torch.profiler import profile, ProfilerActivity
 import paper_2011_11188_b200 as s3
 from paper_2011_11188_b200.mlp import DenseNet
 h = s3.Handle(0)
-sizes, B = [1024, 1024, 1024, 10], 512
+sizes, B = ([4096, 4096, 4096, 4096, 1024], 4096) if os.environ.get("BIG") else ([1024, 1024, 1024, 10], 512)
 X = torch.randn((B, sizes[0]), device="cuda")
 y = torch.randint(0, sizes[-1], (B,), device="cuda", dtype=torch.int32)
 net = DenseNet(sizes, seed=0, mode="three", h=h)
