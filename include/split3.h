@@ -121,9 +121,16 @@ const char *split3_status_string(int status);
 
 /* One GEMM operand.  op(X) = X (trans = 0) or X^T (trans = 1), with X row-major fp32 in device
  * memory (`data`, leading dimension `ld` of the STORED matrix) — or, when `hi` is non-NULL, the
- * operand is given pre-split (planes written by split3_presplit for the same role): `hi`, `lo`
- * FP16 planes (K-major, ldp elements per row, 16-byte aligned) and its device scale exponent.
- * Pre-split planes are immutable inputs and may be reused across calls. */
+ * operand is given pre-split: `hi`, `lo` FP16 planes (ldp elements per row, 16-byte aligned) and
+ * its device scale exponent, either
+ *   stored = 0: planes written by split3_presplit for this role (K-major: M x K for A, N x K for
+ *               B; `trans` is ignored), or
+ *   stored = 1: the plain split of the STORED matrix (split3_presplit_stored: planes have the
+ *               stored matrix's shape) and `trans` relates op(X) to it exactly as for fp32 data.
+ *               The same planes then serve any role and either op(): a dense layer splits W,
+ *               H and dZ once each and uses them in X*W, H^T*dZ and dZ*W^T.
+ * Pre-split planes are immutable inputs and may be reused across calls.
+ * Zero-initialise unused fields (stored = 0 keeps the original meaning). */
 typedef struct split3_matrix {
     const float *data;
     int64_t ld;
@@ -132,6 +139,7 @@ typedef struct split3_matrix {
     const uint16_t *lo;
     int64_t ldp;
     const int32_t *d_sexp;
+    int stored;
 } split3_matrix;
 
 /* C = op(A) * op(B), op(A) M x K, op(B) K x N (PAPER.md:2-24 with the transposes a dense layer's
@@ -149,6 +157,13 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
  * Uses a few bytes of handle-owned scratch; asynchronous on the handle's stream. */
 int split3_presplit(split3_handle_t h, int role, int64_t rows, int64_t cols, const float *X, int64_t ldx,
                     int trans, uint16_t *hi, uint16_t *lo, int64_t ldp, int32_t *d_sexp);
+
+/* Split the STORED matrix X (rows x cols, row-major, leading dimension ldx) once, without a
+ * transpose: max-abs + Eq. A_1 with the scale rule R1 into planes hi/lo of the same shape
+ * (ldp >= cols, multiple of 8, 16-byte aligned); d_sexp receives the exponent.  The result is a
+ * split3_matrix with stored = 1 usable as A or B, transposed or not.  Asynchronous. */
+int split3_presplit_stored(split3_handle_t h, int64_t rows, int64_t cols, const float *X, int64_t ldx,
+                           uint16_t *hi, uint16_t *lo, int64_t ldp, int32_t *d_sexp);
 
 /* ---- lower level: used by the multi-GPU driver and by the tests -------------------------- */
 

@@ -14,8 +14,9 @@
 #include "internal.h"
 
 // handle-owned device scratch (byte offsets): [0] GEMM wave-lockstep counter, [4] max-abs ticket,
-// [12] GEMM exit ticket (the last CTA zeroes [0] and [12]), [16] presplit max, [48..55] grid barrier (arrival count, sense)
-// of the one-launch front end,
+// [12] GEMM exit ticket (the last CTA zeroes [0] and [12]), [16] presplit max, [20] dummy max of
+// the one-matrix ticketed max-abs, [48..55] grid barrier (arrival count, sense) of the one-launch
+// front end,
 // [64..] max-abs block partials (2 x kMaxPartials floats)
 constexpr size_t kMaxPartials = 2048;
 constexpr size_t kCounterBytes = 64 + 2 * kMaxPartials * 4;
@@ -344,9 +345,12 @@ static int split_operand(split3_ctx* h, int role, int64_t opr, int64_t opc, cons
 
 static bool operand_ok(const split3_matrix* X, int64_t opr, int64_t opc, int role, int terms) {
     if (!X || (X->trans != 0 && X->trans != 1)) return false;
-    if (X->hi) {   // pre-split planes: K-major, rows = M (A) or N (B), K columns
-        const int64_t prow_k = role == 0 ? opc : opr;
-        if (!X->d_sexp || X->ldp < prow_k || X->ldp % 8 || !aligned(X->hi, 16)) return false;
+    if (X->hi) {   // pre-split planes
+        // stored: the plain split of the stored matrix (row length: op cols, or op rows if trans);
+        // else split3_presplit's K-major planes (rows = M (A) or N (B), K columns)
+        const int64_t need = X->stored ? (X->trans ? opr : opc) : (role == 0 ? opc : opr);
+        if (X->stored != 0 && X->stored != 1) return false;
+        if (!X->d_sexp || X->ldp < need || X->ldp % 8 || !aligned(X->hi, 16)) return false;
         if (terms != 1 && (!X->lo || !aligned(X->lo, 16))) return false;
         return true;
     }
@@ -449,7 +453,9 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     // scalars: maxA = maxB = 0.0f, sA = sB = 0, badA = badB = INT64_MAX.  The common path (both
     // operands fp32, no check) needs no reset: the two-matrix max-abs writes maxA/maxB itself.
     const bool fast_max = needA && needB && !check;
-    if (!fast_max && cudaMemsetAsync(h->ws, 0, 32, h->stream) != cudaSuccess) return SPLIT3_ERR_CUDA;
+    // (both operands pre-split: no max-abs at all, nothing to reset)
+    if (!fast_max && (needA || needB) && cudaMemsetAsync(h->ws, 0, 32, h->stream) != cudaSuccess)
+        return SPLIT3_ERR_CUDA;
     int launches = 0, n;
     if (check) {
         if (cudaMemsetAsync(w.badA, 0xFF, 16, h->stream) != cudaSuccess ||
@@ -524,10 +530,12 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     const uint16_t *A1 = A->hi, *A2 = A->lo, *B1t = B->hi, *B2t = B->lo;
     const int32_t *sA = A->d_sexp, *sB = B->d_sexp;
     int64_t ldpa = A->ldp, ldpb = B->ldp;
-    const bool a_mn = needA && A->trans && h->mn_major;   // MN-major A planes: no transposing split
+    // pre-split planes of the stored matrix: A stored K x M (trans) is MN-major, B stored K x N
+    // (not trans) is MN-major; the other two cases are K-major
+    const bool a_mn = (needA && A->trans && h->mn_major) || (!needA && A->stored && A->trans);
     if (prepped) {
         A1 = w.A1; A2 = w.A2; sA = w.sA; ldpa = a_mn ? w.ldpa_mn : w.ldpa;
-    } else if (a_mn) {
+    } else if (needA && a_mn) {
         if ((n = split3::launch_split(h->stream, K, M, A->data, A->ld, w.maxA, w.A1, w.A2, w.ldpa_mn, w.sA,
                                       h->num_sms)) < 0)
             return SPLIT3_ERR_CUDA;
@@ -538,10 +546,10 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
         if (st) return st;
         A1 = w.A1; A2 = w.A2; sA = w.sA; ldpa = w.ldpa;
     }
-    const bool b_mn = needB && !B->trans && h->mn_major;   // MN-major B planes: no transposing split
+    const bool b_mn = (needB && !B->trans && h->mn_major) || (!needB && B->stored && !B->trans);
     if (prepped) {
         B1t = w.B1t; B2t = w.B2t; sB = w.sB; ldpb = b_mn ? w.ldpb_mn : w.ldpb;
-    } else if (b_mn) {
+    } else if (needB && b_mn) {
         if ((n = split3::launch_split(h->stream, K, N, B->data, B->ld, w.maxB, w.B1t, w.B2t, w.ldpb_mn, w.sB,
                                       h->num_sms)) < 0)
             return SPLIT3_ERR_CUDA;
@@ -575,8 +583,8 @@ int split3_sgemm(split3_handle_t h, int64_t M, int64_t N, int64_t K, const float
                  const float* B, int64_t ldb, float* C, int64_t ldc, uint32_t flags) {
     if (!h) return SPLIT3_ERR_INVALID_VALUE;
     if (K > 0 && M > 0 && N > 0 && (!A || !B)) return SPLIT3_ERR_INVALID_VALUE;
-    split3_matrix a = {A, lda, 0, nullptr, nullptr, 0, nullptr};
-    split3_matrix b = {B, ldb, 0, nullptr, nullptr, 0, nullptr};
+    split3_matrix a = {A, lda, 0, nullptr, nullptr, 0, nullptr, 0};
+    split3_matrix b = {B, ldb, 0, nullptr, nullptr, 0, nullptr, 0};
     return split3_sgemm_ex(h, M, N, K, &a, &b, C, ldc, flags);
 }
 
@@ -599,10 +607,39 @@ int split3_presplit(split3_handle_t h, int role, int64_t rows, int64_t cols, con
     int n = split3::launch_maxabs(h->stream, sr, sc, X, ldx, d_max, nullptr, h->num_sms);
     if (n < 0) return SPLIT3_ERR_CUDA;
     launches += n;
-    split3_matrix m = {X, ldx, trans, nullptr, nullptr, 0, nullptr};
+    split3_matrix m = {X, ldx, trans, nullptr, nullptr, 0, nullptr, 0};
     int st = split_operand(h, role, rows, cols, &m, d_max, hi, lo, ldp, d_sexp, &launches);
     if (st) return st;
     h->last_launches = launches;
+    return SPLIT3_OK;
+}
+
+int split3_presplit_stored(split3_handle_t h, int64_t rows, int64_t cols, const float* X, int64_t ldx, uint16_t* hi,
+                           uint16_t* lo, int64_t ldp, int32_t* d_sexp) {
+    if (!h || rows < 0 || cols < 0) return SPLIT3_ERR_INVALID_VALUE;
+    if (rows == 0 || cols == 0) return SPLIT3_OK;
+    if (!X || !hi || !lo || !d_sexp || ldx < cols || ldp < cols || ldp % 8 || !aligned(hi, 16) || !aligned(lo, 16))
+        return SPLIT3_ERR_INVALID_VALUE;
+    if (set_dev(h)) return SPLIT3_ERR_CUDA;
+    float* d_max = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(h->d_counters) + 16);
+    int launches = 0, n;
+    if (ldx == cols && aligned(X, 16) && cols >= 4) {
+        // ticketed max-abs (writes *d_max itself: no memset node, so the programmatic edge to the
+        // split survives under graph capture); the second operand is a 4-element dummy
+        float* dummy = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(h->d_counters) + 20);
+        float* parts = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(h->d_counters) + 64);
+        if ((n = split3::launch_maxabs2(h->stream, rows, cols, X, ldx, d_max, 1, 4, X, 4, dummy, h->num_sms, parts,
+                                        (int)kMaxPartials, h->d_counters + 1)) < 0)
+            return SPLIT3_ERR_CUDA;
+    } else {
+        if (cudaMemsetAsync(d_max, 0, 4, h->stream) != cudaSuccess) return SPLIT3_ERR_CUDA;
+        if ((n = split3::launch_maxabs(h->stream, rows, cols, X, ldx, d_max, nullptr, h->num_sms)) < 0)
+            return SPLIT3_ERR_CUDA;
+    }
+    launches += n;
+    if ((n = split3::launch_split(h->stream, rows, cols, X, ldx, d_max, hi, lo, ldp, d_sexp, h->num_sms)) < 0)
+        return SPLIT3_ERR_CUDA;
+    h->last_launches = launches + n;
     return SPLIT3_OK;
 }
 

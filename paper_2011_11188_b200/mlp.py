@@ -47,14 +47,26 @@ class DenseNet:
     def _mm(self, A, B, transA=False, transB=False):
         return self.h.sgemm_ex(A, B, transA=transA, transB=transB, **MODES[self.mode])
 
-    def forward(self, X):
-        """Per-layer activations [X, H1, ..., logits] (logits before softmax)."""
-        acts = [X]
+    def _split(self, X):
+        """The plain split of a stored matrix (split3_presplit_stored), reused by every GEMM that
+        reads X in the step: W in X*W and dZ*W^T, H in H*W and H^T*dZ, dZ in H^T*dZ and dZ*W^T.
+        Same planes and scale as splitting inside each call -> bitwise the same products."""
+        return self.h.presplit_stored(X)
+
+    def _forward(self, X):
+        """(activations [X, H1, ..., logits], planes of [X, H1, ...], planes of the weights)."""
+        acts, act_planes, w_planes = [X], [], []
         L = len(self.W)
         for i, (w, b) in enumerate(zip(self.W, self.b)):
-            Z = self._mm(acts[-1], w)
+            act_planes.append(self._split(acts[-1]))
+            w_planes.append(self._split(w))
+            Z = self._mm(act_planes[-1], w_planes[-1])
             acts.append(self.h.bias_act(Z, b, relu=i < L - 1, out=Z))
-        return acts
+        return acts, act_planes, w_planes
+
+    def forward(self, X):
+        """Per-layer activations [X, H1, ..., logits] (logits before softmax)."""
+        return self._forward(X)[0]
 
     def predict_proba(self, X):
         P, _, _ = self.h.softmax_xent(self.forward(X)[-1], None, want_probs=True, want_grad=False)
@@ -71,14 +83,15 @@ class DenseNet:
 
     def backward_device(self, X, y):
         """As backward(), with the loss left on the device (no host synchronisation)."""
-        acts = self.forward(X)
+        acts, act_planes, w_planes = self._forward(X)
         _, dZ, loss = self.h.softmax_xent(acts[-1], y, want_probs=False, want_grad=True)
         dWs, dbs = [None] * len(self.W), [None] * len(self.W)
         for i in range(len(self.W) - 1, -1, -1):
-            dWs[i] = self._mm(acts[i], dZ, transA=True)          # H^T dZ
+            dZp = self._split(dZ)
+            dWs[i] = self._mm(act_planes[i], dZp, transA=True)     # H^T dZ
             dbs[i] = self.h.bias_grad(dZ)
             if i > 0:
-                dH = self._mm(dZ, self.W[i], transB=True)         # dZ W^T
+                dH = self._mm(dZp, w_planes[i], transB=True)       # dZ W^T
                 dZ = self.h.relu_backward(dH, acts[i], out=dH)
         return loss, dWs, dbs
 

@@ -41,7 +41,7 @@ EXPORTS = (
     "split3_status_string", "split3_maxabs", "split3_split", "split3_gemm_planes",
     "split3_last_launch_count", "split3_timing_enable", "split3_timing_read",
     "split3_set_promotion", "split3_set_wave_sync", "split3_set_schedule",
-    "split3_sgemm_ex", "split3_presplit", "split3_split_bf16x3", "split3_bias_act", "split3_relu_backward",
+    "split3_sgemm_ex", "split3_presplit", "split3_presplit_stored", "split3_split_bf16x3", "split3_bias_act", "split3_relu_backward",
     "split3_softmax_xent", "split3_bias_grad", "split3_sgd_update",
 )
 
@@ -49,17 +49,19 @@ class split3_matrix(ctypes.Structure):
     """ctypes mirror of include/split3.h's split3_matrix."""
     _fields_ = [("data", ctypes.c_void_p), ("ld", ctypes.c_int64), ("trans", ctypes.c_int),
                 ("hi", ctypes.c_void_p), ("lo", ctypes.c_void_p), ("ldp", ctypes.c_int64),
-                ("d_sexp", ctypes.c_void_p)]
+                ("d_sexp", ctypes.c_void_p), ("stored", ctypes.c_int)]
 
 
 class Planes:
-    """A pre-split operand (split3_presplit): FP16 planes (int16 tensors holding binary16 bits,
-    K-major with padded leading dimension) and the device scale exponent.  role 0 = A operand
-    (planes M x K), role 1 = B operand (planes N x K = op(B)^T)."""
+    """A pre-split operand: FP16 planes (int16 tensors holding binary16 bits, padded leading
+    dimension) and the device scale exponent.  From presplit(): role 0 = A operand (planes M x K),
+    role 1 = B operand (planes N x K = op(B)^T), K-major.  From presplit_stored() (role None,
+    stored=True): the plain split of the stored matrix, usable as A or B with either transpose."""
 
-    def __init__(self, hi, lo, sexp, role, rows, cols):
+    def __init__(self, hi, lo, sexp, role, rows, cols, stored=False):
         self.hi, self.lo, self.sexp = hi, lo, sexp
-        self.role, self.rows, self.cols = role, rows, cols   # op(X) is rows x cols
+        self.role, self.rows, self.cols = role, rows, cols   # op(X) (stored matrix if stored)
+        self.stored = stored
 
     @property
     def shape(self):
@@ -122,6 +124,7 @@ def load() -> ctypes.CDLL:
         lib.split3_sgd_update.argtypes = [_p, _i64, _p, _p, ctypes.c_float]
         lib.split3_presplit.argtypes = [_p, ctypes.c_int, _i64, _i64, _p, _i64, ctypes.c_int, _p, _p,
                                         _i64, _p]
+        lib.split3_presplit_stored.argtypes = [_p, _i64, _i64, _p, _i64, _p, _p, _i64, _p]
         lib.split3_timing_read.argtypes = [_p, ctypes.POINTER(ctypes.c_double),
                                            ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]
         lib.split3_status_string.restype = ctypes.c_char_p
@@ -271,19 +274,39 @@ class Handle:
             raise Split3Error(st, "split3_presplit")
         return Planes(hi, lo, sexp, role, rows, cols)
 
+    def presplit_stored(self, X: torch.Tensor) -> Planes:
+        """Split the stored matrix X (rows x cols) once, without a transpose; the planes serve
+        sgemm_ex as A or B, with transA / transB as for the fp32 matrix."""
+        _check_mat(X, "X")
+        rows, cols = X.shape
+        ldp = plane_ld(cols)
+        hi = torch.empty((rows, ldp), dtype=torch.int16, device=X.device)
+        lo = torch.empty((rows, ldp), dtype=torch.int16, device=X.device)
+        sexp = torch.empty(1, dtype=torch.int32, device=X.device)    # written by the split
+        self._bind_stream()
+        st = self._lib.split3_presplit_stored(self._h, rows, cols, _ptr(X), _ld(X), _ptr(hi), _ptr(lo), ldp,
+                                              _ptr(sexp))
+        if st != OK:
+            raise Split3Error(st, "split3_presplit_stored")
+        return Planes(hi, lo, sexp, None, rows, cols, stored=True)
+
     def sgemm_ex(self, A, B, transA: bool = False, transB: bool = False, out=None,
                  four_term: bool = False, one_term: bool = False, check_finite: bool = False,
                  bf16x3: bool = False):
         """C = op(A) @ op(B); A / B are fp32 CUDA tensors or Planes from presplit()."""
         def desc(X, trans, role, name):
             if isinstance(X, Planes):
+                if X.stored:
+                    shp = (X.cols, X.rows) if trans else (X.rows, X.cols)
+                    return split3_matrix(None, 0, int(trans), X.hi.data_ptr(), X.lo.data_ptr(), X.hi.stride(0),
+                                         X.sexp.data_ptr(), 1), shp
                 if X.role != role:
                     raise ValueError(f"{name}: planes were split for role {X.role}")
                 return split3_matrix(None, 0, 0, X.hi.data_ptr(), X.lo.data_ptr(), X.hi.stride(0),
-                                     X.sexp.data_ptr()), X.shape
+                                     X.sexp.data_ptr(), 0), X.shape
             _check_mat(X, name)
             shp = (X.shape[1], X.shape[0]) if trans else tuple(X.shape)
-            return split3_matrix(X.data_ptr(), _ld(X), int(trans), None, None, 0, None), shp
+            return split3_matrix(X.data_ptr(), _ld(X), int(trans), None, None, 0, None, 0), shp
 
         da, (M, K) = desc(A, transA, 0, "A")
         db, (K2, N) = desc(B, transB, 1, "B")
