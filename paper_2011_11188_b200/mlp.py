@@ -47,11 +47,18 @@ class DenseNet:
     def _mm(self, A, B, transA=False, transB=False):
         return self.h.sgemm_ex(A, B, transA=transA, transB=transB, **MODES[self.mode])
 
+    # matrices at least this large are split once per step and reused; smaller ones go to the GEMMs
+    # as fp32 (an eager small net is host-bound: a separate split is one more call per matrix)
+    REUSE_MIN_ELEMS = 4 << 20
+
     def _split(self, X):
         """The plain split of a stored matrix (split3_presplit_stored), reused by every GEMM that
         reads X in the step: W in X*W and dZ*W^T, H in H*W and H^T*dZ, dZ in H^T*dZ and dZ*W^T.
-        Same planes and scale as splitting inside each call -> bitwise the same products."""
-        return self.h.presplit_stored(X)
+        Same planes and scale as splitting inside each call -> bitwise the same products, so small
+        matrices in eager mode are simply passed as fp32 (split inside each GEMM call)."""
+        if X.numel() >= self.REUSE_MIN_ELEMS or torch.cuda.is_current_stream_capturing():
+            return self.h.presplit_stored(X)
+        return X
 
     def _forward(self, X):
         """(activations [X, H1, ..., logits], planes of [X, H1, ...], planes of the weights)."""
