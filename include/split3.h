@@ -68,7 +68,8 @@ typedef enum split3_status {
  *   SPLIT3_MN_MAJOR=0     K-major planes for every operand (transposing splits) instead of
  *                         MN-major planes for a row-major B / a transposed A;
  *   SPLIT3_PREP_MAX=<n>   use the one-launch max-abs + split front end for eager calls whose
- *                         fp32 operands hold <= n elements together (default 4 Mi; 0 = never). */
+ *                         fp32 operands hold <= n elements together (default 4 Mi; 0 = never);
+ *   SPLIT3_FUSE_B=0|1|2, SPLIT3_FUSE_B_MAX_M=<m>   the fused split of B (split3_set_fused_split). */
 int split3_sgemm_create(split3_handle_t *h, int device, void *cuda_stream);
 
 /* Rebind the handle to another stream of the same device. */
@@ -91,9 +92,10 @@ int split3_sgemm_set_workspace(split3_handle_t h, void *dptr, size_t bytes);
 
 /* ---- the whole method --------------------------------------------------------------- */
 
-/* C = A*B emulated by FP16 tensor-core GEMMs.  Enqueues: scalar reset,
- * max-abs of A and B, split of A and B into FP16 planes (B planes stored transposed,
- * N x K, K-major), and the tcgen05 GEMM with fused rescaling epilogue.  C is overwritten
+/* C = A*B emulated by FP16 tensor-core GEMMs.  Enqueues: max-abs of A and B,
+ * split of A and B into FP16 planes (A: M x K K-major; B: K x N MN-major, no transpose), and the
+ * tcgen05 GEMM with fused rescaling epilogue — or, for small M (split3_set_fused_split), the
+ * split of A and a GEMM that splits B's fp32 tiles in shared memory.  C is overwritten
  * (beta = 0).  M == 0 or N == 0: no-op.  K == 0: C is zero-filled.
  * Non-finite inputs: without SPLIT3_CHECK_FINITE they propagate into the rows/columns of C
  * that touch them (the max-abs skips them); with it the call synchronises and returns
@@ -250,6 +252,18 @@ int split3_set_wave_sync(split3_handle_t h, int enable);
  * eviction policy of the A-plane and B-plane TMA loads (0 normal, 1 evict_first, 2 evict_last).
  * Scheduling only: results are identical for every setting. */
 int split3_set_schedule(split3_handle_t h, int group_m, int l2_policy_a, int l2_policy_b);
+
+/* Fused split of B (Eq. A_1, applied inside the GEMM): for a
+ * 3-term call whose B is a row-major K x N fp32 matrix (not pre-split, transB = 0), 16-byte
+ * aligned with ld % 4 == 0, the GEMM TMA-loads B's fp32 tiles into shared memory and converter
+ * warps split them there in place, so B's planes never go through HBM (only the max-abs pass
+ * reads B beforehand).  The planes, and therefore C, are bit-identical to the separate split.
+ * mode 0: off; 1 (default): when M <= max_m (default 2048: each B tile is converted once per
+ * 256-row tile row, and the extra shared-memory traffic slows the GEMM ~11 %, which the saved
+ * 8 B/element of B's split outweighs for small M) and the call is not a one-launch small call;
+ * 2: whenever eligible.  max_m = 0 keeps the current threshold.  Env: SPLIT3_FUSE_B,
+ * SPLIT3_FUSE_B_MAX_M at handle creation.  INVALID_VALUE for mode outside 0..2 or max_m < 0. */
+int split3_set_fused_split(split3_handle_t h, int mode, int64_t max_m);
 
 /* ---- measurement hooks (bench.py's roofline; no effect on results) ---------------------- */
 

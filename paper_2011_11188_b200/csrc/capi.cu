@@ -35,6 +35,11 @@ struct split3_ctx {
     int64_t prep_max = split3::kPrepMaxElems;   // elements of A + B up to which it is used (env SPLIT3_PREP_MAX)
     int mn_major = 1;   // MN-major planes for a row-major B / a transposed A (no transposing split);
                         // env SPLIT3_MN_MAJOR=0: off (K-major planes, transposing split)
+    // fused B: an fp32 B is split inside the GEMM (converter warps) instead of
+    // by a separate pass.  0 off, 1 auto (M <= fuse_b_max_m and not a one-launch small call),
+    // 2 whenever eligible (measured: profiles/fused_b_r01.md).  env SPLIT3_FUSE_B, SPLIT3_FUSE_B_MAX_M
+    int fuse_b = 1;
+    int64_t fuse_b_max_m = 2048;
     split3::GemmTuneIn tune;
     unsigned* d_counters = nullptr;   // 256 B of device scratch owned by the handle
     // host-buffer entry: copy-in / copy-out streams and events, created on first use
@@ -203,6 +208,8 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
     }
     if (const char* e = getenv("SPLIT3_MN_MAJOR")) c->mn_major = atoi(e) != 0;
     if (const char* e = getenv("SPLIT3_PREP_MAX")) c->prep_max = atoll(e);
+    if (const char* e = getenv("SPLIT3_FUSE_B")) c->fuse_b = atoi(e);
+    if (const char* e = getenv("SPLIT3_FUSE_B_MAX_M")) c->fuse_b_max_m = atoll(e);
     *h = c;
     return SPLIT3_OK;
 }
@@ -453,6 +460,10 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     // scalars: maxA = maxB = 0.0f, sA = sB = 0, badA = badB = INT64_MAX.  The common path (both
     // operands fp32, no check) needs no reset: the two-matrix max-abs writes maxA/maxB itself.
     const bool fast_max = needA && needB && !check;
+    // fused B (NEXT #2): 3-term, row-major fp32 B that TMA can read (16-B aligned, ld % 4 == 0)
+    const bool small_call = fast_max && h->mn_major && h->prep_ok && h->prep_max >= M * K + K * N;
+    const bool fuse_b = needB && !B->trans && terms == 3 && aligned(B->data, 16) && (B->ld % 4) == 0 &&
+                        (h->fuse_b == 2 || (h->fuse_b == 1 && M <= h->fuse_b_max_m && !small_call));
     // (both operands pre-split: no max-abs at all, nothing to reset)
     if (!fast_max && (needA || needB) && cudaMemsetAsync(h->ws, 0, 32, h->stream) != cudaSuccess)
         return SPLIT3_ERR_CUDA;
@@ -475,7 +486,7 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     // replay faster than one cooperative node: 0.361 vs 0.403 ms per small-MLP step)
     bool prepped = false;
     cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
-    if (fast_max && h->mn_major && h->prep_ok && h->prep_max >= M * K + K * N &&
+    if (!fuse_b && small_call &&
         cudaStreamIsCapturing(h->stream, &cap_st) == cudaSuccess && cap_st == cudaStreamCaptureStatusNone) {
         const split3::PrepOperand pa{A->data, A->trans ? K : M, A->trans ? M : K, A->ld, w.A1, w.A2,
                                      A->trans ? w.ldpa_mn : w.ldpa, w.maxA, w.sA};
@@ -546,8 +557,10 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
         if (st) return st;
         A1 = w.A1; A2 = w.A2; sA = w.sA; ldpa = w.ldpa;
     }
-    const bool b_mn = (needB && !B->trans && h->mn_major) || (!needB && B->stored && !B->trans);
-    if (prepped) {
+    const bool b_mn = (needB && !B->trans && (h->mn_major || fuse_b)) || (!needB && B->stored && !B->trans);
+    if (fuse_b) {
+        sB = w.sB;   // written by the GEMM (the planes never reach HBM)
+    } else if (prepped) {
         B1t = w.B1t; B2t = w.B2t; sB = w.sB; ldpb = b_mn ? w.ldpb_mn : w.ldpb;
     } else if (needB && b_mn) {
         if ((n = split3::launch_split(h->stream, K, N, B->data, B->ld, w.maxB, w.B1t, w.B2t, w.ldpb_mn, w.sB,
@@ -571,7 +584,8 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     int err = 0;
     n = split3::launch_gemm3(h->stream, M, N, K, A1, A2, ldpa, sA, B1t, B2t, ldpb, sB, C, ldc, terms,
                              h->num_sms, h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune, partial,
-                             partial_elems, &err, nullptr, nullptr, (b_mn ? 1 : 0) | (a_mn ? 2 : 0));
+                             partial_elems, &err, nullptr, nullptr, (b_mn ? 1 : 0) | (a_mn ? 2 : 0),
+                             fuse_b ? B->data : nullptr, B->ld, w.maxB);
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
     launches += n;
@@ -705,6 +719,13 @@ int split3_set_schedule(split3_handle_t h, int group_m, int l2_policy_a, int l2_
 int split3_set_wave_sync(split3_handle_t h, int enable) {
     if (!h) return SPLIT3_ERR_INVALID_VALUE;
     h->wave_sync = enable != 0;
+    return SPLIT3_OK;
+}
+
+int split3_set_fused_split(split3_handle_t h, int mode, int64_t max_m) {
+    if (!h || mode < 0 || mode > 2 || max_m < 0) return SPLIT3_ERR_INVALID_VALUE;
+    h->fuse_b = mode;
+    if (max_m > 0) h->fuse_b_max_m = max_m;
     return SPLIT3_OK;
 }
 

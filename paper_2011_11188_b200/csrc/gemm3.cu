@@ -31,6 +31,7 @@
 #include <atomic>
 
 #include "internal.h"
+#include "split_math.h"
 
 namespace split3 {
 namespace {
@@ -40,6 +41,10 @@ constexpr int BK = 64;                              // 64 fp16 = 128 B = one swi
 constexpr int TILE_A_BYTES = BM * BK * 2;           // 16 KB
 constexpr int NUM_EPI_WARPS = 8;                    // 2 per TMEM lane quadrant
 constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;   // TMA warp, MMA warp, epilogue warps
+constexpr int NUM_CONV_WARPS = 2;                   // fused-B variant: fp32 -> plane converter warps
+constexpr int LAY_FB = 4;                           // LAY bit 2: B arrives as fp32, split in SMEM
+template <int LAY>
+struct NThr { static constexpr int v = NUM_THREADS + ((LAY & LAY_FB) ? 32 * NUM_CONV_WARPS : 0); };
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;         // shared::cluster address of the leader CTA
 
@@ -132,6 +137,33 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
         "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & PEER_MASK), "r"(x), "r"(y), "l"(policy)
         : "memory");
 }
+// 1-SM TMA into this CTA's smem, transaction bytes on this CTA's barrier (fused-B fp32 tiles).
+__device__ __forceinline__ void tma_load_2d_cta(uint32_t dst, const CUtensorMap* map, uint32_t bar, int32_t x,
+                                                int32_t y, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y), "l"(policy)
+        : "memory");
+}
+// arrive on the LEADER's barrier, releasing this thread's prior writes at cluster scope (the
+// converters' plane stores, read by the leader-issued MMAs)
+__device__ __forceinline__ void mbar_arrive_leader_cluster(uint32_t bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar & PEER_MASK) : "memory");
+}
+// wait with acquire at cluster scope (pairs with mbar_arrive_leader_cluster)
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!done);
+}
 // TMA store of a shared-memory box to global (bulk async group of the issuing thread)
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int32_t x, int32_t y) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -143,6 +175,14 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ float4 ld_shared_v4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void st_shared_v2u(uint32_t addr, uint2 v) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(v.x), "r"(v.y) : "memory");
+}
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
@@ -278,8 +318,43 @@ __device__ __forceinline__ void promote_all(uint32_t taddr, float (&master)[NCOL
 // LAY bit 0 (BMN): the B planes are MN-major (K x N row-major, as split from a row-major K x N fp32
 // B without a transpose), else K-major (N x K); bit 1 (AMN): likewise A (K x M planes of a stored
 // K x M fp32 A = op(A)^T), else K-major (M x K).
+// Fused-B stage layout: the fp32 B tile of a k-block (64 k-rows x 128 N, 512-B
+// rows, no swizzle) is TMA-loaded into the stage's 32 KB B region and split IN PLACE, one K = 16
+// MMA step (16 k-rows = 8 KB) at a time: the step's planes take exactly its own 8 KB,
+//     hi: N atom 0 at +0, N atom 1 at +2 KB;  lo: +4 KB, +6 KB   (MN-major SW128, SBO 1 KB),
+// so the MMA reads B1 at B_OFF + 8 KB * k with LBO 2 KB, B2 at +4 KB.
+constexpr int FB_STEP_BYTES = 8192;
+constexpr int FB_LBO = 2048;
+constexpr int FB_LO_OFF = 4096;
+
+// Split one K step in place (one converter warp): each of the 16 LDS.128 reads one fp32 k-row
+// (lane L: N values 4L..4L+3, conflict-free), all reads precede all writes (__syncwarp), then every
+// lane stores two 8-B pieces (hi, lo) of 16-B SW128 chunks: lanes 0-15 -> N atom 0, 16-31 -> atom 1.
+__device__ __forceinline__ void convert_step(uint32_t step, int lane, float f) {
+    float4 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = ld_shared_v4(step + (uint32_t)r * 512u + (uint32_t)lane * 16u);
+    __syncwarp();
+    const int l16 = lane & 15;
+    const uint32_t base = step + (uint32_t)(lane >> 4) * (uint32_t)FB_LBO + (uint32_t)((l16 & 1) << 3);
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+        uint2 hi, lo;
+        split4(v[r], f, hi, lo);
+        const uint32_t a = base + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u +
+                           ((uint32_t)((l16 >> 1) ^ (r & 7)) << 4);
+        st_shared_v2u(a, hi);
+        st_shared_v2u(a + FB_LO_OFF, lo);
+    }
+}
+
+// LAY bit 2 (FB, fused B; 3-term, row-major K x N fp32 B only): mapB1 is a map
+// over the fp32 B, TMA-loaded per k-block into the stage's B region; converter warps 10..11 apply
+// Eq. A_1 in place (split4, the split kernels' arithmetic) and write the B1/B2 planes in the
+// layout above.  The scale exponent comes from *fb_maxB; CTA 0 stores it to *fb_sB (read by the
+// split-K reduction).
 template <int TERMS, int BN_, int LAY>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NThr<LAY>::v, 1)
 gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapA2,
              const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapB2,
              const __grid_constant__ CUtensorMap mapA3, const __grid_constant__ CUtensorMap mapB3,
@@ -287,10 +362,15 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
              int M, int N, int K, int promo_kb, const int32_t* __restrict__ d_sA,
              const int32_t* __restrict__ d_sB, float* __restrict__ C, int64_t ldc,
              unsigned* __restrict__ wave_counter, const GemmTune tune,
-             const SplitPlan plan, float* __restrict__ partial) {
+             const SplitPlan plan, float* __restrict__ partial, const float* __restrict__ fb_maxB,
+             int32_t* __restrict__ fb_sB) {
     constexpr bool BF3 = TERMS == 6;                 // bf16 x 3 split (NEXT #4): 3 planes, 6 products
     constexpr int PL = BF3 ? 3 : 2;
+    constexpr bool FB = (LAY & LAY_FB) != 0;
+    static_assert(!FB || (TERMS == 3 && (LAY & 1)), "fused B: 3-term, MN-major B only");
     using G = Geo<BN_, PL>;
+    constexpr int F32_BYTES = G::BNH * BK * 4;   // fused B: one fp32 tile = the stage's B region
+    static_assert(!FB || F32_BYTES == 2 * G::TILE_B_BYTES, "fused B: in-place split");
     constexpr int STAGES = G::STAGES;
     constexpr int STAGE_BYTES = G::STAGE_BYTES;
     constexpr int TILE_B_BYTES = G::TILE_B_BYTES;
@@ -302,10 +382,11 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     constexpr uint32_t COL_MID = HB * BN_;
     constexpr uint32_t COL_LO = COL_MID + BN_;
     static_assert(HB * BN_ + (HAS_MID ? BN_ : 0) + (TERMS == 4 ? BN_ : 0) <= 512, "TMEM budget");
-    constexpr uint32_t TX_BYTES = 2u * (LOAD_LO ? STAGE_BYTES : TILE_A_BYTES + TILE_B_BYTES);
+    constexpr uint32_t TX_BYTES =
+        FB ? 2u * (2 * TILE_A_BYTES) : 2u * (LOAD_LO ? STAGE_BYTES : TILE_A_BYTES + TILE_B_BYTES);
     constexpr bool BMN = (LAY & 1) != 0, AMN = (LAY & 2) != 0;
     constexpr uint32_t IDESC = make_idesc(2 * BM, BN_, BF3) | (AMN ? (1u << 15) : 0u) | (BMN ? (1u << 16) : 0u);
-    constexpr uint64_t DKB = BMN ? (2048 >> 4) : (32 >> 4);   // B descriptor step per K = 16
+    constexpr uint64_t DKB = FB ? (FB_STEP_BYTES >> 4) : BMN ? (2048 >> 4) : (32 >> 4);   // B step per K = 16
     constexpr uint64_t DKA = AMN ? (2048 >> 4) : (32 >> 4);   // A descriptor step per K = 16
     constexpr int MN_BOX_BYTES = 64 * BK * 2;                 // one 64 (N) x 64 (K) box
     constexpr int B_OFF = PL * TILE_A_BYTES;         // B planes follow the A planes in a stage
@@ -323,7 +404,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     uint64_t* hempty_bar = bars + 2 * STAGES + 2;     // [2]        leader: D_hi chunk drained
     uint64_t* mfull_bar = bars + 2 * STAGES + 4;      // [1]        both: D_mid (D_lo) ready
     uint64_t* mempty_bar = bars + 2 * STAGES + 5;     // [1]        leader: D_mid drained
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 6);
+    uint64_t* ffull_bar = bars + 2 * STAGES + 6;      // [STAGES]   own CTA: fused B fp32 tile landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 6);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -343,9 +425,12 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         if (LOAD_LO) { tma_prefetch(&mapA2); tma_prefetch(&mapB2); }
         if (BF3) { tma_prefetch(&mapA3); tma_prefetch(&mapB3); }
         for (int i = 0; i < STAGES; i++) {
-            mbar_init(smem_u32(&full_bar[i]), 1);
+            // fused B: the leader's full barrier also collects one arrival per converter warp of both CTAs
+            mbar_init(smem_u32(&full_bar[i]), FB ? 1 + 2 * NUM_CONV_WARPS : 1);
             mbar_init(smem_u32(&empty_bar[i]), 1);
         }
+        if (FB)
+            for (int i = 0; i < STAGES; i++) mbar_init(smem_u32(&ffull_bar[i]), 1);
         for (int i = 0; i < 2; i++) {
             mbar_init(smem_u32(&hfull_bar[i]), 1);
             mbar_init(smem_u32(&hempty_bar[i]), EPI_ARRIVALS);
@@ -433,11 +518,16 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                         }
                     };
                     if (leader) mbar_expect_tx(fb, TX_BYTES);
+                    if (FB) {   // fp32 B tile into the stage's B region (own CTA, own barrier)
+                        const uint32_t ffb = smem_u32(&ffull_bar[stage]);
+                        mbar_expect_tx(ffb, F32_BYTES);
+                        tma_load_2d_cta(smem_u32(st + B_OFF), &mapB1, ffb, y_b, x, tune.pol_b);   // 128 N x 64 K
+                    }
                     load_a(0, &mapA1);
-                    load_b(B_OFF, &mapB1);
+                    if (!FB) load_b(B_OFF, &mapB1);
                     if (LOAD_LO) {
                         load_a(TILE_A_BYTES, &mapA2);
-                        load_b(B_OFF + TILE_B_BYTES, &mapB2);
+                        if (!FB) load_b(B_OFF + TILE_B_BYTES, &mapB2);
                     }
                     if (BF3) {
                         load_a(2 * TILE_A_BYTES, &mapA3);
@@ -488,10 +578,11 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     const uint64_t a2 = adesc(TILE_A_BYTES);
                     const uint64_t a3 = adesc(2 * TILE_A_BYTES);
                     auto bdesc = [&](int off) {
-                        return BMN ? sdesc_mn_sw128(smem_u32(st + off), MN_BOX_BYTES) : sdesc_sw128(smem_u32(st + off));
+                        return FB ? sdesc_mn_sw128(smem_u32(st + off), FB_LBO)
+                                  : BMN ? sdesc_mn_sw128(smem_u32(st + off), MN_BOX_BYTES) : sdesc_sw128(smem_u32(st + off));
                     };
                     const uint64_t b1 = bdesc(B_OFF);
-                    const uint64_t b2 = bdesc(B_OFF + TILE_B_BYTES);
+                    const uint64_t b2 = bdesc(B_OFF + (FB ? FB_LO_OFF : TILE_B_BYTES));
                     const uint64_t b3 = bdesc(B_OFF + 2 * TILE_B_BYTES);
                     // D_hi first at both ends of a unit: at the start the epilogue frees D_hi before
                     // D_mid; at the end the last D_hi drain overlaps the last D_mid MMAs
@@ -552,12 +643,43 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                 cc++;
             }
         }
+    } else if (FB && warp >= 2 + NUM_EPI_WARPS) {
+        // ===================== fused-B converters (warps 10..11, both CTAs) ================
+        // Per k-block: wait for the fp32 tile in the stage, split K steps cw and cw + 2 in place,
+        // make the plane stores visible to the async proxy, arrive on the leader's full barrier.
+        const int cw = warp - (2 + NUM_EPI_WARPS);
+        const int sB = scale_exp_dev(*fb_maxB);
+        const float f = pow2_neg(sB);
+        if (fb_sB && blockIdx.x == 0 && cw == 0 && lane == 0) *fb_sB = sB;
+        static_assert(NUM_CONV_WARPS == 2 && BK / 16 == 4, "two K steps per converter warp");
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int64_t unit = pair; unit < num_units; unit += num_pairs) {
+            int64_t tile_unused;
+            int kb_begin, kb_end, slot;
+            decode_unit(unit, plan, num_kb, kps, tile_unused, kb_begin, kb_end, slot);
+            for (int kb = kb_begin; kb < kb_end; kb++) {
+                mbar_wait(smem_u32(&ffull_bar[stage]), phase);
+                const uint32_t breg = smem_u32(smem + stage * STAGE_BYTES + B_OFF);
+#ifndef SPLIT3_EXP_NO_CONVERT   // experiment only: time the fused-B pipeline without the conversion
+                convert_step(breg + (uint32_t)cw * FB_STEP_BYTES, lane, f);
+                convert_step(breg + (uint32_t)(cw + 2) * FB_STEP_BYTES, lane, f);
+#else
+                (void)breg; (void)f;
+#endif
+                fence_async_smem();   // generic-proxy plane stores -> visible to the MMA (async proxy)
+                __syncwarp();
+                if (lane == 0) mbar_arrive_leader(smem_u32(&full_bar[stage]));
+                __syncwarp();
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
     } else {
         // ===================== epilogue (warps 2..9, both CTAs) =====================
         // warp w reads TMEM lane quadrant (w % 4) and columns [NCOL * half, + NCOL).
         const int quad = warp & 3;
         const int half = (warp - 2) >> 2;
-        const int sAB = *d_sA + *d_sB;
+        const int sAB = *d_sA + (FB ? scale_exp_dev(*fb_maxB) : *d_sB);
         const bool fast = sAB >= -126 && sAB <= 127;
         const float fscale = fast ? __uint_as_float((unsigned)(sAB + 127) << 23) : 1.0f;
         const bool vec_ok = (ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(C) & 15u) == 0);
@@ -697,7 +819,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         }
     }
 
-    if (warp >= 2 && tma_store && lane == 0) bulk_wait0();   // the C stores have completed
+    if (warp >= 2 && warp < 2 + NUM_EPI_WARPS && tma_store && lane == 0) bulk_wait0();   // C stores done
 #ifdef SPLIT3_EXP_TRACE
     if (threadIdx.x == 0) {
         atomicAdd(&g_trace[blockIdx.x][7], (unsigned long long)(clock64() - _tkernel));
@@ -822,13 +944,28 @@ bool make_plane_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K,
     return r == CUDA_SUCCESS;
 }
 
+// 2-D map over an fp32 matrix (rows x cols, leading dimension ld elements), box box_cols x
+// box_rows, no swizzle (the fused-B staging tile; the converters read it row by row).
+bool make_f32_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t ld, int box_cols,
+                  int box_rows) {
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int TERMS, int BN_, int LAY>
 int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap& a1,
              const CUtensorMap& a2, const CUtensorMap& b1, const CUtensorMap& b2, const CUtensorMap& a3,
              const CUtensorMap& b3, const CUtensorMap& mc, int tma_store,
              const int32_t* d_sA, const int32_t* d_sB, float* C, int64_t ldc, int num_sms,
              int promo_kb, unsigned* wave_counter, const GemmTune& tune, const SplitPlan& plan,
-             float* partial) {
+             float* partial, const float* fb_maxB = nullptr, int32_t* fb_sB = nullptr) {
     constexpr int SMEM_BYTES = Geo<BN_, TERMS == 6 ? 3 : 2>::SMEM;
     // the dynamic-smem opt-in is per device: remember it per device ordinal
     static std::atomic<uint64_t> attr_set{0};
@@ -844,9 +981,9 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
     const int64_t tiles = plan.whole + plan.nsplit * plan.slices;   // work units
     const int64_t pairs = num_sms / 2;
     const int grid = 2 * (int)(tiles < pairs ? tiles : pairs);
-    if (launch_k(gemm3_kernel<TERMS, BN_, LAY>, dim3((unsigned)grid), dim3(NUM_THREADS), SMEM_BYTES, st, a1, a2, b1, b2, a3,
-                 b3, mc, tma_store, (int)M, (int)N, (int)K, promo_kb, d_sA, d_sB, C, ldc, wave_counter, tune,
-                 plan, partial) != cudaSuccess)
+    if (launch_k(gemm3_kernel<TERMS, BN_, LAY>, dim3((unsigned)grid), dim3(NThr<LAY>::v), SMEM_BYTES, st, a1, a2, b1,
+                 b2, a3, b3, mc, tma_store, (int)M, (int)N, (int)K, promo_kb, d_sA, d_sB, C, ldc, wave_counter,
+                 tune, plan, partial, fb_maxB, fb_sB) != cudaSuccess)
         return -1;
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
@@ -891,9 +1028,16 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
                  const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB, float* C, int64_t ldc,
                  int terms, int num_sms, int promo_kb, unsigned* wave_counter, const GemmTuneIn& tin,
                  float* partial, int64_t partial_elems, int* err, const uint16_t* A3, const uint16_t* B3t,
-                 int mn) {
+                 int mn, const float* Bf, int64_t ldb, const float* d_maxB) {
     const bool b_mn = (mn & 1) != 0, a_mn = (mn & 2) != 0;
     CUtensorMap ma1, ma2, mb1, mb2, ma3, mb3;
+    if (Bf) {   // fused B (3-term): fp32 B map in place of the B plane maps
+        if (terms != 3 || !b_mn || !d_maxB || (ldb % 4) != 0 || (reinterpret_cast<uintptr_t>(Bf) & 15u) != 0) {
+            *err = 1;   // SPLIT3_ERR_INVALID_VALUE
+            return -1;
+        }
+        B1t = B2t = nullptr;
+    }
     const uint16_t* A2e = terms == 1 ? A1 : A2;
     const uint16_t* B2e = terms == 1 ? B1t : B2t;
     const int bnh = (terms == 4 ? 128 : 256) / 2;
@@ -904,7 +1048,10 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     auto map_a = [&](CUtensorMap* m, const uint16_t* p) {
         return a_mn ? make_plane_map(m, p, K, M, ldpa, BK) : make_plane_map(m, p, M, K, ldpa, BM);
     };
-    if (!map_a(&ma1, A1) || !map_a(&ma2, A2e) || !map_b(&mb1, B1t) || !map_b(&mb2, B2e)) {
+    // fused B: row-major K x N fp32, box 128 N x 64 K
+    const bool bmaps = Bf ? make_f32_map(&mb1, Bf, K, N, ldb, bnh, BK) : (map_b(&mb1, B1t) && map_b(&mb2, B2e));
+    if (Bf) mb2 = mb1;
+    if (!map_a(&ma1, A1) || !map_a(&ma2, A2e) || !bmaps) {
         *err = 4;   // SPLIT3_ERR_CUDA
         return -1;
     }
@@ -938,6 +1085,10 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
         switch (mn & 3) { case 1: r = launch_t<4, 128, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 2: r = launch_t<4, 128, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 3: r = launch_t<4, 128, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; default: r = launch_t<4, 128, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); }
     } else if (terms == 6) {
         switch (mn & 3) { case 1: r = launch_t<6, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 2: r = launch_t<6, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 3: r = launch_t<6, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; default: r = launch_t<6, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); }
+    } else if (Bf) {
+        int32_t* sBw = const_cast<int32_t*>(d_sB);
+        if (mn & 2) r = launch_t<3, 256, 7>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial, d_maxB, sBw);
+        else r = launch_t<3, 256, 5>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial, d_maxB, sBw);
     } else {
         switch (mn & 3) { case 1: r = launch_t<3, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 2: r = launch_t<3, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 3: r = launch_t<3, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; default: r = launch_t<3, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); }
     }

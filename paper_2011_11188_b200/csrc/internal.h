@@ -133,13 +133,17 @@ int64_t gemm3_partial_elems(const SplitPlan& p, int terms);   // floats of parti
 // mn bit 0: the B planes are MN-major, K x N row-major with leading dimension ldpb >= N (the
 // plain split of a row-major K x N B), else K-major N x K with ldpb >= K; bit 1: the A planes
 // are MN-major, K x M with ldpa >= M (the plain split of a stored K x M A^T), else M x K.  `partial` (may be NULL: no split-K) holds partial_elems floats.
+// Fused B (terms == 3 only): Bf != NULL is the fp32 B itself (mn bit 0: K x N
+// row-major, else stored N x K; ldb % 4 == 0, 16-B aligned) and d_maxB its max-abs; the GEMM splits
+// it in shared memory (B1t/B2t are ignored) and writes the scale exponent to d_sB.
 // Returns kernels launched (1, or 2 with the split-K reduction) or -1 (*err set to a status).
 int launch_gemm3(cudaStream_t s, int64_t M, int64_t N, int64_t K,
                  const uint16_t* A1, const uint16_t* A2, int64_t ldpa, const int32_t* d_sA,
                  const uint16_t* B1t, const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB,
                  float* C, int64_t ldc, int terms, int num_sms, int promo_kb,
                  unsigned* wave_counter, const GemmTuneIn& tune, float* partial, int64_t partial_elems,
-                 int* err, const uint16_t* A3 = nullptr, const uint16_t* B3t = nullptr, int mn = 0);
+                 int* err, const uint16_t* A3 = nullptr, const uint16_t* B3t = nullptr, int mn = 0,
+                 const float* Bf = nullptr, int64_t ldb = 0, const float* d_maxB = nullptr);
 
 // ---- mlp_kernels.cu (NEXT #3: the non-GEMM steps of a dense-network training step) --------
 int launch_bias_act(cudaStream_t s, int64_t M, int64_t N, const float* Z, int64_t ldz, const float* b, float* H,

@@ -15,6 +15,7 @@
 #include <stdint.h>
 
 #include "internal.h"
+#include "split_math.h"
 
 namespace split3 {
 namespace {
@@ -185,27 +186,7 @@ __global__ void __launch_bounds__(256) maxabs_2d_kernel(const float* __restrict_
     block_fold(m, bad, d_max, d_bad);
 }
 
-// Scale exponent from the max-abs (reading R1): s = max(floor(log2 m) - 14, -127), s(0) = 0.
-__device__ __forceinline__ int scale_exp_dev(float m) {
-    unsigned b = __float_as_uint(m);
-    if (b == 0u) return 0;
-    int E = (b >= 0x00800000u) ? (int)(b >> 23) - 127 : (31 - __clz(b)) - 149;
-    int s = E - 14;
-    return s < -127 ? -127 : s;
-}
-
-// 2^-s as an fp32 (s in [-127, 113] -> exponent field 127 - s in [14, 254]: always normal).
-__device__ __forceinline__ float pow2_neg(int s) { return __uint_as_float((unsigned)(127 - s) << 23); }
-
-// Eq. A_1 for one value: returns (A1 bits, A2 bits).  __fmul_rn/__fsub_rn forbid contraction.
-__device__ __forceinline__ void split1(float x, float f, unsigned short& h1, unsigned short& h2) {
-    float xs = __fmul_rn(x, f);                       // exact: power-of-two scaling
-    __half a1 = __float2half_rn(xs);                  // cvt.rn.f16.f32
-    float r = __fsub_rn(xs, __half2float(a1));        // exact (DESIGN.md §3 R5)
-    __half a2 = __float2half_rn(__fmul_rn(r, 2048.0f));
-    h1 = __half_as_ushort(a1);
-    h2 = __half_as_ushort(a2);
-}
+// scale_exp_dev, pow2_neg, split1: split_math.h (shared with the fused-B GEMM converter)
 
 // Non-transposed split: planes rows x cols (ldp).  VEC: cols % 4 == 0, ld % 4 == 0, aligned.
 template <bool VEC>

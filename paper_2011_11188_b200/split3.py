@@ -40,7 +40,7 @@ EXPORTS = (
     "split3_sgemm_host_workspace_size", "split3_sgemm_host", "split3_last_bad_index",
     "split3_status_string", "split3_maxabs", "split3_split", "split3_gemm_planes",
     "split3_last_launch_count", "split3_timing_enable", "split3_timing_read",
-    "split3_set_promotion", "split3_set_wave_sync", "split3_set_schedule",
+    "split3_set_promotion", "split3_set_wave_sync", "split3_set_schedule", "split3_set_fused_split",
     "split3_sgemm_ex", "split3_presplit", "split3_presplit_stored", "split3_split_bf16x3", "split3_bias_act", "split3_relu_backward",
     "split3_softmax_xent", "split3_bias_grad", "split3_sgd_update",
 )
@@ -114,6 +114,7 @@ def load() -> ctypes.CDLL:
         lib.split3_set_promotion.argtypes = [_p, ctypes.c_int]
         lib.split3_set_wave_sync.argtypes = [_p, ctypes.c_int]
         lib.split3_set_schedule.argtypes = [_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        lib.split3_set_fused_split.argtypes = [_p, ctypes.c_int, _i64]
         lib.split3_sgemm_ex.argtypes = [_p, _i64, _i64, _i64, ctypes.POINTER(split3_matrix),
                                         ctypes.POINTER(split3_matrix), _p, _i64, ctypes.c_uint32]
         lib.split3_split_bf16x3.argtypes = [_p, _i64, _i64, _p, _i64, _p, _p, _p, _i64, ctypes.c_int]
@@ -218,6 +219,12 @@ class Handle:
         st = self._lib.split3_set_schedule(self._h, group_m, l2_policy_a, l2_policy_b)
         if st != OK:
             raise Split3Error(st, "split3_set_schedule")
+
+    def set_fused_split(self, mode: int, max_m: int = 0):
+        """Fused split of an fp32 B inside the GEMM (NEXT #2): 0 off, 1 auto (M <= max_m), 2 always."""
+        st = self._lib.split3_set_fused_split(self._h, int(mode), int(max_m))
+        if st != OK:
+            raise Split3Error(st, "split3_set_fused_split")
 
     def timing_enable(self, enable: bool = True):
         self._lib.split3_timing_enable(self._h, int(enable))

@@ -19,7 +19,9 @@ def _handle(prep_max: int | None):
     else:
         os.environ["SPLIT3_PREP_MAX"] = str(prep_max)
     try:
-        return s3.Handle(0)
+        h = s3.Handle(0)
+        h.set_fused_split(0)     # this file compares the front ends of the separate-split path
+        return h
     finally:
         if old is None:
             os.environ.pop("SPLIT3_PREP_MAX", None)
