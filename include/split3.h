@@ -105,8 +105,11 @@ int split3_sgemm(split3_handle_t h, int64_t M, int64_t N, int64_t K,
                  float *C, int64_t ldc, uint32_t flags);
 
 /* Same computation with HOST buffers (pageable or pinned): copies A and B to the workspace
- * staging area of the handle's device, runs split3_sgemm, copies C back, and synchronises
- * the handle's stream before returning.  Device staging for A, B and C is taken from the
+ * staging area of the handle's device, runs the method, copies C back, and synchronises
+ * the handle's stream before returning.  C is bit-identical to split3_sgemm on the same inputs.
+ * Pipelined: B is copied first, then A in up to 8 row blocks, each split and
+ * multiplied as soon as it lands while the next one copies in, and C row blocks copy out
+ * underneath; env SPLIT3_HOST_BLOCKS=<1..8> at handle creation fixes the block count.  Device staging for A, B and C is taken from the
  * workspace, which must hold split3_sgemm_host_workspace_size(M, N, K, flags) bytes.
  * Host layout is packed row-major (lda = K, ldb = N, ldc = N). */
 size_t split3_sgemm_host_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags);
@@ -116,6 +119,12 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K,
 /* After SPLIT3_ERR_NOT_FINITE: first offending linear index (row*cols+col) of A, or
  * M*K + index within B; -1 if none recorded. */
 int64_t split3_last_bad_index(split3_handle_t h);
+
+/* Row blocks split3_sgemm_host has redone with the per-matrix scale since the handle was created
+ * (the host pipeline splits each A row block with its own scale exponent as it
+ * arrives; a block whose exponent is below the per-matrix one and that holds a nonzero
+ * |a| < 2^(sA-12) is redone so that C keeps the per-matrix bits).  -1 for a NULL handle. */
+int64_t split3_host_redo_count(split3_handle_t h);
 
 const char *split3_status_string(int status);
 

@@ -45,7 +45,10 @@ struct split3_ctx {
     // host-buffer entry: copy-in / copy-out streams and events, created on first use
     cudaStream_t s_in = nullptr, s_out = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_done = nullptr;
-    cudaEvent_t ev_rows[8] = {};
+    cudaEvent_t ev_rows[16] = {};      // C row block b computed
+    cudaEvent_t ev_arows[16] = {};     // A row block b copied in
+    int host_blocks = 0;               // row blocks of the host pipeline (0 = automatic; env SPLIT3_HOST_BLOCKS)
+    long long host_redo = 0;           // row blocks redone with the per-matrix scale (split3_host_redo_count)
     // measurement hooks: event triples (start, after split, after gemm) per timed call
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -209,6 +212,7 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
     if (const char* e = getenv("SPLIT3_MN_MAJOR")) c->mn_major = atoi(e) != 0;
     if (const char* e = getenv("SPLIT3_PREP_MAX")) c->prep_max = atoll(e);
     if (const char* e = getenv("SPLIT3_FUSE_B")) c->fuse_b = atoi(e);
+    if (const char* e = getenv("SPLIT3_HOST_BLOCKS")) c->host_blocks = std::min(std::max(atoi(e), 0), 8);
     if (const char* e = getenv("SPLIT3_FUSE_B_MAX_M")) c->fuse_b_max_m = atoll(e);
     *h = c;
     return SPLIT3_OK;
@@ -252,6 +256,7 @@ int split3_sgemm_set_workspace(split3_handle_t h, void* dptr, size_t bytes) {
 int64_t split3_last_bad_index(split3_handle_t h) { return h ? h->last_bad : -1; }
 
 int split3_last_launch_count(split3_handle_t h) { return h ? h->last_launches : 0; }
+int64_t split3_host_redo_count(split3_handle_t h) { return h ? h->host_redo : -1; }
 
 int split3_maxabs(split3_handle_t h, int64_t rows, int64_t cols, const float* X, int64_t ldx,
                   float* d_maxabs, int64_t* d_bad) {
@@ -794,9 +799,13 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
             return SPLIT3_ERR_CUDA;
         return SPLIT3_OK;
     }
-    // Pipelined path.  The per-matrix scale needs all of A (B) on the device before its split,
-    // so the overlap available is: split of A under the copy of B, and the copy-out of C row
-    // blocks under the GEMM of the following row blocks (copy engines run both directions).
+    // Pipelined path.  B first (its split needs all of B), then A in row blocks:
+    // each block is split with its OWN scale exponent as soon as it lands and multiplied while the
+    // next block copies in, and C row blocks copy out underneath (copy engines run both directions).
+    // A block exponent below the per-matrix one (reading R1) scales the block's planes, products and
+    // C partial sums by an exact power of two, so C gets the per-matrix bits, unless the block holds
+    // a nonzero |x| < 2^(sA-12) (fp16-subnormal planes): a check kernel flags such blocks after the
+    // last copy and they are redone with the per-matrix scale before the call returns.
     if (!h->s_in) {
         if (cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking) != cudaSuccess ||
             cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking) != cudaSuccess ||
@@ -806,26 +815,59 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
             return SPLIT3_ERR_CUDA;
         for (cudaEvent_t& e : h->ev_rows)
             if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return SPLIT3_ERR_CUDA;
+        for (cudaEvent_t& e : h->ev_arows)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return SPLIT3_ERR_CUDA;
     }
     cudaStream_t s0 = h->stream;
+    // row blocks: multiples of the 256-row pair tile, each >= 2 waves of tiles (more blocks shorten
+    // the exposed tail: the last block's split + GEMM + copy-out)
+    const int64_t tiles_n = (N + 255) / 256;
+    int nblk = 1;
+    if (h->host_blocks > 0) {
+        nblk = h->host_blocks;
+    } else {
+        while (nblk < 8 && ((M / (2 * nblk)) / 256) * tiles_n >= 2 * (h->num_sms / 2)) nblk *= 2;
+    }
+    const int64_t rows_per = ((M + nblk - 1) / nblk + 255) / 256 * 256;
+    // blocks (r0, rows): rows_per each; with >= 4 blocks the last one is cut into 1/2 + 1/4 + 1/4
+    // (each still >= 2 waves) so the exposed tail — its split, GEMM and copy-out — is 4x shorter
+    int64_t blk_r0[16], blk_mr[16];
+    nblk = 0;
+    for (int64_t r0 = 0; r0 < M; r0 += rows_per) {
+        blk_r0[nblk] = r0;
+        blk_mr[nblk++] = std::min(rows_per, M - r0);
+    }
+    if (h->host_blocks == 0 && nblk >= 4 && blk_mr[nblk - 1] == rows_per && rows_per % 1024 == 0) {
+        const int64_t r0 = blk_r0[nblk - 1], q = rows_per / 4;
+        blk_mr[nblk - 1] = 2 * q;
+        blk_r0[nblk] = r0 + 2 * q; blk_mr[nblk++] = q;
+        blk_r0[nblk] = r0 + 3 * q; blk_mr[nblk++] = q;
+    }
+    Carve w = carve(h->ws, M, N, K);
+    // per-block scalars (<= 12 blocks) in the scalars block: max bits [48, +48), min-nonzero bits
+    // [96, +48), exponents [144, +48), redo flags [192, +48)
+    uint8_t* sc = static_cast<uint8_t*>(h->ws);
+    unsigned* maxblk = reinterpret_cast<unsigned*>(sc + 48);
+    unsigned* minblk = reinterpret_cast<unsigned*>(sc + 96);
+    int32_t* sblk = reinterpret_cast<int32_t*>(sc + 144);
+    int32_t* flags_d = reinterpret_cast<int32_t*>(sc + 192);
     // copy-in must not overwrite the staging buffers while an earlier call on s0 still reads them
     if (cudaEventRecord(h->ev_done, s0) != cudaSuccess || cudaStreamWaitEvent(h->s_in, h->ev_done, 0) != cudaSuccess)
         return SPLIT3_ERR_CUDA;
-    if (cudaMemcpyAsync(dA, A_host, (size_t)M * K * 4, cudaMemcpyHostToDevice, h->s_in) != cudaSuccess ||
-        cudaEventRecord(h->ev_a, h->s_in) != cudaSuccess ||
-        cudaMemcpyAsync(dB, B_host, (size_t)K * N * 4, cudaMemcpyHostToDevice, h->s_in) != cudaSuccess ||
+    if (cudaMemcpyAsync(dB, B_host, (size_t)K * N * 4, cudaMemcpyHostToDevice, h->s_in) != cudaSuccess ||
         cudaEventRecord(h->ev_b, h->s_in) != cudaSuccess)
         return SPLIT3_ERR_CUDA;
-    Carve w = carve(h->ws, M, N, K);
+    for (int b = 0; b < nblk; b++) {
+        const int64_t r0 = blk_r0[b], mr = blk_mr[b];
+        if (cudaMemcpyAsync(dA + r0 * K, A_host + r0 * K, (size_t)mr * K * 4, cudaMemcpyHostToDevice, h->s_in) !=
+                cudaSuccess ||
+            cudaEventRecord(h->ev_arows[b], h->s_in) != cudaSuccess)
+            return SPLIT3_ERR_CUDA;
+    }
     int launches = 0, n;
-    if (cudaMemsetAsync(h->ws, 0, 32, s0) != cudaSuccess || cudaStreamWaitEvent(s0, h->ev_a, 0) != cudaSuccess)
+    if (cudaMemsetAsync(h->ws, 0, 32, s0) != cudaSuccess || cudaMemsetAsync(maxblk, 0, 48, s0) != cudaSuccess ||
+        cudaMemsetAsync(minblk, 0xFF, 48, s0) != cudaSuccess || cudaStreamWaitEvent(s0, h->ev_b, 0) != cudaSuccess)
         return SPLIT3_ERR_CUDA;
-    if ((n = split3::launch_maxabs(s0, M, K, dA, K, w.maxA, nullptr, h->num_sms)) < 0) return SPLIT3_ERR_CUDA;
-    launches += n;
-    if ((n = split3::launch_split(s0, M, K, dA, K, w.maxA, w.A1, w.A2, w.ldpa, w.sA, h->num_sms)) < 0)
-        return SPLIT3_ERR_CUDA;
-    launches += n;
-    if (cudaStreamWaitEvent(s0, h->ev_b, 0) != cudaSuccess) return SPLIT3_ERR_CUDA;
     if ((n = split3::launch_maxabs(s0, K, N, dB, N, w.maxB, nullptr, h->num_sms)) < 0) return SPLIT3_ERR_CUDA;
     launches += n;
     const bool b_mn = h->mn_major != 0;  // MN-major B planes (plain split) unless disabled
@@ -834,26 +876,55 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
                   : split3::launch_split_t(s0, K, N, dB, N, w.maxB, w.B1t, w.B2t, ldpb, w.sB, h->num_sms)) < 0)
         return SPLIT3_ERR_CUDA;
     launches += n;
-    // GEMM in row blocks (multiples of the 256-row pair tile); copy each block out as it completes
-    // more blocks shorten the exposed copy-out of the last one; each block keeps >= 2 waves of tiles
-    const int64_t tiles_n = (N + 255) / 256;
-    int nblk = 1;
-    while (nblk < 8 && ((M / (2 * nblk)) / 256) * tiles_n >= 2 * (h->num_sms / 2)) nblk *= 2;
-    int64_t rows_per = ((M + nblk - 1) / nblk + 255) / 256 * 256;
-    for (int b = 0; b < nblk; b++) {
-        const int64_t r0 = b * rows_per;
-        if (r0 >= M) break;
-        const int64_t mr = (M - r0 < rows_per) ? M - r0 : rows_per;
+    auto gemm_block = [&](int64_t r0, int64_t mr, const int32_t* d_sA) {
         int err = 0;
-        n = split3::launch_gemm3(s0, mr, N, K, w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa, w.ldpa, w.sA, w.B1t, w.B2t,
-                                 ldpb, w.sB, dC + r0 * N, N, terms_of(flags), h->num_sms, h->promo_kb,
-                                 h->wave_sync ? h->d_counters : nullptr, h->tune, nullptr, 0, &err, nullptr, nullptr,
-                                 b_mn ? 1 : 0);
-        if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
+        int r = split3::launch_gemm3(s0, mr, N, K, w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa, w.ldpa, d_sA, w.B1t, w.B2t,
+                                     ldpb, w.sB, dC + r0 * N, N, terms_of(flags), h->num_sms, h->promo_kb,
+                                     h->wave_sync ? h->d_counters : nullptr, h->tune, nullptr, 0, &err, nullptr,
+                                     nullptr, b_mn ? 1 : 0);
+        return r < 0 ? -(err ? err : SPLIT3_ERR_CUDA) : r;
+    };
+    for (int b = 0; b < nblk; b++) {
+        const int64_t r0 = blk_r0[b], mr = blk_mr[b];
+        if (cudaStreamWaitEvent(s0, h->ev_arows[b], 0) != cudaSuccess) return SPLIT3_ERR_CUDA;
+        const float* Ab = dA + r0 * K;
+        float* bmax = reinterpret_cast<float*>(maxblk + b);
+        if (nblk > 1) {
+            if ((n = split3::launch_maxmin(s0, mr * K, Ab, maxblk + b, minblk + b, h->num_sms)) < 0) return SPLIT3_ERR_CUDA;
+        } else if ((n = split3::launch_maxabs(s0, mr, K, Ab, K, bmax, nullptr, h->num_sms)) < 0) {
+            return SPLIT3_ERR_CUDA;
+        }
+        launches += n;
+        if ((n = split3::launch_split(s0, mr, K, Ab, K, bmax, w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa, w.ldpa, sblk + b,
+                                      h->num_sms)) < 0)
+            return SPLIT3_ERR_CUDA;
+        launches += n;
+        if ((n = gemm_block(r0, mr, sblk + b)) < 0) return -n;
         launches += n;
         if (cudaEventRecord(h->ev_rows[b], s0) != cudaSuccess || cudaStreamWaitEvent(h->s_out, h->ev_rows[b], 0) != cudaSuccess ||
             cudaMemcpyAsync(C_host + r0 * N, dC + r0 * N, (size_t)mr * N * 4, cudaMemcpyDeviceToHost, h->s_out) != cudaSuccess)
             return SPLIT3_ERR_CUDA;
+    }
+    if (nblk > 1) {
+        int32_t flags_h[12] = {0};
+        if ((n = split3::launch_host_scale_check(s0, maxblk, minblk, sblk, nblk, w.maxA, w.sA, flags_d)) < 0 ||
+            cudaMemcpyAsync(flags_h, flags_d, (size_t)nblk * 4, cudaMemcpyDeviceToHost, s0) != cudaSuccess ||
+            cudaStreamSynchronize(s0) != cudaSuccess || cudaStreamSynchronize(h->s_out) != cudaSuccess)
+            return SPLIT3_ERR_CUDA;
+        launches += n;
+        for (int b = 0; b < nblk; b++) {   // rare: redo with the per-matrix scale
+            if (!flags_h[b]) continue;
+            const int64_t r0 = blk_r0[b], mr = blk_mr[b];
+            if ((n = split3::launch_split(s0, mr, K, dA + r0 * K, K, w.maxA, w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa,
+                                          w.ldpa, w.sA, h->num_sms)) < 0)
+                return SPLIT3_ERR_CUDA;
+            launches += n;
+            if ((n = gemm_block(r0, mr, w.sA)) < 0) return -n;
+            launches += n;
+            if (cudaMemcpyAsync(C_host + r0 * N, dC + r0 * N, (size_t)mr * N * 4, cudaMemcpyDeviceToHost, s0) != cudaSuccess)
+                return SPLIT3_ERR_CUDA;
+            h->host_redo++;
+        }
     }
     if (cudaStreamSynchronize(h->s_out) != cudaSuccess || cudaStreamSynchronize(s0) != cudaSuccess)
         return SPLIT3_ERR_CUDA;

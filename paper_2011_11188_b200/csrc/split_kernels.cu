@@ -188,6 +188,76 @@ __global__ void __launch_bounds__(256) maxabs_2d_kernel(const float* __restrict_
 
 // scale_exp_dev, pow2_neg, split1: split_math.h (shared with the fused-B GEMM converter)
 
+// Host-buffer pipeline (split3_sgemm_host): max |x| and min nonzero |x| over the
+// finite entries of a contiguous chunk, as uint bits (non-negative floats order like uints);
+// *d_max must start at 0, *d_min at 0xFFFFFFFF (= no nonzero entry).
+template <bool VEC>
+__global__ void __launch_bounds__(256) maxmin_1d_kernel(const float* __restrict__ X, int64_t n, unsigned* d_max,
+                                                        unsigned* d_min) {
+    pdl_enter();
+    unsigned mx = 0, mn = 0xFFFFFFFFu;
+    auto fold = [&](float x) {
+        const unsigned u = __float_as_uint(x) & 0x7FFFFFFFu;
+        if (u < kFiniteLimit) {
+            mx = max(mx, u);
+            if (u) mn = min(mn, u);
+        }
+    };
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    int64_t done = 0;
+    if (VEC) {
+        const int64_t n4 = n / 4;
+        const float4* X4 = reinterpret_cast<const float4*>(X);
+        for (int64_t i = tid; i < n4; i += nthr) {
+            const float4 v = __ldcs(X4 + i);
+            fold(v.x); fold(v.y); fold(v.z); fold(v.w);
+        }
+        done = n4 * 4;
+    }
+    for (int64_t i = done + tid; i < n; i += nthr) fold(__ldcs(X + i));
+    __shared__ unsigned sx[32], sn[32];
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { sx[w] = mx; sn[w] = mn; }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        mx = l < nw ? sx[l] : 0u;
+        mn = l < nw ? sn[l] : 0xFFFFFFFFu;
+        for (int o = 16; o > 0; o >>= 1) {
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        }
+        if (l == 0) {
+            if (mx) atomicMax(d_max, mx);
+            if (mn != 0xFFFFFFFFu) atomicMin(d_min, mn);
+        }
+    }
+}
+
+// After all row blocks: the per-matrix max (reading R1) and scale exponent sA from the block maxima;
+// flags[b] = 1 iff block b was split with an exponent below sA AND holds a nonzero |x| < 2^(sA-12):
+// only such an entry can round differently (fp16-subnormal A1 or A2), every other
+// entry's planes, products and C are the global-scale ones times an exact power of two.
+__global__ void host_scale_check_kernel(const unsigned* maxblk, const unsigned* minblk, const int32_t* sblk, int nblk,
+                                        float* d_max, int32_t* d_sexp, int32_t* flags) {
+    pdl_enter();
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    unsigned g = 0;
+    for (int b = 0; b < nblk; b++) g = max(g, maxblk[b]);
+    const int s = scale_exp_dev(__uint_as_float(g));
+    *d_max = __uint_as_float(g);
+    *d_sexp = s;
+    const int e = s - 12;                                   // in [-139, 101]
+    const unsigned thr = e >= -126 ? (unsigned)(e + 127) << 23 : 1u << (e + 149);   // bits of 2^e
+    for (int b = 0; b < nblk; b++) flags[b] = (sblk[b] != s && minblk[b] < thr) ? 1 : 0;
+}
+
+
 // Non-transposed split: planes rows x cols (ldp).  VEC: cols % 4 == 0, ld % 4 == 0, aligned.
 template <bool VEC>
 __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ X, int64_t rows,
@@ -551,6 +621,22 @@ int launch_maxabs(cudaStream_t st, int64_t rows, int64_t cols, const float* X, i
         dim3 grid((unsigned)bx, (unsigned)grid_rows(rows, num_sms, bx));
         launch_k(maxabs_2d_kernel, grid, dim3(256), 0, st, X, rows, cols, ld, d_max, d_bad);
     }
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_maxmin(cudaStream_t st, int64_t n, const float* X, unsigned* d_max, unsigned* d_min, int num_sms) {
+    if (n <= 0) return 0;
+    int64_t blocks = (n / 4 + 255) / 256;
+    const int64_t cap = (int64_t)num_sms * 8;
+    const int g = (int)(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+    if (aligned16(X)) launch_k(maxmin_1d_kernel<true>, dim3(g), dim3(256), 0, st, X, n, d_max, d_min);
+    else launch_k(maxmin_1d_kernel<false>, dim3(g), dim3(256), 0, st, X, n, d_max, d_min);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_host_scale_check(cudaStream_t st, const unsigned* maxblk, const unsigned* minblk, const int32_t* sblk,
+                            int nblk, float* d_max, int32_t* d_sexp, int32_t* flags) {
+    launch_k(host_scale_check_kernel, dim3(1), dim3(32), 0, st, maxblk, minblk, sblk, nblk, d_max, d_sexp, flags);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -37,7 +37,7 @@ BF16X3 = 1 << 3
 EXPORTS = (
     "split3_sgemm_create", "split3_set_stream", "split3_sgemm_destroy",
     "split3_sgemm_workspace_size", "split3_sgemm_set_workspace", "split3_sgemm",
-    "split3_sgemm_host_workspace_size", "split3_sgemm_host", "split3_last_bad_index",
+    "split3_sgemm_host_workspace_size", "split3_sgemm_host", "split3_last_bad_index", "split3_host_redo_count",
     "split3_status_string", "split3_maxabs", "split3_split", "split3_gemm_planes",
     "split3_last_launch_count", "split3_timing_enable", "split3_timing_read",
     "split3_set_promotion", "split3_set_wave_sync", "split3_set_schedule", "split3_set_fused_split",
@@ -109,6 +109,8 @@ def load() -> ctypes.CDLL:
         lib.split3_sgemm_host.argtypes = [_p, _i64, _i64, _i64, _p, _p, _p, ctypes.c_uint32]
         lib.split3_last_bad_index.restype = _i64
         lib.split3_last_bad_index.argtypes = [_p]
+        lib.split3_host_redo_count.restype = _i64
+        lib.split3_host_redo_count.argtypes = [_p]
         lib.split3_last_launch_count.argtypes = [_p]
         lib.split3_timing_enable.argtypes = [_p, ctypes.c_int]
         lib.split3_set_promotion.argtypes = [_p, ctypes.c_int]
@@ -236,6 +238,10 @@ class Handle:
         if st != OK:
             raise Split3Error(st, "split3_timing_read")
         return s.value, g.value, n.value
+
+    def host_redo_count(self) -> int:
+        """row blocks the host pipeline redid with the per-matrix scale"""
+        return int(self._lib.split3_host_redo_count(self._h))
 
     def last_launch_count(self) -> int:
         return int(self._lib.split3_last_launch_count(self._h))
