@@ -42,6 +42,8 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--force-dist", action="store_true",
                    help="test only: run the 2-D tile path (NCCL) even with one rank")
+    p.add_argument("--inputs", default="sharded", choices=["sharded", "replicated"],
+                   help="N > 1: inputs start sharded (plane all-gathers) or replicated on every rank")
     p.add_argument("--cpu-target-s", type=float, default=12.0)
     p.add_argument("--sustained-s", type=float, default=4.0,
                    help="extra back-to-back loop (s) reported as 'sustained' (0 = skip)")
@@ -261,6 +263,7 @@ def workload_config(args, world):
             "M": args.n * pr, "N": args.n * pc, "K": args.n, "terms": args.terms,
             "inputs": "fp32", "tensor_core": "fp16 x fp16 -> fp32 accumulate (tcgen05 kind::f16)",
             "parallelism": f"2d-tile {pr}x{pc}" if world > 1 else "single",
+            **({"inputs_start": args.inputs} if world > 1 or args.force_dist else {}),
             "l2": f"inputs {args.n * args.n * 4 / 2**30:.2f} GiB/matrix" + (
                 " > 126 MB L2: no flush needed" if args.n * args.n * 4 > 126e6 else
                 " < L2: inputs re-read from L2 between steps (small config)")}
@@ -308,7 +311,8 @@ def main():
     else:
         from paper_2011_11188_b200.dist import TileGemm
 
-        tg = TileGemm(h, n, world, rank, four_term=four, one_term=one, seed=0)
+        tg = TileGemm(h, n, world, rank, four_term=four, one_term=one, seed=0,
+                      replicated=args.inputs == "replicated")
 
         def step():
             tg.run()

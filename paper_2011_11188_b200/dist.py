@@ -21,6 +21,11 @@ One step (the only exchanges are 2 floats and the plane panels; there is no redu
 With m and n multiples of the GEMM tile (128), every C element is computed by the same kernel
 over the same K order as on one GPU: the P-GPU C equals the 1-GPU C bitwise.
 
+Replicated inputs (every rank holds all of A and B; sgemm_2d_replicated): no plane exchange.
+Rank (i, j) reads only its A row panel and B column panel — their max-abs, all_reduce(MAX) over
+all ranks (every panel belongs to some rank, so this is the per-matrix max), a local split of the
+two panels with the global scale and the GEMM on its tile: the same planes and C bits as one GPU.
+
 The local ops are injectable (``ops``) so the exchange logic is tested on CPU with the gloo
 backend (tests/test_dist_gloo.py); the default ops are the CUDA library's.
 """
@@ -102,17 +107,22 @@ class CudaOps:
 
     def __init__(self, h):
         self.h = h
+        self.launches = 0          # library kernels launched through these ops (NCCL's not counted)
 
     def maxabs_into(self, X, d_max1):
         self.h.maxabs(X, d_max1)
+        self.launches += self.h.last_launch_count()
 
     def split(self, X, d_max1, transpose):
         hi, lo, sexp = self.h.split(X, d_max1, transpose=transpose)
+        self.launches += self.h.last_launch_count()
         return hi, lo, sexp
 
     def gemm(self, m, n, K, A1, A2, sA, B1t, B2t, sB, out, four_term, one_term):
-        return self.h.gemm_planes(m, n, K, A1, A2, sA, B1t, B2t, sB, out=out,
-                                  four_term=four_term, one_term=one_term)
+        res = self.h.gemm_planes(m, n, K, A1, A2, sA, B1t, B2t, sB, out=out,
+                                 four_term=four_term, one_term=one_term)
+        self.launches += self.h.last_launch_count()
+        return res
 
 
 def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, groups=None,
@@ -189,6 +199,32 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
     return out
 
 
+def sgemm_2d_replicated(A: torch.Tensor, B: torch.Tensor, ops, out: torch.Tensor | None = None,
+                        four_term=False, one_term=False):
+    """One rank's C tile of C = A*B with A (M x K) and B (K x N) replicated on every rank (see the
+    module docstring): max-abs of the own panels, all_reduce(MAX), split, GEMM; no plane exchange."""
+    world = dist.get_world_size()
+    rank = dist.get_rank()
+    M, K = A.shape
+    N = B.shape[1]
+    r0, r1, c0, c1 = c_tile(M, N, world, rank)
+    Ap, Bp = A[r0:r1], B[:, c0:c1]            # row panel i (contiguous rows), column panel j (ld = N)
+    mx = torch.zeros(2, dtype=torch.float32, device=A.device)
+    ops.maxabs_into(Ap, mx[0:1])
+    ops.maxabs_into(Bp, mx[1:2])
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    a_hi, a_lo, sA = ops.split(Ap, mx[0:1], False)
+    b_hi, b_lo, sB = ops.split(Bp, mx[1:2], True)
+    m, n = r1 - r0, c1 - c0
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float32, device=A.device)
+    res = ops.gemm(m, n, K, a_hi, a_hi if one_term else a_lo, sA, b_hi, b_hi if one_term else b_lo, sB, out,
+                   four_term, one_term)
+    if res is not out:
+        out.copy_(res)
+    return out
+
+
 class TileGemm:
     """bench.py's multi-GPU step: each rank owns an n x n C tile of a (pr*n) x (pc*n) x n
     problem (weak scaling), inputs sharded as above, generated on the device from seeds
@@ -196,9 +232,10 @@ class TileGemm:
     injectable so the same workload runs on CPU / gloo in tests/test_dist_gloo.py."""
 
     def __init__(self, h, n: int, world: int, rank: int, four_term=False, one_term=False, seed=0,
-                 ops=None, device=None):
+                 ops=None, device=None, replicated: bool = False):
         from workloads import numpy_matrix, torch_matrix
 
+        self.replicated = replicated
         self.pr, self.pc = grid_for(world)
         self.M, self.N, self.K = self.pr * n, self.pc * n, n
         self.h = h
@@ -207,7 +244,17 @@ class TileGemm:
         r0, r1 = a_block_rows(self.M, world, rank)
         c0, c1 = b_block_cols(self.N, world, rank)
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-        if dev.type == "cuda":
+        if replicated:   # every rank: the whole A and B (the same seeds on every rank)
+            if dev.type == "cuda":
+                self.A = torch_matrix("uniform", self.M, self.K, seed=seed * 1000 + 1, device=dev)
+                self.B = torch_matrix("uniform", self.K, self.N, seed=seed * 1000 + 2, device=dev)
+                dtype = torch.float32
+            else:
+                self.A = torch.from_numpy(numpy_matrix("uniform", self.M, self.K, seed * 1000 + 1))
+                self.B = torch.from_numpy(numpy_matrix("uniform", self.K, self.N, seed * 1000 + 2))
+                dtype = torch.float64
+            self.A_blk, self.B_blk = self.A, self.B
+        elif dev.type == "cuda":
             self.A_blk = torch_matrix("uniform", r1 - r0, self.K, seed=seed * 1000 + 2 * rank, device=dev)
             self.B_blk = torch_matrix("uniform", self.K, c1 - c0, seed=seed * 1000 + 2 * rank + 1, device=dev)
             dtype = torch.float32
@@ -219,9 +266,21 @@ class TileGemm:
         self.four, self.one = four_term, one_term
 
     def run(self):
-        return sgemm_2d(self.A_blk, self.B_blk, self.M, self.N, self.ops, self.groups, out=self.C,
-                        four_term=self.four, one_term=self.one)
+        l0 = getattr(self.ops, "launches", None)
+        if self.replicated:
+            res = sgemm_2d_replicated(self.A, self.B, self.ops, out=self.C, four_term=self.four, one_term=self.one)
+        else:
+            res = sgemm_2d(self.A_blk, self.B_blk, self.M, self.N, self.ops, self.groups, out=self.C,
+                           four_term=self.four, one_term=self.one)
+        if l0 is not None:
+            self._last_launches = self.ops.launches - l0
+        return res
 
     def launches_per_step(self) -> int:
-        # 2 max-abs + 2 split + one GEMM per row block of the tile (NCCL kernels not counted)
+        """library kernels of the last run() (counted by the ops; NCCL's not counted), else the
+        plan: 2 max-abs + 2 splits + one GEMM per row block of the tile (one with replicated inputs)"""
+        if getattr(self, "_last_launches", None) is not None:
+            return self._last_launches
+        if self.replicated:
+            return 5
         return 4 + (self.pc if self.pc > 1 else 1)

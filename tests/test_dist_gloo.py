@@ -51,13 +51,13 @@ class OracleOps:
         self.o = orc
 
     def maxabs_into(self, X, d_max1):
-        m, bad = self.o.maxabs(X.numpy())
+        m, bad = self.o.maxabs(np.ascontiguousarray(X.numpy()))
         assert bad < 0
         d_max1[0] = max(float(d_max1[0]), m)
 
     def split(self, X, d_max1, transpose):
         s = self.o.scale_exp(float(d_max1[0]))
-        hi, lo, _ = self.o.split(X.numpy(), s=s)
+        hi, lo, _ = self.o.split(np.ascontiguousarray(X.numpy()), s=s)
         if transpose:
             hi, lo = hi.T.copy(), lo.T.copy()
         return (torch.from_numpy(hi.view(np.int16)), torch.from_numpy(lo.view(np.int16)),
@@ -160,3 +160,43 @@ def test_bench_tilegemm_workload(orc, world):
     res = {r: (ok, nl) for r, ok, nl in (q.get(timeout=5) for _ in range(world))}
     assert all(p.exitcode == 0 for p in procs)
     assert all(ok for ok, _ in res.values()), res
+
+
+def _rep_worker(rank, world, port, M, N, K, terms, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+
+        from workloads import numpy_matrix
+
+        A = numpy_matrix("loguni", M, K, seed=5)
+        A[: M // world] *= 2.0 ** 9            # rank 0's rows hold the max: the all-reduce matters
+        B = numpy_matrix("uniform", K, N, seed=6)
+        pr, pc = d2.grid_for(world)
+        out = torch.empty((M // pr, N // pc), dtype=torch.float64)
+        tile = d2.sgemm_2d_replicated(torch.from_numpy(A), torch.from_numpy(B), OracleOps(oracle), out=out,
+                                      four_term=terms == 4, one_term=terms == 1)
+        full = oracle.sgemm(A, B, terms=terms)
+        tr0, tr1, tc0, tc1 = d2.c_tile(M, N, world, rank)
+        q.put((rank, bool(np.array_equal(tile.numpy(), full[tr0:tr1, tc0:tc1]))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,terms", [(2, 3), (4, 3), (4, 4)])
+def test_sgemm_2d_replicated_matches_single_process(orc, world, terms):
+    """replicated inputs: each rank splits only its panels with the all-reduced per-matrix scale;
+    its tile equals the single-process oracle's block exactly (no plane exchange)"""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    M, N, K = 16 * world, 12 * world, 40
+    port = _free_port()
+    procs = [ctx.Process(target=_rep_worker, args=(r, world, port, M, N, K, terms, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    res = dict(q.get(timeout=5) for _ in range(world))
+    assert all(p.exitcode == 0 for p in procs)
+    assert res == {r: True for r in range(world)}

@@ -39,5 +39,21 @@ def test_tile_gemm_one_rank_matches_single_call(nccl_one_rank, n, kw):
     C64 = tg.A_blk.double() @ tg.B_blk.double()
     e64 = float((C.double() - C64).norm() / C64.norm())
     assert e64 < 2e-6, e64
-    assert tg.launches_per_step() == 5
+    assert tg.launches_per_step() >= 5       # counted: + the split-K tail reduction when planned
     assert np.isfinite(C.cpu().numpy()).all()
+
+
+@pytest.mark.parametrize("n", [1024, 2048])
+def test_tile_gemm_replicated_one_rank(nccl_one_rank, n):
+    """replicated inputs (no plane exchange): same planes and scales as the single-GPU call"""
+    import paper_2011_11188_b200 as s3
+    from paper_2011_11188_b200.dist import TileGemm
+
+    h = s3.Handle(0)
+    tg = TileGemm(h, n, 1, 0, seed=6, replicated=True)
+    C = tg.run()
+    torch.cuda.synchronize()
+    ref = h.sgemm_ex(tg.A, tg.B)
+    assert torch.equal(C.view(torch.int32), ref.view(torch.int32)) or \
+        float((C.double() - ref.double()).norm() / ref.double().norm()) < 1e-6
+    assert tg.launches_per_step() >= 5
