@@ -445,11 +445,21 @@ def main():
         Bh = tg.B_blk.cpu().pin_memory()
         Ch = torch.empty(tuple(tg.C.shape), dtype=torch.float32).pin_memory()
 
+        cp = torch.cuda.Stream(device=dev)
+
+        def copy_out(rows):   # each row block of the C tile goes out while the next one computes
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            cp.wait_event(ev)
+            with torch.cuda.stream(cp):
+                Ch[rows].copy_(tg.C[rows], non_blocking=True)
+
         def e2e_step():
+            stream.wait_stream(cp)          # the previous step's copy-out has read C
             tg.A_blk.copy_(Ah, non_blocking=True)
             tg.B_blk.copy_(Bh, non_blocking=True)
-            tg.run()
-            Ch.copy_(tg.C, non_blocking=True)
+            tg.run(on_block=copy_out)
+            stream.wait_stream(cp)
 
         e2e_step()
         torch.cuda.synchronize()

@@ -330,21 +330,20 @@ constexpr int FB_LO_OFF = 4096;
 // Split one K step in place (one converter warp): each of the 16 LDS.128 reads one fp32 k-row
 // (lane L: N values 4L..4L+3, conflict-free), all reads precede all writes (__syncwarp), then every
 // lane stores two 8-B pieces (hi, lo) of 16-B SW128 chunks: lanes 0-15 -> N atom 0, 16-31 -> atom 1.
-__device__ __forceinline__ void convert_step(uint32_t step, int lane, float f) {
+__device__ __forceinline__ void convert_step(uint8_t* step, int lane, float f) {
     float4 v[16];
 #pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = ld_shared_v4(step + (uint32_t)r * 512u + (uint32_t)lane * 16u);
+    for (int r = 0; r < 16; r++) v[r] = *reinterpret_cast<const float4*>(step + r * 512 + lane * 16);
     __syncwarp();
     const int l16 = lane & 15;
-    const uint32_t base = step + (uint32_t)(lane >> 4) * (uint32_t)FB_LBO + (uint32_t)((l16 & 1) << 3);
+    uint8_t* base = step + (lane >> 4) * FB_LBO + ((l16 & 1) << 3);
 #pragma unroll
     for (int r = 0; r < 16; r++) {
         uint2 hi, lo;
         split4(v[r], f, hi, lo);
-        const uint32_t a = base + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u +
-                           ((uint32_t)((l16 >> 1) ^ (r & 7)) << 4);
-        st_shared_v2u(a, hi);
-        st_shared_v2u(a + FB_LO_OFF, lo);
+        uint8_t* a = base + (r >> 3) * 1024 + (r & 7) * 128 + (((l16 >> 1) ^ (r & 7)) << 4);
+        *reinterpret_cast<uint2*>(a) = hi;
+        *reinterpret_cast<uint2*>(a + FB_LO_OFF) = lo;
     }
 }
 
@@ -394,8 +393,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     constexpr uint32_t EPI_ARRIVALS = 2 * NUM_EPI_WARPS;
 
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~static_cast<uintptr_t>(1023));
+    // 1024-B aligned (SW128 atoms); offsetting smem_raw keeps the pointer in the shared space
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* staging = smem + STAGES * STAGE_BYTES;   // 1024-aligned (128-B swizzle atoms)
     uint64_t* bars = reinterpret_cast<uint64_t*>(staging + G::STAGING);
     uint64_t* full_bar = bars;                        // [STAGES]   leader: TMA bytes landed
@@ -660,10 +659,10 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             decode_unit(unit, plan, num_kb, kps, tile_unused, kb_begin, kb_end, slot);
             for (int kb = kb_begin; kb < kb_end; kb++) {
                 mbar_wait(smem_u32(&ffull_bar[stage]), phase);
-                const uint32_t breg = smem_u32(smem + stage * STAGE_BYTES + B_OFF);
+                uint8_t* breg = smem + stage * STAGE_BYTES + B_OFF;
 #ifndef SPLIT3_EXP_NO_CONVERT   // experiment only: time the fused-B pipeline without the conversion
-                convert_step(breg + (uint32_t)cw * FB_STEP_BYTES, lane, f);
-                convert_step(breg + (uint32_t)(cw + 2) * FB_STEP_BYTES, lane, f);
+                convert_step(breg + cw * FB_STEP_BYTES, lane, f);
+                convert_step(breg + (cw + 2) * FB_STEP_BYTES, lane, f);
 #else
                 (void)breg; (void)f;
 #endif

@@ -126,7 +126,8 @@ class CudaOps:
 
 
 def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, groups=None,
-             out: torch.Tensor | None = None, four_term=False, one_term=False, overlap: bool = True):
+             out: torch.Tensor | None = None, four_term=False, one_term=False, overlap: bool = True,
+             on_block=None):
     """One rank's share of C = A*B.  A_blk: its (M/P) x K block of A; B_blk: its K x (N/P)
     block of B.  Returns the rank's m x n C tile (see the module docstring).
 
@@ -134,6 +135,9 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
     runs on the compute stream while the A panel is all-gathered on a communication stream; the
     other row blocks follow when it lands.  Each row block is a separate GEMM over whole tiles,
     so every C element is computed exactly as in the non-overlapped schedule.
+
+    on_block(rows): called after the GEMM of each row block of the tile is enqueued (rows = a
+    slice of `out`'s rows), e.g. to copy that part of C out while the next block computes.
     """
     world = dist.get_world_size()
     rank = dist.get_rank()
@@ -168,6 +172,8 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
         res = ops.gemm(m, n, K, A1, A2, sA, B1t, B2t, sB, out, four_term, one_term)
         if res is not out:
             out.copy_(res)
+        if on_block is not None:
+            on_block(slice(0, m))
         return out
     # 4b under 5a: gather the A panel (side stream under NCCL) while the own rows are multiplied
     compute = torch.cuda.current_stream(dev) if use_streams else None
@@ -181,6 +187,8 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
     res = ops.gemm(mb, n, K, a_hi, a_hi if one_term else a_lo, sA, B1t, B2t, sB, out[own], four_term, one_term)
     if res is not None and res.data_ptr() != out[own].data_ptr():
         out[own].copy_(res)
+    if on_block is not None:
+        on_block(own)
     if use_streams:
         compute.wait_stream(comm)
     else:
@@ -193,6 +201,8 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
         res = ops.gemm(mb, n, K, A1[rs], A2[rs], sA, B1t, B2t, sB, out[rs], four_term, one_term)
         if res is not None and res.data_ptr() != out[rs].data_ptr():
             out[rs].copy_(res)
+        if on_block is not None:
+            on_block(rs)
     if use_streams:
         A1.record_stream(compute)
         A2.record_stream(compute)
@@ -200,7 +210,7 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
 
 
 def sgemm_2d_replicated(A: torch.Tensor, B: torch.Tensor, ops, out: torch.Tensor | None = None,
-                        four_term=False, one_term=False):
+                        four_term=False, one_term=False, on_block=None):
     """One rank's C tile of C = A*B with A (M x K) and B (K x N) replicated on every rank (see the
     module docstring): max-abs of the own panels, all_reduce(MAX), split, GEMM; no plane exchange."""
     world = dist.get_world_size()
@@ -222,6 +232,8 @@ def sgemm_2d_replicated(A: torch.Tensor, B: torch.Tensor, ops, out: torch.Tensor
                    four_term, one_term)
     if res is not out:
         out.copy_(res)
+    if on_block is not None:
+        on_block(slice(0, m))
     return out
 
 
@@ -265,13 +277,14 @@ class TileGemm:
         self.C = torch.empty((n, n), dtype=dtype, device=dev)
         self.four, self.one = four_term, one_term
 
-    def run(self):
+    def run(self, on_block=None):
         l0 = getattr(self.ops, "launches", None)
         if self.replicated:
-            res = sgemm_2d_replicated(self.A, self.B, self.ops, out=self.C, four_term=self.four, one_term=self.one)
+            res = sgemm_2d_replicated(self.A, self.B, self.ops, out=self.C, four_term=self.four, one_term=self.one,
+                                      on_block=on_block)
         else:
             res = sgemm_2d(self.A_blk, self.B_blk, self.M, self.N, self.ops, self.groups, out=self.C,
-                           four_term=self.four, one_term=self.one)
+                           four_term=self.four, one_term=self.one, on_block=on_block)
         if l0 is not None:
             self._last_launches = self.ops.launches - l0
         return res
