@@ -107,9 +107,9 @@ int split3_sgemm(split3_handle_t h, int64_t M, int64_t N, int64_t K,
 /* Same computation with HOST buffers (pageable or pinned): copies A and B to the workspace
  * staging area of the handle's device, runs the method, copies C back, and synchronises
  * the handle's stream before returning.  C is bit-identical to split3_sgemm on the same inputs.
- * Pipelined: B is copied first, then A in up to 8 row blocks, each split and
+ * Pipelined: B is copied first, then A in up to 20 row blocks, each split and
  * multiplied as soon as it lands while the next one copies in, and C row blocks copy out
- * underneath; env SPLIT3_HOST_BLOCKS=<1..8> at handle creation fixes the block count.  Device staging for A, B and C is taken from the
+ * underneath; env SPLIT3_HOST_BLOCKS=<1..16> at handle creation fixes the block count.  Device staging for A, B and C is taken from the
  * workspace, which must hold split3_sgemm_host_workspace_size(M, N, K, flags) bytes.
  * Host layout is packed row-major (lda = K, ldb = N, ldc = N). */
 size_t split3_sgemm_host_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags);

@@ -45,8 +45,8 @@ struct split3_ctx {
     // host-buffer entry: copy-in / copy-out streams and events, created on first use
     cudaStream_t s_in = nullptr, s_out = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_done = nullptr;
-    cudaEvent_t ev_rows[16] = {};      // C row block b computed
-    cudaEvent_t ev_arows[16] = {};     // A row block b copied in
+    cudaEvent_t ev_rows[32] = {};      // C row block b computed
+    cudaEvent_t ev_arows[32] = {};     // A row block b copied in
     int host_blocks = 0;               // row blocks of the host pipeline (0 = automatic; env SPLIT3_HOST_BLOCKS)
     long long host_redo = 0;           // row blocks redone with the per-matrix scale (split3_host_redo_count)
     // measurement hooks: event triples (start, after split, after gemm) per timed call
@@ -212,7 +212,7 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
     if (const char* e = getenv("SPLIT3_MN_MAJOR")) c->mn_major = atoi(e) != 0;
     if (const char* e = getenv("SPLIT3_PREP_MAX")) c->prep_max = atoll(e);
     if (const char* e = getenv("SPLIT3_FUSE_B")) c->fuse_b = atoi(e);
-    if (const char* e = getenv("SPLIT3_HOST_BLOCKS")) c->host_blocks = std::min(std::max(atoi(e), 0), 8);
+    if (const char* e = getenv("SPLIT3_HOST_BLOCKS")) c->host_blocks = std::min(std::max(atoi(e), 0), 16);
     if (const char* e = getenv("SPLIT3_FUSE_B_MAX_M")) c->fuse_b_max_m = atoll(e);
     *h = c;
     return SPLIT3_OK;
@@ -767,10 +767,14 @@ int split3_timing_read(split3_handle_t h, double* split_ms, double* gemm_ms, int
     return SPLIT3_OK;
 }
 
+// host pipeline: per-row-block scalars after the staging buffers
+constexpr int kMaxHostBlocks = 32;
+constexpr size_t kHostScalarBytes = 4 * 4 * kMaxHostBlocks;
+
 size_t split3_sgemm_host_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags) {
     if (M < 0 || N < 0 || K < 0) return 0;
     return split3_sgemm_workspace_size(M, N, K, flags) + align256((size_t)M * K * 4) +
-           align256((size_t)K * N * 4) + align256((size_t)M * N * 4);
+           align256((size_t)K * N * 4) + align256((size_t)M * N * 4) + kHostScalarBytes;
 }
 
 int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const float* A_host,
@@ -826,31 +830,38 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
     if (h->host_blocks > 0) {
         nblk = h->host_blocks;
     } else {
-        while (nblk < 8 && ((M / (2 * nblk)) / 256) * tiles_n >= 2 * (h->num_sms / 2)) nblk *= 2;
+        while (nblk < 16 && ((M / (2 * nblk)) / 256) * tiles_n >= h->num_sms / 2) nblk *= 2;
     }
     const int64_t rows_per = ((M + nblk - 1) / nblk + 255) / 256 * 256;
-    // blocks (r0, rows): rows_per each; with >= 4 blocks the last one is cut into 1/2 + 1/4 + 1/4
-    // (each still >= 2 waves) so the exposed tail — its split, GEMM and copy-out — is 4x shorter
-    int64_t blk_r0[16], blk_mr[16];
+    // blocks (r0, rows): rows_per each (>= 1 wave of tiles; <= 16 blocks: the copy-out of C trails
+    // the copy-in of A by about one block); with >= 4 blocks the first one is cut into 1/4 + 1/4 + 1/2
+    // (the GEMMs, and so the copy-out, start a quarter block after B has landed) and the last
+    // into 1/2 + 1/4 + 1/4 (short exposed tail: the last piece's split, GEMM and copy-out)
+    int64_t blk_r0[kMaxHostBlocks], blk_mr[kMaxHostBlocks];
+    const bool cut = h->host_blocks == 0 && M >= 4 * rows_per && rows_per % 1024 == 0;
+    const int64_t q = rows_per / 4;
     nblk = 0;
     for (int64_t r0 = 0; r0 < M; r0 += rows_per) {
-        blk_r0[nblk] = r0;
-        blk_mr[nblk++] = std::min(rows_per, M - r0);
-    }
-    if (h->host_blocks == 0 && nblk >= 4 && blk_mr[nblk - 1] == rows_per && rows_per % 1024 == 0) {
-        const int64_t r0 = blk_r0[nblk - 1], q = rows_per / 4;
-        blk_mr[nblk - 1] = 2 * q;
-        blk_r0[nblk] = r0 + 2 * q; blk_mr[nblk++] = q;
-        blk_r0[nblk] = r0 + 3 * q; blk_mr[nblk++] = q;
+        const int64_t mr = std::min(rows_per, M - r0);
+        if (cut && r0 == 0) {
+            blk_r0[nblk] = 0; blk_mr[nblk++] = q;
+            blk_r0[nblk] = q; blk_mr[nblk++] = q;
+            blk_r0[nblk] = 2 * q; blk_mr[nblk++] = 2 * q;
+        } else if (cut && r0 + rows_per == M) {
+            blk_r0[nblk] = r0; blk_mr[nblk++] = 2 * q;
+            blk_r0[nblk] = r0 + 2 * q; blk_mr[nblk++] = q;
+            blk_r0[nblk] = r0 + 3 * q; blk_mr[nblk++] = q;
+        } else {
+            blk_r0[nblk] = r0; blk_mr[nblk++] = mr;
+        }
     }
     Carve w = carve(h->ws, M, N, K);
-    // per-block scalars (<= 12 blocks) in the scalars block: max bits [48, +48), min-nonzero bits
-    // [96, +48), exponents [144, +48), redo flags [192, +48)
-    uint8_t* sc = static_cast<uint8_t*>(h->ws);
-    unsigned* maxblk = reinterpret_cast<unsigned*>(sc + 48);
-    unsigned* minblk = reinterpret_cast<unsigned*>(sc + 96);
-    int32_t* sblk = reinterpret_cast<int32_t*>(sc + 144);
-    int32_t* flags_d = reinterpret_cast<int32_t*>(sc + 192);
+    // per-block scalars after the staging buffers: max bits, min-nonzero bits, exponents, redo flags
+    uint8_t* sc = reinterpret_cast<uint8_t*>(dC) + align256((size_t)M * N * 4);
+    unsigned* maxblk = reinterpret_cast<unsigned*>(sc);
+    unsigned* minblk = reinterpret_cast<unsigned*>(sc + 4 * kMaxHostBlocks);
+    int32_t* sblk = reinterpret_cast<int32_t*>(sc + 8 * kMaxHostBlocks);
+    int32_t* flags_d = reinterpret_cast<int32_t*>(sc + 12 * kMaxHostBlocks);
     // copy-in must not overwrite the staging buffers while an earlier call on s0 still reads them
     if (cudaEventRecord(h->ev_done, s0) != cudaSuccess || cudaStreamWaitEvent(h->s_in, h->ev_done, 0) != cudaSuccess)
         return SPLIT3_ERR_CUDA;
@@ -865,8 +876,8 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
             return SPLIT3_ERR_CUDA;
     }
     int launches = 0, n;
-    if (cudaMemsetAsync(h->ws, 0, 32, s0) != cudaSuccess || cudaMemsetAsync(maxblk, 0, 48, s0) != cudaSuccess ||
-        cudaMemsetAsync(minblk, 0xFF, 48, s0) != cudaSuccess || cudaStreamWaitEvent(s0, h->ev_b, 0) != cudaSuccess)
+    if (cudaMemsetAsync(h->ws, 0, 32, s0) != cudaSuccess || cudaMemsetAsync(maxblk, 0, 4 * kMaxHostBlocks, s0) != cudaSuccess ||
+        cudaMemsetAsync(minblk, 0xFF, 4 * kMaxHostBlocks, s0) != cudaSuccess || cudaStreamWaitEvent(s0, h->ev_b, 0) != cudaSuccess)
         return SPLIT3_ERR_CUDA;
     if ((n = split3::launch_maxabs(s0, K, N, dB, N, w.maxB, nullptr, h->num_sms)) < 0) return SPLIT3_ERR_CUDA;
     launches += n;
@@ -906,7 +917,7 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
             return SPLIT3_ERR_CUDA;
     }
     if (nblk > 1) {
-        int32_t flags_h[12] = {0};
+        int32_t flags_h[kMaxHostBlocks] = {0};
         if ((n = split3::launch_host_scale_check(s0, maxblk, minblk, sblk, nblk, w.maxA, w.sA, flags_d)) < 0 ||
             cudaMemcpyAsync(flags_h, flags_d, (size_t)nblk * 4, cudaMemcpyDeviceToHost, s0) != cudaSuccess ||
             cudaStreamSynchronize(s0) != cudaSuccess || cudaStreamSynchronize(h->s_out) != cudaSuccess)
