@@ -143,3 +143,20 @@ def test_fused_mode_validation(hf):
         hf.set_fused_split(3)
     with pytest.raises(s3.Split3Error):
         hf.set_fused_split(1, -1)
+
+
+def test_fused_nonfinite_b(hf, hs):
+    """Inf / NaN in B: skipped by the max, propagated by the converters exactly as by the split
+    kernel (bitwise, NaN payloads included); SPLIT3_CHECK_FINITE reports the first bad index"""
+    M, N, K = 256, 2048, 1024
+    A = torch_matrix("uniform", M, K, seed=52)
+    B = torch_matrix("uniform", K, N, seed=53)
+    B[10, 7] = float("inf")
+    B[500, 1000] = float("nan")
+    Cf = hf.sgemm(A, B).clone()
+    Cs = hs.sgemm(A, B)
+    assert torch.equal(_bits(Cf), _bits(Cs))
+    assert not torch.isfinite(Cf[:, 7]).any() and torch.isnan(Cf[:, 1000]).all()
+    with pytest.raises(s3.NotFiniteError) as ei:
+        hf.sgemm(A, B, check_finite=True)
+    assert ei.value.index == M * K + 10 * N + 7
