@@ -42,6 +42,8 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--force-dist", action="store_true",
                    help="test only: run the 2-D tile path (NCCL) even with one rank")
+    p.add_argument("--global-n", type=int, default=0,
+                   help="strong scaling: one global_n^3 product cut into 2-D tiles (config D5, e.g. 65536)")
     p.add_argument("--inputs", default="sharded", choices=["sharded", "replicated"],
                    help="N > 1: inputs start sharded (plane all-gathers) or replicated on every rank")
     p.add_argument("--cpu-target-s", type=float, default=12.0)
@@ -258,6 +260,13 @@ def run_reference(args, rank, world):
 def workload_config(args, world):
     name = {3: "3-term", 4: "4-term", 1: "1-term control"}[args.terms]
     pr, pc = grid_shape(world)
+    g = getattr(args, "global_n", 0)
+    if g:   # strong scaling (config D5)
+        return {"workload": f"square N={g} FP32 uniform[-1,1], {name} split-FP16 GEMM, 2-D tiles {pr}x{pc}",
+                "M": g, "N": g, "K": g, "terms": args.terms, "inputs": "fp32",
+                "tensor_core": "fp16 x fp16 -> fp32 accumulate (tcgen05 kind::f16)",
+                "parallelism": f"2d-tile {pr}x{pc}", "inputs_start": args.inputs,
+                "l2": f"inputs {g * g * 4 / 2**30:.2f} GiB/matrix > 126 MB L2: no flush needed"}
     return {"workload": f"square N={args.n} FP32 uniform[-1,1], {name} split-FP16 GEMM"
                         + (f", 2-D tiles {pr}x{pc}" if world > 1 else ""),
             "M": args.n * pr, "N": args.n * pc, "K": args.n, "terms": args.terms,
@@ -284,7 +293,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    use_dist = world > 1 or args.force_dist
+    use_dist = world > 1 or args.force_dist or args.global_n > 0
 
     import torch
 
@@ -296,7 +305,10 @@ def main():
     if use_dist:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if "RANK" in os.environ:
+            dist.init_process_group("nccl", device_id=dev)
+        else:   # one process without a launcher (--force-dist / --global-n on one GPU)
+            dist.init_process_group("nccl", store=dist.HashStore(), world_size=1, rank=0, device_id=dev)
     n = args.n
     h = s3.Handle(local)
     four, one = args.terms == 4, args.terms == 1
@@ -312,7 +324,7 @@ def main():
         from paper_2011_11188_b200.dist import TileGemm
 
         tg = TileGemm(h, n, world, rank, four_term=four, one_term=one, seed=0,
-                      replicated=args.inputs == "replicated")
+                      replicated=args.inputs == "replicated", global_n=args.global_n or None)
 
         def step():
             tg.run()
@@ -354,7 +366,10 @@ def main():
         t = torch.tensor([t_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t_ms = float(t.item())
-    M_loc = N_loc = K = n
+    if use_dist:
+        M_loc, N_loc, K = tg.M // tg.pr, tg.N // tg.pc, tg.K
+    else:
+        M_loc = N_loc = K = n
     flops_step = 2.0 * M_loc * N_loc * K * world
     value = flops_step * args.steps / (t_ms / 1e3) / 1e12
     pk = peaks()
@@ -473,7 +488,7 @@ def main():
         t = torch.tensor([x0.elapsed_time(x1) / args.e2e_steps], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         te = float(t.item())
-        e2e = {"value": 2.0 * n ** 3 * world / (te / 1e3) / 1e12, "unit": "TFLOPS",
+        e2e = {"value": flops_step / (te / 1e3) / 1e12, "unit": "TFLOPS",
                "h2d_bytes_per_step": int(Ah.numel() + Bh.numel()) * 4 * world,
                "d2h_bytes_per_step": int(Ch.numel()) * 4 * world, "ms_per_step": te,
                "api": "paper_2011_11188_b200.dist.sgemm_2d (pinned host blocks, max over ranks)"}
@@ -483,7 +498,7 @@ def main():
             "metric": "split-FP16 SGEMM effective TFLOPS (2MNK/t)",
             "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+            "scaling": "strong" if args.global_n else "weak", "vs_baseline": None, "dtype": "f16",
             "data": "synthetic", "config": workload_config(args, world),
             "frac_of_peak_over_3": value / world / (pk["tc_burst"] / n_prod),
             "gpu_launches": launches_per_step * args.steps,

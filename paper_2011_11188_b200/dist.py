@@ -239,17 +239,22 @@ def sgemm_2d_replicated(A: torch.Tensor, B: torch.Tensor, ops, out: torch.Tensor
 
 class TileGemm:
     """bench.py's multi-GPU step: each rank owns an n x n C tile of a (pr*n) x (pc*n) x n
-    problem (weak scaling), inputs sharded as above, generated on the device from seeds
+    problem (weak scaling; or a tile of a global_n^3 problem: strong scaling), inputs sharded as above, generated on the device from seeds
     (A block of rank r: seed*1000 + 2r, B block: seed*1000 + 2r + 1).  `ops`/`device` are
     injectable so the same workload runs on CPU / gloo in tests/test_dist_gloo.py."""
 
     def __init__(self, h, n: int, world: int, rank: int, four_term=False, one_term=False, seed=0,
-                 ops=None, device=None, replicated: bool = False):
+                 ops=None, device=None, replicated: bool = False, global_n: int | None = None):
         from workloads import numpy_matrix, torch_matrix
 
         self.replicated = replicated
         self.pr, self.pc = grid_for(world)
-        self.M, self.N, self.K = self.pr * n, self.pc * n, n
+        # weak scaling: an n x n tile per rank of a (pr*n) x (pc*n) x n product; strong scaling
+        # (global_n): the global_n^3 product cut into pr x pc tiles (SURVEY §8d config D5)
+        if global_n:
+            self.M = self.N = self.K = global_n
+        else:
+            self.M, self.N, self.K = self.pr * n, self.pc * n, n
         self.h = h
         self.ops = ops if ops is not None else CudaOps(h)
         self.groups = make_groups(world)
@@ -274,7 +279,7 @@ class TileGemm:
             self.A_blk = torch.from_numpy(numpy_matrix("uniform", r1 - r0, self.K, seed * 1000 + 2 * rank))
             self.B_blk = torch.from_numpy(numpy_matrix("uniform", self.K, c1 - c0, seed * 1000 + 2 * rank + 1))
             dtype = torch.float64          # the oracle's tiles
-        self.C = torch.empty((n, n), dtype=dtype, device=dev)
+        self.C = torch.empty((self.M // self.pr, self.N // self.pc), dtype=dtype, device=dev)
         self.four, self.one = four_term, one_term
 
     def run(self, on_block=None):
