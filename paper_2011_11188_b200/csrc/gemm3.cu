@@ -128,6 +128,38 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             : "memory");
     } while (!done);
 }
+// Epilogue-side wait (the epilogue warps idle most of a k-block period between promotions):
+// experiment builds try a suspend-time hint (SPLIT3_EXP_EPI_HINT_NS) or a back-off sleep
+// (SPLIT3_EXP_EPI_SLEEP_NS) instead of re-polling, to cut the issue slots (power) of spinning.
+__device__ __forceinline__ void mbar_wait_epi(uint32_t bar, uint32_t parity) {
+#if defined(SPLIT3_EXP_EPI_HINT_NS)
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity), "n"(SPLIT3_EXP_EPI_HINT_NS)
+            : "memory");
+    } while (!done);
+#elif defined(SPLIT3_EXP_EPI_SLEEP_NS)
+    uint32_t done;
+    for (;;) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (done) break;
+        __nanosleep(SPLIT3_EXP_EPI_SLEEP_NS);
+    }
+#else
+    mbar_wait(bar, parity);
+#endif
+}
 // 2-SM TMA: data lands in this CTA's smem, the transaction bytes on the leader's barrier.
 __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar,
                                                  int32_t x, int32_t y, uint64_t policy) {
@@ -698,7 +730,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                 const uint32_t hphase = HB == 2 ? ((cc >> 1) & 1) : (cc & 1);
                 {
                     TRACE_T0();
-                    mbar_wait(smem_u32(&hfull_bar[hb]), hphase);
+                    mbar_wait_epi(smem_u32(&hfull_bar[hb]), hphase);
                     if (warp == 2 && lane == 0) TRACE_ADD(3);
                 }
                 tc_fence_after();
@@ -715,7 +747,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             const long long _tend = clock64();
 #endif
             if (HAS_MID) {
-                mbar_wait(smem_u32(&mfull_bar[0]), tc & 1);
+                mbar_wait_epi(smem_u32(&mfull_bar[0]), tc & 1);
                 tc_fence_after();
 #pragma unroll
                 for (int c = 0; c < NCOL / 16; c++) {
