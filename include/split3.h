@@ -263,10 +263,10 @@ int split3_set_wave_sync(split3_handle_t h, int enable);
 int split3_set_schedule(split3_handle_t h, int group_m, int l2_policy_a, int l2_policy_b);
 
 /* Fused split of B (Eq. A_1, applied inside the GEMM): for a
- * 3-term call whose B is a row-major K x N fp32 matrix (not pre-split, transB = 0), 16-byte
- * aligned with ld % 4 == 0, the GEMM TMA-loads B's fp32 tiles into shared memory and converter
- * warps split them there in place, so B's planes never go through HBM (only the max-abs pass
- * reads B beforehand).  The planes, and therefore C, are bit-identical to the separate split.
+ * 3-term call whose B is an fp32 matrix (not pre-split; row-major K x N, or stored N x K with
+ * transB = 1), 16-byte aligned with ld % 4 == 0, the GEMM TMA-loads B's fp32 tiles into shared
+ * memory and converter warps split them there in place, so B's planes never go through HBM (only
+ * the max-abs pass reads B beforehand).  The planes, and therefore C, are bit-identical to the separate split.
  * mode 0: off; 1 (default): when M <= max_m (default 2048: each B tile is converted once per
  * 256-row tile row, and the extra shared-memory traffic slows the GEMM ~11 %, which the saved
  * 8 B/element of B's split outweighs for small M) and the call is not a one-launch small call;

@@ -465,9 +465,10 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     // scalars: maxA = maxB = 0.0f, sA = sB = 0, badA = badB = INT64_MAX.  The common path (both
     // operands fp32, no check) needs no reset: the two-matrix max-abs writes maxA/maxB itself.
     const bool fast_max = needA && needB && !check;
-    // fused B (NEXT #2): 3-term, row-major fp32 B that TMA can read (16-B aligned, ld % 4 == 0)
+    // fused B (NEXT #2): 3-term, fp32 B (row-major K x N, or stored N x K for transB) that TMA
+    // can read (16-B aligned, ld % 4 == 0)
     const bool small_call = fast_max && h->mn_major && h->prep_ok && h->prep_max >= M * K + K * N;
-    const bool fuse_b = needB && !B->trans && terms == 3 && aligned(B->data, 16) && (B->ld % 4) == 0 &&
+    const bool fuse_b = needB && terms == 3 && aligned(B->data, 16) && (B->ld % 4) == 0 &&
                         (h->fuse_b == 2 || (h->fuse_b == 1 && M <= h->fuse_b_max_m && !small_call));
     // (both operands pre-split: no max-abs at all, nothing to reset)
     if (!fast_max && (needA || needB) && cudaMemsetAsync(h->ws, 0, 32, h->stream) != cudaSuccess)

@@ -259,11 +259,11 @@ __device__ __forceinline__ void tmem_ld_wait() {
 }
 
 // Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart.
-__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t sbo = 1024) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);   // start address      [0,14)
     d |= (uint64_t)1 << 16;                       // LBO (unused, SW128 K-major) [16,30)
-    d |= (uint64_t)(1024 >> 4) << 32;             // SBO = 1024 B       [32,46)
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;  // SBO (1024 B: dense 8-row groups) [32,46)
     d |= (uint64_t)1 << 46;                       // descriptor version [46,48) = 1 (sm_100)
     d |= (uint64_t)2 << 61;                       // layout: SWIZZLE_128B
     return d;
@@ -358,6 +358,11 @@ __device__ __forceinline__ void promote_all(uint32_t taddr, float (&master)[NCOL
 constexpr int FB_STEP_BYTES = 8192;
 constexpr int FB_LBO = 2048;
 constexpr int FB_LO_OFF = 4096;
+// K-major (B given as B^T, stored N x K): the tile is 128 n-rows x 64 K (256-B rows); each 8-row
+// group (2 KB) is split in place into its hi atom (+0, 8 rows x 128 B, SW128) and lo atom (+1 KB),
+// so the MMA reads B1 with SBO 2 KB and B2 at +1 KB; a K = 16 step is +32 B as usual.
+constexpr int FBK_GROUP_BYTES = 2048;
+constexpr int FBK_LO_OFF = 1024;
 
 // Split one K step in place (one converter warp): each of the 16 LDS.128 reads one fp32 k-row
 // (lane L: N values 4L..4L+3, conflict-free), all reads precede all writes (__syncwarp), then every
@@ -379,10 +384,37 @@ __device__ __forceinline__ void convert_step(uint8_t* step, int lane, float f) {
     }
 }
 
-// LAY bit 2 (FB, fused B; 3-term, row-major K x N fp32 B only): mapB1 is a map
-// over the fp32 B, TMA-loaded per k-block into the stage's B region; converter warps 10..11 apply
-// Eq. A_1 in place (split4, the split kernels' arithmetic) and write the B1/B2 planes in the
-// layout above.  The scale exponent comes from *fb_maxB; CTA 0 stores it to *fb_sB (read by the
+// Split NG 8-row groups (at grp + j * stride) of a K-major fp32 tile in place (one converter
+// warp): per group 4 LDS.128 (lane L: row 2i + L/16, K values 4(L%16)..+3, conflict-free); all
+// groups' reads precede the writes (__syncwarp; each group's region is this warp's alone); each
+// lane then stores 8-B hi / lo pieces of its rows' 16-B SW128 chunks (lanes 0-15 and 16-31 each
+// fill one 128-B row per store).  NG groups keep 4 * NG independent rows in flight.
+template <int NG>
+__device__ __forceinline__ void convert_kgroups(uint8_t* grp, int stride, int lane, float f) {
+    float4 v[NG][4];
+#pragma unroll
+    for (int j = 0; j < NG; j++)
+#pragma unroll
+        for (int i = 0; i < 4; i++) v[j][i] = *reinterpret_cast<const float4*>(grp + j * stride + i * 512 + lane * 16);
+    __syncwarp();
+    const int c4 = lane & 15;
+#pragma unroll
+    for (int j = 0; j < NG; j++)
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int r = 2 * i + (lane >> 4);    // row within the group (= row & 7 of the atom)
+            uint2 hi, lo;
+            split4(v[j][i], f, hi, lo);
+            uint8_t* a = grp + j * stride + r * 128 + (((c4 >> 1) ^ r) << 4) + ((c4 & 1) << 3);
+            *reinterpret_cast<uint2*>(a) = hi;
+            *reinterpret_cast<uint2*>(a + FBK_LO_OFF) = lo;
+        }
+}
+
+// LAY bit 2 (FB, fused B; 3-term): mapB1 is a map
+// over the fp32 B (row-major K x N when BMN, else B^T stored N x K), TMA-loaded per k-block into
+// the stage's B region; converter warps 10..11 apply Eq. A_1 in place (split4, the split kernels'
+// arithmetic) and write the B1/B2 planes in the layouts above.  The scale exponent comes from *fb_maxB; CTA 0 stores it to *fb_sB (read by the
 // split-K reduction).
 template <int TERMS, int BN_, int LAY>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NThr<LAY>::v, 1)
@@ -398,7 +430,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     constexpr bool BF3 = TERMS == 6;                 // bf16 x 3 split (NEXT #4): 3 planes, 6 products
     constexpr int PL = BF3 ? 3 : 2;
     constexpr bool FB = (LAY & LAY_FB) != 0;
-    static_assert(!FB || (TERMS == 3 && (LAY & 1)), "fused B: 3-term, MN-major B only");
+    static_assert(!FB || TERMS == 3, "fused B: 3-term only");
     using G = Geo<BN_, PL>;
     constexpr int F32_BYTES = G::BNH * BK * 4;   // fused B: one fp32 tile = the stage's B region
     static_assert(!FB || F32_BYTES == 2 * G::TILE_B_BYTES, "fused B: in-place split");
@@ -417,7 +449,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         FB ? 2u * (2 * TILE_A_BYTES) : 2u * (LOAD_LO ? STAGE_BYTES : TILE_A_BYTES + TILE_B_BYTES);
     constexpr bool BMN = (LAY & 1) != 0, AMN = (LAY & 2) != 0;
     constexpr uint32_t IDESC = make_idesc(2 * BM, BN_, BF3) | (AMN ? (1u << 15) : 0u) | (BMN ? (1u << 16) : 0u);
-    constexpr uint64_t DKB = FB ? (FB_STEP_BYTES >> 4) : BMN ? (2048 >> 4) : (32 >> 4);   // B step per K = 16
+    constexpr uint64_t DKB = (FB && BMN) ? (FB_STEP_BYTES >> 4) : BMN ? (2048 >> 4) : (32 >> 4);   // B step per K = 16
     constexpr uint64_t DKA = AMN ? (2048 >> 4) : (32 >> 4);   // A descriptor step per K = 16
     constexpr int MN_BOX_BYTES = 64 * BK * 2;                 // one 64 (N) x 64 (K) box
     constexpr int B_OFF = PL * TILE_A_BYTES;         // B planes follow the A planes in a stage
@@ -552,7 +584,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     if (FB) {   // fp32 B tile into the stage's B region (own CTA, own barrier)
                         const uint32_t ffb = smem_u32(&ffull_bar[stage]);
                         mbar_expect_tx(ffb, F32_BYTES);
-                        tma_load_2d_cta(smem_u32(st + B_OFF), &mapB1, ffb, y_b, x, tune.pol_b);   // 128 N x 64 K
+                        if (BMN) tma_load_2d_cta(smem_u32(st + B_OFF), &mapB1, ffb, y_b, x, tune.pol_b);   // 128 N x 64 K
+                        else tma_load_2d_cta(smem_u32(st + B_OFF), &mapB1, ffb, x, y_b, tune.pol_b);       // 64 K x 128 N
                     }
                     load_a(0, &mapA1);
                     if (!FB) load_b(B_OFF, &mapB1);
@@ -609,11 +642,12 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     const uint64_t a2 = adesc(TILE_A_BYTES);
                     const uint64_t a3 = adesc(2 * TILE_A_BYTES);
                     auto bdesc = [&](int off) {
-                        return FB ? sdesc_mn_sw128(smem_u32(st + off), FB_LBO)
+                        return FB ? (BMN ? sdesc_mn_sw128(smem_u32(st + off), FB_LBO)
+                                         : sdesc_sw128(smem_u32(st + off), FBK_GROUP_BYTES))
                                   : BMN ? sdesc_mn_sw128(smem_u32(st + off), MN_BOX_BYTES) : sdesc_sw128(smem_u32(st + off));
                     };
                     const uint64_t b1 = bdesc(B_OFF);
-                    const uint64_t b2 = bdesc(B_OFF + (FB ? FB_LO_OFF : TILE_B_BYTES));
+                    const uint64_t b2 = bdesc(B_OFF + (FB ? (BMN ? FB_LO_OFF : FBK_LO_OFF) : TILE_B_BYTES));
                     const uint64_t b3 = bdesc(B_OFF + 2 * TILE_B_BYTES);
                     // D_hi first at both ends of a unit: at the start the epilogue frees D_hi before
                     // D_mid; at the end the last D_hi drain overlaps the last D_mid MMAs
@@ -693,8 +727,16 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                 mbar_wait(smem_u32(&ffull_bar[stage]), phase);
                 uint8_t* breg = smem + stage * STAGE_BYTES + B_OFF;
 #ifndef SPLIT3_EXP_NO_CONVERT   // experiment only: time the fused-B pipeline without the conversion
-                convert_step(breg + cw * FB_STEP_BYTES, lane, f);
-                convert_step(breg + (cw + 2) * FB_STEP_BYTES, lane, f);
+                if (BMN) {
+                    convert_step(breg + cw * FB_STEP_BYTES, lane, f);
+                    convert_step(breg + (cw + 2) * FB_STEP_BYTES, lane, f);
+                } else {
+                    // groups cw, cw + 2, ... (8 per warp) in two passes of 4
+                    static_assert(!FB || BNH / 8 == 8 * NUM_CONV_WARPS, "8 groups per converter warp");
+                    convert_kgroups<4>(breg + cw * FBK_GROUP_BYTES, NUM_CONV_WARPS * FBK_GROUP_BYTES, lane, f);
+                    convert_kgroups<4>(breg + (cw + 4 * NUM_CONV_WARPS) * FBK_GROUP_BYTES, NUM_CONV_WARPS * FBK_GROUP_BYTES,
+                                       lane, f);
+                }
 #else
                 (void)breg; (void)f;
 #endif
@@ -1063,7 +1105,7 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     const bool b_mn = (mn & 1) != 0, a_mn = (mn & 2) != 0;
     CUtensorMap ma1, ma2, mb1, mb2, ma3, mb3;
     if (Bf) {   // fused B (3-term): fp32 B map in place of the B plane maps
-        if (terms != 3 || !b_mn || !d_maxB || (ldb % 4) != 0 || (reinterpret_cast<uintptr_t>(Bf) & 15u) != 0) {
+        if (terms != 3 || !d_maxB || (ldb % 4) != 0 || (reinterpret_cast<uintptr_t>(Bf) & 15u) != 0) {
             *err = 1;   // SPLIT3_ERR_INVALID_VALUE
             return -1;
         }
@@ -1080,7 +1122,8 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
         return a_mn ? make_plane_map(m, p, K, M, ldpa, BK) : make_plane_map(m, p, M, K, ldpa, BM);
     };
     // fused B: row-major K x N fp32, box 128 N x 64 K
-    const bool bmaps = Bf ? make_f32_map(&mb1, Bf, K, N, ldb, bnh, BK) : (map_b(&mb1, B1t) && map_b(&mb2, B2e));
+    const bool bmaps = Bf ? (b_mn ? make_f32_map(&mb1, Bf, K, N, ldb, bnh, BK) : make_f32_map(&mb1, Bf, N, K, ldb, BK, bnh))
+                          : (map_b(&mb1, B1t) && map_b(&mb2, B2e));
     if (Bf) mb2 = mb1;
     if (!map_a(&ma1, A1) || !map_a(&ma2, A2e) || !bmaps) {
         *err = 4;   // SPLIT3_ERR_CUDA
@@ -1118,8 +1161,7 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
         switch (mn & 3) { case 1: r = launch_t<6, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 2: r = launch_t<6, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 3: r = launch_t<6, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; default: r = launch_t<6, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); }
     } else if (Bf) {
         int32_t* sBw = const_cast<int32_t*>(d_sB);
-        if (mn & 2) r = launch_t<3, 256, 7>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial, d_maxB, sBw);
-        else r = launch_t<3, 256, 5>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial, d_maxB, sBw);
+        switch (mn & 3) { case 1: r = launch_t<3, 256, 5>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial, d_maxB, sBw); break; case 2: r = launch_t<3, 256, 6>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial, d_maxB, sBw); break; case 3: r = launch_t<3, 256, 7>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial, d_maxB, sBw); break; default: r = launch_t<3, 256, 4>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial, d_maxB, sBw); }
     } else {
         switch (mn & 3) { case 1: r = launch_t<3, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 2: r = launch_t<3, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 3: r = launch_t<3, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; default: r = launch_t<3, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); }
     }

@@ -160,3 +160,18 @@ def test_fused_nonfinite_b(hf, hs):
     with pytest.raises(s3.NotFiniteError) as ei:
         hf.sgemm(A, B, check_finite=True)
     assert ei.value.index == M * K + 10 * N + 7
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 512), (1000, 1030, 129), (257, 72, 4100), (7, 4096, 8192),
+                                   (2048, 2048, 2048), (1, 1, 1)])
+@pytest.mark.parametrize("dist", ["uniform", "loguni"])
+def test_fused_kmajor_equals_separate(hf, hs, M, N, K, dist):
+    """B given as B^T (stored N x K): the K-major in-place layout (8-row groups, SBO 2 KB)"""
+    A = torch_matrix("uniform", M, K, seed=54)
+    Bt = torch_matrix(dist, N, K, seed=55)
+    Cf = hf.sgemm_ex(A, Bt, transB=True).clone()
+    nf = hf.last_launch_count()
+    Cs = hs.sgemm_ex(A, Bt, transB=True)
+    assert torch.equal(_bits(Cf), _bits(Cs))
+    if M * K + N * K > 4 << 20:
+        assert nf == hs.last_launch_count() - 1      # no transposing split of B
