@@ -426,6 +426,33 @@ def test_planes_exhaustive_fp32_range(h, orc):
     assert checked == 2 * 0x47000000
 
 
+def test_planes_exhaustive_fp32_large(h, orc):
+    """The rest of the finite fp32 patterns, 2^15 <= |x| <= FLT_MAX (2 x 0x38800000 ~ 1.9e9
+    values): each 2^28-pattern chunk's max sets a large scale exponent (up to the s = 113 of
+    FLT_MAX), so most of the chunk lands in the fp16 subnormal / zero range after the exact
+    2^-s scaling — GPU planes == oracle planes, bit for bit, with the two pins above covering
+    every finite fp32 pattern."""
+    chunk = 1 << 28
+    lo_pat, hi_pat = 0x47000000, 0x7F800000
+    checked = 0
+    for sign in (0, 0x80000000):
+        for start in range(lo_pat, hi_pat, chunk):
+            n = min(chunk, hi_pat - start)
+            assert n % 4096 == 0
+            bits = torch.arange(start, start + n, dtype=torch.int64, device="cuda") + sign
+            X = bits.to(torch.int32).view(torch.float32).view(n // 4096, 4096)
+            del bits
+            hi, lo, s, _ = _gpu_split(h, X, transpose=False)
+            hi_o, lo_o, s_o = orc.split(X.cpu().numpy())
+            assert s == s_o
+            assert np.array_equal(_planes_np(hi, X.shape[0], 4096), hi_o)
+            assert np.array_equal(_planes_np(lo, X.shape[0], 4096), lo_o)
+            checked += n
+            del X, hi, lo
+            torch.cuda.empty_cache()
+    assert checked == 2 * (hi_pat - lo_pat)
+
+
 @pytest.mark.parametrize("shape,kw", [((2048, 2048, 1024), {}), ((256, 1024, 4096), {}),
                                       ((700, 900, 1500), {"bf16x3": True})])
 def test_cuda_graph_capture_replay(h, shape, kw):
