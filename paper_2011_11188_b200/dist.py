@@ -131,10 +131,11 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
     """One rank's share of C = A*B.  A_blk: its (M/P) x K block of A; B_blk: its K x (N/P)
     block of B.  Returns the rank's m x n C tile (see the module docstring).
 
-    overlap (NCCL only): the B^T panel is gathered first; the GEMM on the rank's OWN A rows then
-    runs on the compute stream while the A panel is all-gathered on a communication stream; the
-    other row blocks follow when it lands.  Each row block is a separate GEMM over whole tiles,
-    so every C element is computed exactly as in the non-overlapped schedule.
+    overlap: the rank's own A rows are multiplied first — by its own B block's columns before the
+    B^T panel has landed, then by the rest of the panel — while (NCCL) the panels are all-gathered
+    on a communication stream; the other row blocks follow when the A panel lands.  Each piece is
+    a separate GEMM over whole tiles, so every C element is computed exactly as in the
+    non-overlapped schedule.
 
     on_block(rows): called after the GEMM of each row block of the tile is enqueued (rows = a
     slice of `out`'s rows), e.g. to copy that part of C out while the next block computes.
@@ -160,33 +161,65 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
     b_hi, b_lo, sB = ops.split(B_blk, mx[1:2], True)
     rowblocks = overlap and pc > 1
     use_streams = rowblocks and dev.type == "cuda" and dist.get_backend() == "nccl"
-    # 4a: B^T panel (needed by every row block)
-    B1t = _gather_rows(b_hi, col_groups[j], pr)
-    B2t = B1t if one_term else _gather_rows(b_lo, col_groups[j], pr)
+    a_lo2 = a_hi if one_term else a_lo
+    b_lo2 = b_hi if one_term else b_lo
     if out is None:
         out = torch.empty((m, n), dtype=torch.float32, device=dev)
+
+    def put(dst, res):
+        if res is not None and res.data_ptr() != dst.data_ptr():
+            dst.copy_(res)
+
     if not rowblocks:
-        # 4b + 5: A panel, then one GEMM on the whole tile
+        # 4 + 5: both panels, then one GEMM on the whole tile
+        B1t = _gather_rows(b_hi, col_groups[j], pr)
+        B2t = B1t if one_term else _gather_rows(b_lo, col_groups[j], pr)
         A1 = _gather_rows(a_hi, row_groups[i], pc)
         A2 = A1 if one_term else _gather_rows(a_lo, row_groups[i], pc)
-        res = ops.gemm(m, n, K, A1, A2, sA, B1t, B2t, sB, out, four_term, one_term)
-        if res is not out:
-            out.copy_(res)
+        put(out, ops.gemm(m, n, K, A1, A2, sA, B1t, B2t, sB, out, four_term, one_term))
         if on_block is not None:
             on_block(slice(0, m))
         return out
-    # 4b under 5a: gather the A panel (side stream under NCCL) while the own rows are multiplied
+    # 4 under 5: the B^T panel and then the A panel are gathered on a communication stream (NCCL)
+    # while the compute stream multiplies what is already local — the own A rows times the own
+    # B block's columns first (no exchange at all), then the own rows times the other B blocks of
+    # the column panel, then the other row blocks of the A panel.  Every piece is a GEMM over whole
+    # tiles (block widths are multiples of the tile), so C is the same as without the overlap.
     compute = torch.cuda.current_stream(dev) if use_streams else None
     comm = torch.cuda.Stream(device=dev) if use_streams else None
     if use_streams:
         comm.wait_stream(compute)
         with torch.cuda.stream(comm):
+            B1t = _gather_rows(b_hi, col_groups[j], pr)
+            B2t = B1t if one_term else _gather_rows(b_lo, col_groups[j], pr)
+            ev_b = torch.cuda.Event()
+            ev_b.record(comm)
             A1 = _gather_rows(a_hi, row_groups[i], pc)
             A2 = A1 if one_term else _gather_rows(a_lo, row_groups[i], pc)
+
+    def panel_b():
+        nonlocal B1t, B2t
+        if use_streams:
+            compute.wait_event(ev_b)
+        else:
+            B1t = _gather_rows(b_hi, col_groups[j], pr)
+            B2t = B1t if one_term else _gather_rows(b_lo, col_groups[j], pr)
+
     own = slice(j * mb, (j + 1) * mb)
-    res = ops.gemm(mb, n, K, a_hi, a_hi if one_term else a_lo, sA, B1t, B2t, sB, out[own], four_term, one_term)
-    if res is not None and res.data_ptr() != out[own].data_ptr():
-        out[own].copy_(res)
+    if pr > 1:
+        nbk = n // pr                         # columns of one B block in the column panel
+        oc = slice(i * nbk, (i + 1) * nbk)    # this rank's own block (position i in the panel)
+        put(out[own, oc], ops.gemm(mb, nbk, K, a_hi, a_lo2, sA, b_hi, b_lo2, sB, out[own, oc], four_term, one_term))
+        panel_b()
+        for q in range(pr):
+            if q == i:
+                continue
+            cs = slice(q * nbk, (q + 1) * nbk)
+            put(out[own, cs], ops.gemm(mb, nbk, K, a_hi, a_lo2, sA, B1t[cs], B2t[cs], sB, out[own, cs],
+                                       four_term, one_term))
+    else:
+        panel_b()
+        put(out[own], ops.gemm(mb, n, K, a_hi, a_lo2, sA, B1t, B2t, sB, out[own], four_term, one_term))
     if on_block is not None:
         on_block(own)
     if use_streams:
@@ -198,14 +231,12 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
         if q == j:
             continue
         rs = slice(q * mb, (q + 1) * mb)
-        res = ops.gemm(mb, n, K, A1[rs], A2[rs], sA, B1t, B2t, sB, out[rs], four_term, one_term)
-        if res is not None and res.data_ptr() != out[rs].data_ptr():
-            out[rs].copy_(res)
+        put(out[rs], ops.gemm(mb, n, K, A1[rs], A2[rs], sA, B1t, B2t, sB, out[rs], four_term, one_term))
         if on_block is not None:
             on_block(rs)
     if use_streams:
-        A1.record_stream(compute)
-        A2.record_stream(compute)
+        for t in (A1, A2, B1t, B2t):
+            t.record_stream(compute)
     return out
 
 

@@ -57,3 +57,30 @@ def test_tile_gemm_replicated_one_rank(nccl_one_rank, n):
     assert torch.equal(C.view(torch.int32), ref.view(torch.int32)) or \
         float((C.double() - ref.double()).norm() / ref.double().norm()) < 1e-6
     assert tg.launches_per_step() >= 5
+
+
+def test_gemm_planes_column_pieces_equal_whole():
+    """the 2-D driver's column pieces (own rows x one B block of the panel, written into a column
+    slice of the tile): gemm_planes on B^T plane row slices into strided C views == one whole call
+    (to the oracle tolerance: the pieces' split-K plans, and so summation orders, differ)"""
+    import paper_2011_11188_b200 as s3
+    from workloads import torch_matrix
+
+    h = s3.Handle(0)
+    m, n, K, pr = 1024, 2048, 1536, 2
+    A = torch_matrix("uniform", m, K, seed=61)
+    B = torch_matrix("loguni", K, n, seed=62)
+    mx = torch.zeros(2, dtype=torch.float32, device="cuda")
+    h.maxabs(A, mx[0:1])
+    h.maxabs(B, mx[1:2])
+    a_hi, a_lo, sA = h.split(A, mx[0:1])
+    b_hi, b_lo, sB = h.split(B, mx[1:2], transpose=True)          # B^T planes: n x K
+    whole = h.gemm_planes(m, n, K, a_hi, a_lo, sA, b_hi, b_lo, sB).clone()
+    C = torch.full((m, n), 7.0, device="cuda")
+    nbk = n // pr
+    for q in range(pr):
+        cs = slice(q * nbk, (q + 1) * nbk)
+        h.gemm_planes(m, nbk, K, a_hi, a_lo, sA, b_hi[cs], b_lo[cs], sB, out=C[:, cs])
+    torch.cuda.synchronize()
+    assert torch.isfinite(C).all()
+    assert float((C.double() - whole.double()).norm() / whole.double().norm()) < 1e-6
