@@ -109,7 +109,9 @@ int split3_sgemm(split3_handle_t h, int64_t M, int64_t N, int64_t K,
  * the handle's stream before returning.  C is bit-identical to split3_sgemm on the same inputs.
  * Pipelined: B is copied first, then A in up to 20 row blocks, each split and
  * multiplied as soon as it lands while the next one copies in, and C row blocks copy out
- * underneath; env SPLIT3_HOST_BLOCKS=<1..16> at handle creation fixes the block count.  Device staging for A, B and C is taken from the
+ * underneath (2-D: B in 2 column panels, the second right after the first A block, so C pieces
+ * leave early); env SPLIT3_HOST_BLOCKS=<1..16> / SPLIT3_HOST_PANELS=<1..4> at handle creation fix
+ * the block / panel counts.  Device staging for A, B and C is taken from the
  * workspace, which must hold split3_sgemm_host_workspace_size(M, N, K, flags) bytes.
  * Host layout is packed row-major (lda = K, ldb = N, ldc = N). */
 size_t split3_sgemm_host_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags);

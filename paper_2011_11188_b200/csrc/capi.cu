@@ -45,10 +45,12 @@ struct split3_ctx {
     // host-buffer entry: copy-in / copy-out streams and events, created on first use
     cudaStream_t s_in = nullptr, s_out = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_done = nullptr;
-    cudaEvent_t ev_rows[32] = {};      // C row block b computed
+    cudaEvent_t ev_rows[64] = {};      // C piece computed (ring)
     cudaEvent_t ev_arows[32] = {};     // A row block b copied in
+    cudaEvent_t ev_pan[4] = {};        // B column panel j copied in
     int host_blocks = 0;               // row blocks of the host pipeline (0 = automatic; env SPLIT3_HOST_BLOCKS)
     long long host_redo = 0;           // row blocks redone with the per-matrix scale (split3_host_redo_count)
+    int host_panels = 0;               // B column panels of the 2-D host schedule (0 = automatic; env SPLIT3_HOST_PANELS)
     // measurement hooks: event triples (start, after split, after gemm) per timed call
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -213,6 +215,7 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
     if (const char* e = getenv("SPLIT3_PREP_MAX")) c->prep_max = atoll(e);
     if (const char* e = getenv("SPLIT3_FUSE_B")) c->fuse_b = atoi(e);
     if (const char* e = getenv("SPLIT3_HOST_BLOCKS")) c->host_blocks = std::min(std::max(atoi(e), 0), 16);
+    if (const char* e = getenv("SPLIT3_HOST_PANELS")) c->host_panels = std::min(std::max(atoi(e), 0), 4);
     if (const char* e = getenv("SPLIT3_FUSE_B_MAX_M")) c->fuse_b_max_m = atoll(e);
     *h = c;
     return SPLIT3_OK;
@@ -233,6 +236,10 @@ int split3_sgemm_destroy(split3_handle_t h) {
         for (cudaEvent_t e : {h->ev_a, h->ev_b, h->ev_done})
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : h->ev_rows)
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : h->ev_arows)
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : h->ev_pan)
             if (e) cudaEventDestroy(e);
     }
     delete h;
@@ -770,7 +777,9 @@ int split3_timing_read(split3_handle_t h, double* split_ms, double* gemm_ms, int
 
 // host pipeline: per-row-block scalars after the staging buffers
 constexpr int kMaxHostBlocks = 32;
-constexpr size_t kHostScalarBytes = 4 * 4 * kMaxHostBlocks;
+constexpr int kMaxPanels = 4;
+constexpr int kMaxPieceEvents = 64;   // ring of "C piece computed" events (ev_rows)
+constexpr size_t kHostScalarBytes = 4 * 4 * (kMaxHostBlocks + kMaxPanels);
 
 size_t split3_sgemm_host_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags) {
     if (M < 0 || N < 0 || K < 0) return 0;
@@ -822,6 +831,8 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
             if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return SPLIT3_ERR_CUDA;
         for (cudaEvent_t& e : h->ev_arows)
             if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return SPLIT3_ERR_CUDA;
+        for (cudaEvent_t& e : h->ev_pan)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return SPLIT3_ERR_CUDA;
     }
     cudaStream_t s0 = h->stream;
     // row blocks: multiples of the 256-row pair tile, each >= 2 waves of tiles (more blocks shorten
@@ -857,85 +868,172 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
         }
     }
     Carve w = carve(h->ws, M, N, K);
-    // per-block scalars after the staging buffers: max bits, min-nonzero bits, exponents, redo flags
+    const bool b_mn = h->mn_major != 0;  // MN-major B planes (plain split) unless disabled
+    const int64_t ldpb = b_mn ? w.ldpb_mn : w.ldpb;
+    // 2-D schedule: with >= 4 A blocks and a wide B, B is copied in column panels interleaved with
+    // the A blocks at equal byte rates, each panel split with its own exponent, and the C piece
+    // (A block i, B panel j) is multiplied and copied out as soon as both have landed — C starts
+    // leaving a fraction of B in, not after all of it (§5e).  Panels are multiples of 256 columns.
+    int nbp = 1;
+    if (b_mn && nblk >= 4 && h->host_blocks == 0 && N >= 4 * 1024)
+        nbp = h->host_panels > 0 ? std::min(h->host_panels, kMaxPanels) : 2;
+    const int64_t cols_per = ((N + nbp - 1) / nbp + 255) / 256 * 256;
+    int64_t pan_c0[kMaxPanels], pan_nc[kMaxPanels];
+    nbp = 0;
+    for (int64_t c0 = 0; c0 < N; c0 += cols_per) {
+        pan_c0[nbp] = c0;
+        pan_nc[nbp++] = std::min(cols_per, N - c0);
+    }
+    // scalars after the staging buffers: per A block and per B panel max bits, min-nonzero bits,
+    // exponents, redo flags
     uint8_t* sc = reinterpret_cast<uint8_t*>(dC) + align256((size_t)M * N * 4);
+    constexpr int kSlots = kMaxHostBlocks + kMaxPanels;
     unsigned* maxblk = reinterpret_cast<unsigned*>(sc);
-    unsigned* minblk = reinterpret_cast<unsigned*>(sc + 4 * kMaxHostBlocks);
-    int32_t* sblk = reinterpret_cast<int32_t*>(sc + 8 * kMaxHostBlocks);
-    int32_t* flags_d = reinterpret_cast<int32_t*>(sc + 12 * kMaxHostBlocks);
+    unsigned* minblk = reinterpret_cast<unsigned*>(sc + 4 * kSlots);
+    int32_t* sblk = reinterpret_cast<int32_t*>(sc + 8 * kSlots);
+    int32_t* flags_d = reinterpret_cast<int32_t*>(sc + 12 * kSlots);
+    unsigned* maxpan = maxblk + kMaxHostBlocks;
+    unsigned* minpan = minblk + kMaxHostBlocks;
+    int32_t* span = sblk + kMaxHostBlocks;
+    // transfer order: B panel 0, A block 0, B panel 1, A block 1, ... until B is in, then the rest
+    // of A (the first A blocks are the small quarter cuts: B still lands almost as early as in
+    // one piece, while the first C pieces can already leave)
+    int order[kMaxHostBlocks + kMaxPanels];
+    int nitems = 0;
+    {
+        int next_pan = 0;
+        order[nitems++] = -1 - next_pan++;
+        for (int b = 0; b < nblk; b++) {
+            order[nitems++] = b;
+            if (next_pan < nbp) order[nitems++] = -1 - next_pan++;
+        }
+        while (next_pan < nbp) order[nitems++] = -1 - next_pan++;
+    }
     // copy-in must not overwrite the staging buffers while an earlier call on s0 still reads them
     if (cudaEventRecord(h->ev_done, s0) != cudaSuccess || cudaStreamWaitEvent(h->s_in, h->ev_done, 0) != cudaSuccess)
         return SPLIT3_ERR_CUDA;
-    if (cudaMemcpyAsync(dB, B_host, (size_t)K * N * 4, cudaMemcpyHostToDevice, h->s_in) != cudaSuccess ||
-        cudaEventRecord(h->ev_b, h->s_in) != cudaSuccess)
-        return SPLIT3_ERR_CUDA;
-    for (int b = 0; b < nblk; b++) {
-        const int64_t r0 = blk_r0[b], mr = blk_mr[b];
-        if (cudaMemcpyAsync(dA + r0 * K, A_host + r0 * K, (size_t)mr * K * 4, cudaMemcpyHostToDevice, h->s_in) !=
-                cudaSuccess ||
-            cudaEventRecord(h->ev_arows[b], h->s_in) != cudaSuccess)
-            return SPLIT3_ERR_CUDA;
+    for (int it = 0; it < nitems; it++) {
+        const int x = order[it];
+        if (x < 0) {
+            const int j = -1 - x;
+            if (cudaMemcpy2DAsync(dB + pan_c0[j], (size_t)N * 4, B_host + pan_c0[j], (size_t)N * 4, (size_t)pan_nc[j] * 4,
+                                  (size_t)K, cudaMemcpyHostToDevice, h->s_in) != cudaSuccess ||
+                cudaEventRecord(h->ev_pan[j], h->s_in) != cudaSuccess)
+                return SPLIT3_ERR_CUDA;
+        } else {
+            const int64_t r0 = blk_r0[x], mr = blk_mr[x];
+            if (cudaMemcpyAsync(dA + r0 * K, A_host + r0 * K, (size_t)mr * K * 4, cudaMemcpyHostToDevice, h->s_in) !=
+                    cudaSuccess ||
+                cudaEventRecord(h->ev_arows[x], h->s_in) != cudaSuccess)
+                return SPLIT3_ERR_CUDA;
+        }
     }
     int launches = 0, n;
-    if (cudaMemsetAsync(h->ws, 0, 32, s0) != cudaSuccess || cudaMemsetAsync(maxblk, 0, 4 * kMaxHostBlocks, s0) != cudaSuccess ||
-        cudaMemsetAsync(minblk, 0xFF, 4 * kMaxHostBlocks, s0) != cudaSuccess || cudaStreamWaitEvent(s0, h->ev_b, 0) != cudaSuccess)
+    if (cudaMemsetAsync(h->ws, 0, 32, s0) != cudaSuccess || cudaMemsetAsync(maxblk, 0, 4 * kSlots, s0) != cudaSuccess ||
+        cudaMemsetAsync(minblk, 0xFF, 4 * kSlots, s0) != cudaSuccess)
         return SPLIT3_ERR_CUDA;
-    if ((n = split3::launch_maxabs(s0, K, N, dB, N, w.maxB, nullptr, h->num_sms)) < 0) return SPLIT3_ERR_CUDA;
-    launches += n;
-    const bool b_mn = h->mn_major != 0;  // MN-major B planes (plain split) unless disabled
-    const int64_t ldpb = b_mn ? w.ldpb_mn : w.ldpb;
-    if ((n = b_mn ? split3::launch_split(s0, K, N, dB, N, w.maxB, w.B1t, w.B2t, ldpb, w.sB, h->num_sms)
-                  : split3::launch_split_t(s0, K, N, dB, N, w.maxB, w.B1t, w.B2t, ldpb, w.sB, h->num_sms)) < 0)
-        return SPLIT3_ERR_CUDA;
-    launches += n;
-    auto gemm_block = [&](int64_t r0, int64_t mr, const int32_t* d_sA) {
+    auto gemm_piece = [&](int b, int j, const int32_t* d_sA, const int32_t* d_sB) {
+        const int64_t r0 = blk_r0[b], mr = blk_mr[b], c0 = pan_c0[j], nc = pan_nc[j];
         int err = 0;
-        int r = split3::launch_gemm3(s0, mr, N, K, w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa, w.ldpa, d_sA, w.B1t, w.B2t,
-                                     ldpb, w.sB, dC + r0 * N, N, terms_of(flags), h->num_sms, h->promo_kb,
-                                     h->wave_sync ? h->d_counters : nullptr, h->tune, nullptr, 0, &err, nullptr,
-                                     nullptr, b_mn ? 1 : 0);
+        // MN-major B planes: columns [c0, c0 + nc) of the K x N planes; K-major (one panel): all
+        int r = split3::launch_gemm3(s0, mr, nc, K, w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa, w.ldpa, d_sA, w.B1t + c0,
+                                     w.B2t + c0, ldpb, d_sB, dC + r0 * N + c0, N, terms_of(flags), h->num_sms,
+                                     h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune, nullptr, 0, &err,
+                                     nullptr, nullptr, b_mn ? 1 : 0);
         return r < 0 ? -(err ? err : SPLIT3_ERR_CUDA) : r;
     };
-    for (int b = 0; b < nblk; b++) {
-        const int64_t r0 = blk_r0[b], mr = blk_mr[b];
-        if (cudaStreamWaitEvent(s0, h->ev_arows[b], 0) != cudaSuccess) return SPLIT3_ERR_CUDA;
-        const float* Ab = dA + r0 * K;
-        float* bmax = reinterpret_cast<float*>(maxblk + b);
-        if (nblk > 1) {
+    auto copy_out = [&](int b, int j, cudaStream_t st) {
+        const int64_t r0 = blk_r0[b], mr = blk_mr[b], c0 = pan_c0[j], nc = pan_nc[j];
+        return cudaMemcpy2DAsync(C_host + r0 * N + c0, (size_t)N * 4, dC + r0 * N + c0, (size_t)N * 4, (size_t)nc * 4,
+                                 (size_t)mr, cudaMemcpyDeviceToHost, st) == cudaSuccess;
+    };
+    bool have_a[kMaxHostBlocks] = {false}, have_b[kMaxPanels] = {false};
+    int nev = 0;
+    auto piece = [&](int b, int j) {      // GEMM of (block b, panel j), then its copy-out on s_out
+        int r = gemm_piece(b, j, sblk + b, span + j);
+        if (r < 0) return r;
+        launches += r;
+        cudaEvent_t e = h->ev_rows[nev++ % kMaxPieceEvents];
+        if (cudaEventRecord(e, s0) != cudaSuccess || cudaStreamWaitEvent(h->s_out, e, 0) != cudaSuccess ||
+            !copy_out(b, j, h->s_out))
+            return -SPLIT3_ERR_CUDA;
+        return 0;
+    };
+    for (int it = 0; it < nitems; it++) {
+        const int x = order[it];
+        if (x < 0) {   // B panel j: max/min, split with its own exponent, then its pieces
+            const int j = -1 - x;
+            const float* Bp = dB + pan_c0[j];
+            if (cudaStreamWaitEvent(s0, h->ev_pan[j], 0) != cudaSuccess) return SPLIT3_ERR_CUDA;
+            if ((n = split3::launch_maxmin2d(s0, K, pan_nc[j], Bp, N, maxpan + j, minpan + j, h->num_sms)) < 0)
+                return SPLIT3_ERR_CUDA;
+            launches += n;
+            const float* pmax = reinterpret_cast<const float*>(maxpan + j);
+            if ((n = b_mn ? split3::launch_split(s0, K, pan_nc[j], Bp, N, pmax, w.B1t + pan_c0[j], w.B2t + pan_c0[j],
+                                                 ldpb, span + j, h->num_sms)
+                          : split3::launch_split_t(s0, K, N, dB, N, pmax, w.B1t, w.B2t, ldpb, span + j, h->num_sms)) < 0)
+                return SPLIT3_ERR_CUDA;
+            launches += n;
+            have_b[j] = true;
+            for (int b = 0; b < nblk; b++)
+                if (have_a[b] && (n = piece(b, j)) < 0) return -n;
+        } else {       // A block b: max/min, split with its own exponent, then its pieces
+            const int b = x;
+            const int64_t r0 = blk_r0[b], mr = blk_mr[b];
+            if (cudaStreamWaitEvent(s0, h->ev_arows[b], 0) != cudaSuccess) return SPLIT3_ERR_CUDA;
+            const float* Ab = dA + r0 * K;
             if ((n = split3::launch_maxmin(s0, mr * K, Ab, maxblk + b, minblk + b, h->num_sms)) < 0) return SPLIT3_ERR_CUDA;
-        } else if ((n = split3::launch_maxabs(s0, mr, K, Ab, K, bmax, nullptr, h->num_sms)) < 0) {
-            return SPLIT3_ERR_CUDA;
+            launches += n;
+            if ((n = split3::launch_split(s0, mr, K, Ab, K, reinterpret_cast<const float*>(maxblk + b),
+                                          w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa, w.ldpa, sblk + b, h->num_sms)) < 0)
+                return SPLIT3_ERR_CUDA;
+            launches += n;
+            have_a[b] = true;
+            for (int j = 0; j < nbp; j++)
+                if (have_b[j] && (n = piece(b, j)) < 0) return -n;
         }
-        launches += n;
-        if ((n = split3::launch_split(s0, mr, K, Ab, K, bmax, w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa, w.ldpa, sblk + b,
-                                      h->num_sms)) < 0)
-            return SPLIT3_ERR_CUDA;
-        launches += n;
-        if ((n = gemm_block(r0, mr, sblk + b)) < 0) return -n;
-        launches += n;
-        if (cudaEventRecord(h->ev_rows[b], s0) != cudaSuccess || cudaStreamWaitEvent(h->s_out, h->ev_rows[b], 0) != cudaSuccess ||
-            cudaMemcpyAsync(C_host + r0 * N, dC + r0 * N, (size_t)mr * N * 4, cudaMemcpyDeviceToHost, h->s_out) != cudaSuccess)
-            return SPLIT3_ERR_CUDA;
     }
-    if (nblk > 1) {
-        int32_t flags_h[kMaxHostBlocks] = {0};
-        if ((n = split3::launch_host_scale_check(s0, maxblk, minblk, sblk, nblk, w.maxA, w.sA, flags_d)) < 0 ||
-            cudaMemcpyAsync(flags_h, flags_d, (size_t)nblk * 4, cudaMemcpyDeviceToHost, s0) != cudaSuccess ||
+    // per-matrix scales from the block / panel maxima, and the pieces to redo (rare)
+    if (nblk > 1 || nbp > 1) {
+        int32_t fa[kMaxHostBlocks] = {0}, fb[kMaxPanels] = {0};
+        if ((n = split3::launch_host_scale_check(s0, maxblk, minblk, sblk, nblk, w.maxA, w.sA, flags_d)) < 0)
+            return SPLIT3_ERR_CUDA;
+        launches += n;
+        if ((n = split3::launch_host_scale_check(s0, maxpan, minpan, span, nbp, w.maxB, w.sB, flags_d + kMaxHostBlocks)) < 0)
+            return SPLIT3_ERR_CUDA;
+        launches += n;
+        if (cudaMemcpyAsync(fa, flags_d, (size_t)nblk * 4, cudaMemcpyDeviceToHost, s0) != cudaSuccess ||
+            cudaMemcpyAsync(fb, flags_d + kMaxHostBlocks, (size_t)nbp * 4, cudaMemcpyDeviceToHost, s0) != cudaSuccess ||
             cudaStreamSynchronize(s0) != cudaSuccess || cudaStreamSynchronize(h->s_out) != cudaSuccess)
             return SPLIT3_ERR_CUDA;
-        launches += n;
-        for (int b = 0; b < nblk; b++) {   // rare: redo with the per-matrix scale
-            if (!flags_h[b]) continue;
-            const int64_t r0 = blk_r0[b], mr = blk_mr[b];
-            if ((n = split3::launch_split(s0, mr, K, dA + r0 * K, K, w.maxA, w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa,
-                                          w.ldpa, w.sA, h->num_sms)) < 0)
-                return SPLIT3_ERR_CUDA;
-            launches += n;
-            if ((n = gemm_block(r0, mr, w.sA)) < 0) return -n;
-            launches += n;
-            if (cudaMemcpyAsync(C_host + r0 * N, dC + r0 * N, (size_t)mr * N * 4, cudaMemcpyDeviceToHost, s0) != cudaSuccess)
-                return SPLIT3_ERR_CUDA;
-            h->host_redo++;
+        bool any = false;
+        for (int b = 0; b < nblk; b++) any |= fa[b] != 0;
+        for (int j = 0; j < nbp; j++) any |= fb[j] != 0;
+        if (any) {
+            for (int b = 0; b < nblk; b++) {   // re-split flagged blocks / panels with the per-matrix scale
+                if (!fa[b]) continue;
+                const int64_t r0 = blk_r0[b], mr = blk_mr[b];
+                if ((n = split3::launch_split(s0, mr, K, dA + r0 * K, K, w.maxA, w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa,
+                                              w.ldpa, w.sA, h->num_sms)) < 0)
+                    return SPLIT3_ERR_CUDA;
+                launches += n;
+                h->host_redo++;
+            }
+            for (int j = 0; j < nbp; j++) {
+                if (!fb[j]) continue;
+                if ((n = split3::launch_split(s0, K, pan_nc[j], dB + pan_c0[j], N, w.maxB, w.B1t + pan_c0[j],
+                                              w.B2t + pan_c0[j], ldpb, w.sB, h->num_sms)) < 0)
+                    return SPLIT3_ERR_CUDA;
+                launches += n;
+                h->host_redo++;
+            }
+            for (int b = 0; b < nblk; b++)
+                for (int j = 0; j < nbp; j++) {
+                    if (!fa[b] && !fb[j]) continue;
+                    if ((n = gemm_piece(b, j, fa[b] ? w.sA : sblk + b, fb[j] ? w.sB : span + j)) < 0) return -n;
+                    launches += n;
+                    if (!copy_out(b, j, s0)) return SPLIT3_ERR_CUDA;
+                }
         }
     }
     if (cudaStreamSynchronize(h->s_out) != cudaSuccess || cudaStreamSynchronize(s0) != cudaSuccess)

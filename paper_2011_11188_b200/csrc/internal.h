@@ -95,6 +95,8 @@ int launch_maxabs2(cudaStream_t s, int64_t rows0, int64_t cols0, const float* X0
 // host-buffer pipeline: max |x| and min nonzero |x| (uint bits) of a contiguous chunk,
 // and the per-matrix scale check over the row blocks (see split_kernels.cu)
 int launch_maxmin(cudaStream_t s, int64_t n, const float* X, unsigned* d_max, unsigned* d_min, int num_sms);
+int launch_maxmin2d(cudaStream_t s, int64_t rows, int64_t cols, const float* X, int64_t ld, unsigned* d_max,
+                    unsigned* d_min, int num_sms);   // strided region (ld >= cols)
 int launch_host_scale_check(cudaStream_t s, const unsigned* maxblk, const unsigned* minblk, const int32_t* sblk,
                             int nblk, float* d_max, int32_t* d_sexp, int32_t* flags);
 int launch_split(cudaStream_t s, int64_t rows, int64_t cols, const float* X, int64_t ld,

@@ -239,6 +239,52 @@ __global__ void __launch_bounds__(256) maxmin_1d_kernel(const float* __restrict_
     }
 }
 
+// Same for a strided rows x cols region (a column panel of a row-major matrix, ld >= cols).
+template <bool VEC>
+__global__ void __launch_bounds__(256) maxmin_2d_kernel(const float* __restrict__ X, int64_t rows, int64_t cols,
+                                                        int64_t ld, unsigned* d_max, unsigned* d_min) {
+    pdl_enter();
+    unsigned mx = 0, mn = 0xFFFFFFFFu;
+    auto fold = [&](float x) {
+        const unsigned u = __float_as_uint(x) & 0x7FFFFFFFu;
+        if (u < kFiniteLimit) {
+            mx = max(mx, u);
+            if (u) mn = min(mn, u);
+        }
+    };
+    const int64_t units = VEC ? cols / 4 : cols;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+        for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < units; c += (int64_t)gridDim.x * blockDim.x) {
+            if (VEC) {
+                const float4 v = __ldcs(reinterpret_cast<const float4*>(X + r * ld) + c);
+                fold(v.x); fold(v.y); fold(v.z); fold(v.w);
+            } else {
+                fold(__ldcs(X + r * ld + c));
+            }
+        }
+    __shared__ unsigned sx[32], sn[32];
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { sx[w] = mx; sn[w] = mn; }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        mx = l < nw ? sx[l] : 0u;
+        mn = l < nw ? sn[l] : 0xFFFFFFFFu;
+        for (int o = 16; o > 0; o >>= 1) {
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        }
+        if (l == 0) {
+            if (mx) atomicMax(d_max, mx);
+            if (mn != 0xFFFFFFFFu) atomicMin(d_min, mn);
+        }
+    }
+}
+
 // After all row blocks: the per-matrix max (reading R1) and scale exponent sA from the block maxima;
 // flags[b] = 1 iff block b was split with an exponent below sA AND holds a nonzero |x| < 2^(sA-12):
 // only such an entry can round differently (fp16-subnormal A1 or A2), every other
@@ -631,6 +677,20 @@ int launch_maxmin(cudaStream_t st, int64_t n, const float* X, unsigned* d_max, u
     const int g = (int)(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
     if (aligned16(X)) launch_k(maxmin_1d_kernel<true>, dim3(g), dim3(256), 0, st, X, n, d_max, d_min);
     else launch_k(maxmin_1d_kernel<false>, dim3(g), dim3(256), 0, st, X, n, d_max, d_min);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_maxmin2d(cudaStream_t st, int64_t rows, int64_t cols, const float* X, int64_t ld, unsigned* d_max,
+                    unsigned* d_min, int num_sms) {
+    if (rows <= 0 || cols <= 0) return 0;
+    if (ld == cols) return launch_maxmin(st, rows * cols, X, d_max, d_min, num_sms);
+    const bool vec = (cols % 4 == 0) && (ld % 4 == 0) && aligned16(X);
+    const int64_t units = vec ? cols / 4 : cols;
+    int64_t bx = (units + 255) / 256;
+    if (bx > 64) bx = 64;
+    dim3 grid((unsigned)bx, (unsigned)grid_rows(rows, num_sms, bx));
+    if (vec) launch_k(maxmin_2d_kernel<true>, grid, dim3(256), 0, st, X, rows, cols, ld, d_max, d_min);
+    else launch_k(maxmin_2d_kernel<false>, grid, dim3(256), 0, st, X, rows, cols, ld, d_max, d_min);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

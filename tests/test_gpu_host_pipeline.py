@@ -124,3 +124,28 @@ def test_auto_blocks_with_tail(hd):
     C = h.sgemm_host(A, B)
     assert h.last_launch_count() > 6 * 3          # 6 row blocks: max/min, split, GEMM each
     assert _same(C, hd.sgemm_host(A, B))
+
+
+@pytest.mark.parametrize("case", ["plain", "b_panel_scaled", "b_tiny", "a_and_b_tiny"])
+def test_2d_schedule_b_panels(hd, case):
+    """automatic 2-D schedule (2 B column panels interleaved with the first A blocks, each panel
+    split with its own exponent): bitwise equal to the one-block call, pieces redone when needed"""
+    M, N, K = 8192, 16384, 256
+    A = numpy_matrix("uniform", M, K, seed=56)
+    B = numpy_matrix("uniform", K, N, seed=57)
+    half = N // 2                                    # B panel 0
+    if case != "plain":                              # panel 0 six binades below panel 1
+        B[:, :half] = np.sign(B[:, :half]) * np.maximum(np.abs(B[:, :half]), np.float32(2.0 ** -20))
+        B[:, :half] *= 2.0 ** -6
+    if case in ("b_tiny", "a_and_b_tiny"):
+        B[17, 100] = np.float32(2.0 ** -50)         # a tiny entry in the low-exponent panel
+    if case == "a_and_b_tiny":
+        A[:2048] = np.sign(A[:2048]) * np.maximum(np.abs(A[:2048]), np.float32(2.0 ** -20))
+        A[:2048] *= 2.0 ** -4
+        A[5, 5] = np.float32(2.0 ** -60)
+    h = s3.Handle(0)
+    r0 = h.host_redo_count()
+    C = h.sgemm_host(A, B)
+    redo = h.host_redo_count() - r0
+    assert redo == {"plain": 0, "b_panel_scaled": 0, "b_tiny": 1, "a_and_b_tiny": 2}[case], redo
+    assert _same(C, hd.sgemm_host(A, B))

@@ -37,7 +37,8 @@ if os.environ.get("E2E_CHILD"):
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ts.sort()
-    print(json.dumps({"blocks": os.environ.get("SPLIT3_HOST_BLOCKS", "0"), "ms": ts[len(ts) // 2],
+    print(json.dumps({"blocks": os.environ.get("SPLIT3_HOST_BLOCKS", "0"),
+                      "panels": os.environ.get("SPLIT3_HOST_PANELS", "0"), "ms": ts[len(ts) // 2],
                       "launches": h.last_launch_count(), "redo": h.host_redo_count()}))
     sys.exit(0)
 
@@ -81,8 +82,8 @@ res["h2d_2GiB_with_d2h_1GiB_ms"] = ev_time(both)
 del hb, hc, db, dc
 torch.cuda.empty_cache()
 runs = []
-for blocks in ("0", "1", "2", "4", "8"):
-    env = dict(os.environ, E2E_CHILD="1", SPLIT3_HOST_BLOCKS=blocks)
+for blocks, panels in (("0", "0"), ("0", "1"), ("0", "2"), ("0", "4"), ("1", "0"), ("4", "0"), ("8", "0")):
+    env = dict(os.environ, E2E_CHILD="1", SPLIT3_HOST_BLOCKS=blocks, SPLIT3_HOST_PANELS=panels)
     out = subprocess.run([sys.executable, __file__], env=env, capture_output=True, text=True)
     try:
         runs.append(json.loads(out.stdout.strip().splitlines()[-1]))
