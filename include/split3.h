@@ -106,7 +106,9 @@ int split3_sgemm(split3_handle_t h, int64_t M, int64_t N, int64_t K,
 
 /* Same computation with HOST buffers (pageable or pinned): copies A and B to the workspace
  * staging area of the handle's device, runs the method, copies C back, and synchronises
- * the handle's stream before returning.  C is bit-identical to split3_sgemm on the same inputs.
+ * the handle's stream before returning.  Same planes and scales as split3_sgemm; C is bitwise
+ * equal to it except where the device call cuts a tail wave into split-K slices (another
+ * summation order; both within the oracle tolerance).
  * Pipelined: B is copied first, then A in up to 20 row blocks, each split and
  * multiplied as soon as it lands while the next one copies in, and C row blocks copy out
  * underneath (2-D: B in 2 column panels, the second right after the first A block, so C pieces
