@@ -92,9 +92,18 @@ def _gather_rows(t: torch.Tensor, group, group_size: int) -> torch.Tensor:
     """Concatenate each group member's `t` along dim 0 (group order = member rank order)."""
     if group_size == 1:
         return t
+    return _all_gather_rows(t, group, group_size)
+
+
+def _all_gather_rows(t: torch.Tensor, group, group_size: int) -> torch.Tensor:
     out = torch.empty((group_size * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
     if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+        # the planes are int16 tensors holding binary16 bits; NCCL has no 16-bit integer type, so
+        # move them as float16 (an all-gather copies bytes, it never interprets them)
+        src, dst = t.contiguous(), out
+        if t.dtype == torch.int16:
+            src, dst = src.view(torch.float16), out.view(torch.float16)
+        dist.all_gather_into_tensor(dst, src, group=group)
     else:   # gloo (CPU tests): no 16-bit integer support, move the bytes
         src = t.contiguous().view(torch.uint8)
         parts = list(out.view(torch.uint8).chunk(group_size, 0))

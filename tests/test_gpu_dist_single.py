@@ -84,3 +84,16 @@ def test_gemm_planes_column_pieces_equal_whole():
     torch.cuda.synchronize()
     assert torch.isfinite(C).all()
     assert float((C.double() - whole.double()).norm() / whole.double().norm()) < 1e-6
+
+
+def test_nccl_plane_all_gather_dtype(nccl_one_rank):
+    """the plane all-gather runs through NCCL with int16 plane tensors (moved as float16 bytes:
+    NCCL has no int16) and keeps every bit pattern, NaN / Inf payloads included"""
+    import torch.distributed as dist
+
+    from paper_2011_11188_b200.dist import _all_gather_rows
+
+    bits = torch.arange(-32768, 32768, dtype=torch.int32, device="cuda").to(torch.int16).view(256, 256)
+    out = _all_gather_rows(bits, dist.group.WORLD, 1)
+    torch.cuda.synchronize()
+    assert out.dtype == torch.int16 and torch.equal(out, bits)
