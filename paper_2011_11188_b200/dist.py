@@ -136,7 +136,7 @@ class CudaOps:
 
 def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, groups=None,
              out: torch.Tensor | None = None, four_term=False, one_term=False, overlap: bool = True,
-             on_block=None):
+             on_block=None, streams: bool | None = None):
     """One rank's share of C = A*B.  A_blk: its (M/P) x K block of A; B_blk: its K x (N/P)
     block of B.  Returns the rank's m x n C tile (see the module docstring).
 
@@ -148,6 +148,8 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
 
     on_block(rows): called after the GEMM of each row block of the tile is enqueued (rows = a
     slice of `out`'s rows), e.g. to copy that part of C out while the next block computes.
+    streams: gather on a side stream (default: with NCCL only; True also with gloo + CUDA
+    tensors — tests of the stream schedule on one GPU).
     """
     world = dist.get_world_size()
     rank = dist.get_rank()
@@ -169,7 +171,8 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
     a_hi, a_lo, sA = ops.split(A_blk, mx[0:1], False)
     b_hi, b_lo, sB = ops.split(B_blk, mx[1:2], True)
     rowblocks = overlap and pc > 1
-    use_streams = rowblocks and dev.type == "cuda" and dist.get_backend() == "nccl"
+    use_streams = rowblocks and dev.type == "cuda" and (
+        dist.get_backend() == "nccl" if streams is None else bool(streams))
     a_lo2 = a_hi if one_term else a_lo
     b_lo2 = b_hi if one_term else b_lo
     if out is None:
@@ -284,10 +287,12 @@ class TileGemm:
     injectable so the same workload runs on CPU / gloo in tests/test_dist_gloo.py."""
 
     def __init__(self, h, n: int, world: int, rank: int, four_term=False, one_term=False, seed=0,
-                 ops=None, device=None, replicated: bool = False, global_n: int | None = None):
+                 ops=None, device=None, replicated: bool = False, global_n: int | None = None,
+                 streams: bool | None = None):
         from workloads import numpy_matrix, torch_matrix
 
         self.replicated = replicated
+        self.streams = streams
         self.pr, self.pc = grid_for(world)
         # weak scaling: an n x n tile per rank of a (pr*n) x (pc*n) x n product; strong scaling
         # (global_n): the global_n^3 product cut into pr x pc tiles (SURVEY §8d config D5)
@@ -329,7 +334,7 @@ class TileGemm:
                                       on_block=on_block)
         else:
             res = sgemm_2d(self.A_blk, self.B_blk, self.M, self.N, self.ops, self.groups, out=self.C,
-                           four_term=self.four, one_term=self.one, on_block=on_block)
+                           four_term=self.four, one_term=self.one, on_block=on_block, streams=self.streams)
         if l0 is not None:
             self._last_launches = self.ops.launches - l0
         return res

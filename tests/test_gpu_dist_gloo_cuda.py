@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, replicated, q):
+def _worker(rank, world, port, n, replicated, q, streams=None):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -34,7 +34,7 @@ def _worker(rank, world, port, n, replicated, q):
 
         torch.cuda.set_device(0)
         h = s3.Handle(0)
-        tg = d2.TileGemm(h, n, world, rank, seed=7, replicated=replicated)
+        tg = d2.TileGemm(h, n, world, rank, seed=7, replicated=replicated, streams=streams)
         tile = tg.run().cpu()
         torch.cuda.synchronize()
         r0, r1, c0, c1 = d2.c_tile(tg.M, tg.N, world, rank)
@@ -57,12 +57,15 @@ def _worker(rank, world, port, n, replicated, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,replicated", [(2, False), (4, False), (4, True)])
-def test_tile_driver_real_kernels(world, replicated):
+@pytest.mark.parametrize("world,replicated,streams", [(2, False, None), (4, False, None), (4, True, None),
+                                                     (2, False, True), (4, False, True)])
+def test_tile_driver_real_kernels(world, replicated, streams):
+    """streams=True: the side-stream schedule the NCCL path uses (gathers on a communication
+    stream, own-rows / own-columns pieces first, events and record_stream), here over gloo"""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, 1024, replicated, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 1024, replicated, q, streams)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
