@@ -35,13 +35,16 @@ def parse():
     p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="split3", choices=["split3", "reference"])
-    p.add_argument("--n", type=int, default=16384)
+    p.add_argument("--n", "--size", dest="n", type=int, default=16384)
     p.add_argument("--terms", type=int, default=3, choices=[1, 3, 4])
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--force-dist", action="store_true",
                    help="test only: run the 2-D tile path (NCCL) even with one rank")
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                   help="rehearsal only: gloo runs every rank on cuda:0 (checks the N > 1 flow on one GPU; "
+                        "not a measurement)")
     p.add_argument("--global-n", type=int, default=0,
                    help="strong scaling: one global_n^3 product cut into 2-D tiles (config D5, e.g. 65536)")
     p.add_argument("--inputs", default="sharded", choices=["sharded", "replicated"],
@@ -300,12 +303,16 @@ def main():
     from paper_2011_11188_b200 import split3 as s3
     from workloads import torch_matrix
 
+    if args.dist_backend == "gloo":
+        local = 0                           # rehearsal: all ranks share cuda:0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if use_dist:
         import torch.distributed as dist
 
-        if "RANK" in os.environ:
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+        elif "RANK" in os.environ:
             dist.init_process_group("nccl", device_id=dev)
         else:   # one process without a launcher (--force-dist / --global-n on one GPU)
             dist.init_process_group("nccl", store=dist.HashStore(), world_size=1, rank=0, device_id=dev)
@@ -500,6 +507,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if args.global_n else "weak", "vs_baseline": None, "dtype": "f16",
             "data": "synthetic", "config": workload_config(args, world),
+            **({"rehearsal": "gloo, every rank on cuda:0: checks the N > 1 flow, not a measurement"}
+               if args.dist_backend == "gloo" else {}),
             "frac_of_peak_over_3": value / world / (pk["tc_burst"] / n_prod),
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
