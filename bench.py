@@ -37,7 +37,7 @@ def parse():
     p.add_argument("--impl", default="split3", choices=["split3", "reference"])
     p.add_argument("--n", "--size", dest="n", type=int, default=16384)
     p.add_argument("--terms", type=int, default=3, choices=[1, 3, 4])
-    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--force-dist", action="store_true",
