@@ -45,8 +45,11 @@ def parse():
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                    help="rehearsal only: gloo runs every rank on cuda:0 (checks the N > 1 flow on one GPU; "
                         "not a measurement)")
-    p.add_argument("--global-n", type=int, default=0,
-                   help="strong scaling: one global_n^3 product cut into 2-D tiles (config D5, e.g. 65536)")
+    p.add_argument("--global-n", type=int, default=None,
+                   help="strong scaling: one global_n^3 product cut into 2-D tiles (config D5); default "
+                        "65536 when N > 1 (BASELINE configs[4]), off at N = 1 (configs[1], --n)")
+    p.add_argument("--weak", action="store_true",
+                   help="N > 1: weak scaling instead (each rank one --n sized tile of a (pr*n) x (pc*n) x n product)")
     p.add_argument("--inputs", default="sharded", choices=["sharded", "replicated"],
                    help="N > 1: inputs start sharded (plane all-gathers) or replicated on every rank")
     p.add_argument("--cpu-target-s", type=float, default=12.0)
@@ -165,6 +168,17 @@ class ClockSampler:
                 "samples": len(sm), "source": "nvidia-smi 100 ms", "reasons": sorted(reasons)}
 
 
+def split_kernels_ncu():
+    """Per-kernel GB/s and DRAM bytes of the split phase's kernels from the committed ncu capture
+    (profiles/split_kernels.json; ncu times are cold-cache, serialised launches)."""
+    path = os.path.join(ROOT, "profiles", "split_kernels.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 # ------------------------------------------------------------- cpu oracle -----
 def cpu_oracle_sample(A_host: np.ndarray, B_host: np.ndarray, terms: int, target_s: float, C_gpu=None):
     """Time oracle.sgemm_sampled on R x R sampled outputs of the full-size problem.  With the
@@ -214,11 +228,55 @@ def cpu_oracle_sample(A_host: np.ndarray, B_host: np.ndarray, terms: int, target
                "E64": float(np.sqrt(scale) * np.linalg.norm(Cg - C64) / (nA * nB)),
                "samples": f"{len(rows)}x{len(cols)} outputs of the timed run's C",
                "tolerances": {"E_or": 1e-6, "E64": 2e-6}}
+    try:
+        phases = cpu_phases(A_host, B_host)
+    except Exception as ex:   # reported, never silently replaced
+        phases = {"error": repr(ex)}
     return {"value": flops / dt / 1e12, "unit": "TFLOPS", "cores": oracle.num_threads(),
+            "cpu_model": cpu_model(), "phases": phases,
             "kind": "oracle", "seconds": dt, "accuracy": acc,
             "sample": f"{R}x{R} sampled outputs of the {A_host.shape[0]}x{Nc}x{K} product "
                       f"(fp64 oracle: full-matrix max-abs, split of the sampled rows/cols, "
                       f"{terms}-term Eq. A_2); value = 2*R*R*K / time"}
+
+
+def cpu_model() -> str | None:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_phases(A_host: np.ndarray, B_host: np.ndarray) -> dict:
+    """Per-phase rates of the oracle on the host cores: encode (max-abs + split,
+    ns per element, on a 2048 x 2048 block of A), the FP64 reference GEMM and the split
+    emulation (Eq. A_2 on the decoded planes, 3 terms) on a 512 x 512 x 2048 sub-problem."""
+    import oracle
+
+    out = {}
+    n = min(2048, A_host.shape[0], A_host.shape[1])
+    X = np.ascontiguousarray(A_host[:n, :n])
+    t = time.perf_counter()
+    m, _ = oracle.maxabs(X)
+    hi, lo, s = oracle.split(X, s=oracle.scale_exp(m))
+    out["encode_ns_per_el"] = (time.perf_counter() - t) / X.size * 1e9
+    r, k = min(512, n), n
+    a = np.ascontiguousarray(A_host[:r, :k])
+    b = np.ascontiguousarray(B_host[:k, :r])
+    t = time.perf_counter()
+    oracle.gemm64(a, b)
+    out["gemm64_gflops"] = 2.0 * r * r * k / (time.perf_counter() - t) / 1e9
+    ah, al, sa = oracle.split(a)
+    bh, bl, sb = oracle.split(b)
+    t = time.perf_counter()
+    oracle.split_gemm(ah, al, sa, bh, bl, sb, terms=3)
+    out["split_emulation_gflops"] = 2.0 * r * r * k / (time.perf_counter() - t) / 1e9
+    out["sub_problem"] = f"encode {n}x{n}; GEMMs {r}x{r}x{k}"
+    return out
 
 
 # ------------------------------------------------------------ reference arm ---
@@ -228,33 +286,58 @@ def run_reference(args, rank, world):
     import oracle
     from workloads import numpy_matrix
 
-    n = args.n
-    # the oracle's own inputs (same recipe as the GPU arm: uniform[-1,1], seeds 0/1)
-    A = numpy_matrix("uniform", n, n, seed=0)
-    B = numpy_matrix("uniform", n, n, seed=1)
     per_step_target = max(2.0, min(20.0, 150.0 / max(args.steps + args.warmup, 1)))
-    info = cpu_oracle_sample(A, B, args.terms, per_step_target)
-    R = int(info["sample"].split("x")[0])
-    rng = np.random.Generator(np.random.PCG64(99))
     times = []
-    for i in range(args.warmup + args.steps):
-        rows = np.sort(rng.choice(n, R, replace=False))
-        cols = np.sort(rng.choice(n, R, replace=False))
+    if args.global_n:
+        # config D5 (N = 65536): the full matrices (16 GiB each) would make every oracle step pay two
+        # full-matrix max-abs passes (minutes); each step is instead the oracle's whole method on an
+        # R x K row sample of A and a K x R column sample of B drawn from the same distribution
+        # (scales from the sample), i.e. R x R outputs of a 65536-deep product
+        n = args.global_n
+        R = 64
+        A = numpy_matrix("uniform", R, n, seed=0)
+        B = numpy_matrix("uniform", n, R, seed=1)
         t = time.perf_counter()
-        oracle.sgemm_sampled(A, B, rows, cols, terms=args.terms)
-        dt = time.perf_counter() - t
-        if i >= args.warmup:
-            times.append(dt)
+        oracle.sgemm(A, B, terms=args.terms)
+        t1 = time.perf_counter() - t
+        R = int(max(16, min(2048, R * np.sqrt(per_step_target / max(t1, 1e-6)))))
+        A = numpy_matrix("uniform", R, n, seed=0)
+        B = numpy_matrix("uniform", n, R, seed=1)
+        for i in range(args.warmup + args.steps):
+            t = time.perf_counter()
+            oracle.sgemm(A, B, terms=args.terms)
+            dt = time.perf_counter() - t
+            if i >= args.warmup:
+                times.append(dt)
+        sample = (f"{R}x{n} rows of A and {n}x{R} columns of B (uniform[-1,1], scales of the sample): "
+                  f"{R}x{R} outputs of the {n}^3 product per step")
+    else:
+        n = args.n
+        # the oracle's own inputs (same recipe as the GPU arm: uniform[-1,1], seeds 0/1)
+        A = numpy_matrix("uniform", n, n, seed=0)
+        B = numpy_matrix("uniform", n, n, seed=1)
+        info = cpu_oracle_sample(A, B, args.terms, per_step_target)
+        R = int(info["sample"].split("x")[0])
+        rng = np.random.Generator(np.random.PCG64(99))
+        for i in range(args.warmup + args.steps):
+            rows = np.sort(rng.choice(n, R, replace=False))
+            cols = np.sort(rng.choice(n, R, replace=False))
+            t = time.perf_counter()
+            oracle.sgemm_sampled(A, B, rows, cols, terms=args.terms)
+            dt = time.perf_counter() - t
+            if i >= args.warmup:
+                times.append(dt)
+        sample = info["sample"] + " per step"
     t_total = sum(times)
     value = 2.0 * R * R * n * len(times) / t_total / 1e12
     line = {
         "impl": "reference", "metric": "split-FP16 SGEMM effective TFLOPS (2MNK/t)",
         "value": value, "unit": "TFLOPS", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_total / max(len(times), 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(args, world),
+        "higher_is_better": True, "scaling": "strong" if args.global_n else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": workload_config(args, world),
         "cpu_baseline": {"value": value, "unit": "TFLOPS", "cores": oracle.num_threads(),
-                         "kind": "oracle", "sample": info["sample"] + " per step"},
+                         "kind": "oracle", "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -294,8 +377,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
+        if args.global_n is None:
+            args.global_n = 65536 if (world > 1 and not args.weak) else 0
         run_reference(args, rank, world)
         return
+    if args.global_n is None:   # N > 1: config D5 (N = 65536, strong scaling) unless --weak
+        args.global_n = 65536 if (world > 1 and not args.weak) else 0
     use_dist = world > 1 or args.force_dist or args.global_n > 0
 
     import torch
@@ -388,18 +475,26 @@ def main():
     achieved = n_prod * 2.0 * M_loc * N_loc * K / (gemm_step_ms / 1e3) / 1e12 if ncalls else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "gemm3_traffic.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and not use_dist:
         try:
             with open(prof) as f:
                 traffic = json.load(f)["bytes_per_launch"].get(str(n), {}).get(str(args.terms))
         except Exception:
             traffic = None
+    # the peak for the timed region's length: the burst figure for a region shorter than the
+    # 4-s back-to-back loop MEASURED_PEAKS' sustained figure comes from, else the sustained one
+    long_region = t_ms >= 4000.0
+    peak = pk["tc_sustained"] if long_region else pk["tc_burst"]
     roofline = {"bound": "tensor", "kernel": "gemm3_kernel", "achieved": achieved,
-                "peak": pk["tc_sustained"], "unit": "TFLOP/s",
-                "frac": (achieved / pk["tc_sustained"]) if achieved else None,
+                "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if achieved else None,
                 "traffic": traffic,
-                "peak_src": f"{pk['src']} bf16_tflops_sustained (fp16 = bf16 nominal rate)",
+                "peak_src": f"{pk['src']} bf16_tflops{'_sustained' if long_region else ''} "
+                            f"(timed region {t_ms / 1e3:.2f} s; fp16 = bf16 nominal rate)",
                 "frac_of_burst": (achieved / pk["tc_burst"]) if achieved else None,
+                "frac_of_sustained": (achieved / pk["tc_sustained"]) if achieved else None,
+                "frac_of_datasheet": (achieved / 2250.0) if achieved else None,
+                "split_kernels_ncu": split_kernels_ncu(),
                 "gemm_share_of_step": gemm_ms / max(t_ms, 1e-9) if ncalls else None,
                 "gemm_launches_per_step": ncalls / args.steps,
                 "split_ms_per_step": split_ms / args.steps if not use_dist else None,
@@ -510,6 +605,7 @@ def main():
             **({"rehearsal": "gloo, every rank on cuda:0: checks the N > 1 flow, not a measurement"}
                if args.dist_backend == "gloo" else {}),
             "frac_of_peak_over_3": value / world / (pk["tc_burst"] / n_prod),
+            "frac_of_datasheet_peak_over_3": value / world / (2250.0 / n_prod),
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "sustained": sustained,

@@ -83,7 +83,8 @@ int split3_sgemm_destroy(split3_handle_t h);
  * region fits either its K-major N x K planes or the MN-major K x N planes a row-major B is split
  * into) and,
  * when the problem has fewer 256-wide C tiles than CTA pairs, S*M*N floats of split-K partials
- * (S <= 16 slices of K, reduced in a fixed order: results are deterministic). */
+ * (S <= 16 slices of K, reduced in a fixed order: results are deterministic), sized for the
+ * largest plan over every GEMM SM count up to 148 (split3_set_max_sms). */
 size_t split3_sgemm_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags);
 
 /* Attach caller-owned device workspace (256-byte aligned).  The handle keeps the pointer;
@@ -164,6 +165,12 @@ typedef struct split3_matrix {
  * linear index in the STORED fp32 matrix (A first, then M*K + index in B). */
 int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const split3_matrix *A,
                     const split3_matrix *B, float *C, int64_t ldc, uint32_t flags);
+
+/* Workspace bytes split3_sgemm_ex needs when A and/or B are given pre-split (a_presplit,
+ * b_presplit != 0): with both pre-split only the 256-byte scalars block and the split-K partials
+ * (none if split3_set_split_k(h, 0)); otherwise split3_sgemm_workspace_size(M, N, K, flags). */
+size_t split3_sgemm_ex_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags, int a_presplit,
+                                      int b_presplit);
 
 /* Split an operand once for reuse (a1 + a2 on one matrix, Eq. A_1, scale rule R1).  role 0: op(X)
  * is an A operand, rows x cols = M x K, planes M x K; role 1: op(X) is a B operand, rows x cols =
@@ -265,6 +272,24 @@ int split3_set_wave_sync(split3_handle_t h, int enable);
  * eviction policy of the A-plane and B-plane TMA loads (0 normal, 1 evict_first, 2 evict_last).
  * Scheduling only: results are identical for every setting. */
 int split3_set_schedule(split3_handle_t h, int group_m, int l2_policy_a, int l2_policy_b);
+
+/* Split-K tail (default on): when the last wave of 256-wide C tiles is partial (or there are fewer
+ * tiles than CTA pairs), those tiles are cut along K into S <= 16 slices whose FP32 partials are
+ * summed in a fixed slice order (deterministic, but another summation order than a whole tile).
+ * enable = 0: whole tiles only — every C element is then accumulated over K in the same order
+ * whatever the shape of the problem it belongs to, so a C piece computed by split3_gemm_planes
+ * (the multi-GPU driver's pieces, always whole tiles) and the same rows/columns of one
+ * split3_sgemm call are bitwise equal (SURVEY §8e invariant; tests/test_gpu_dist_gloo_cuda.py).
+ * Scheduling only for the numerics contract: both modes meet the oracle tolerance. */
+int split3_set_split_k(split3_handle_t h, int enable);
+
+/* Cap on the SMs the persistent GEMM occupies (0 = all, else an even count >= 2; counts above
+ * the device's are ignored).  The multi-GPU driver leaves SMs free this way while its plane
+ * all-gathers run on another stream: the GEMM holds ~225 KB of shared memory per SM, so a
+ * collective kernel finds no SM to run on until a full-width GEMM drains.  Results are
+ * identical for every cap with split-K off; with split-K on the tail plan depends on the cap.
+ * INVALID_VALUE for an odd or negative count. */
+int split3_set_max_sms(split3_handle_t h, int sms);
 
 /* Fused split of B (Eq. A_1, applied inside the GEMM): for a
  * 3-term call whose B is an fp32 matrix (not pre-split; row-major K x N, or stored N x K with

@@ -31,6 +31,8 @@ struct split3_ctx {
     int last_launches = 0;
     int promo_kb = 0;   // 0 = library default
     int wave_sync = 1;  // GEMM wave lockstep hint (L2 locality)
+    int split_k = 1;    // split-K tail for partial last waves (0: whole tiles only, split3_set_split_k)
+    int max_sms = 0;    // SMs the GEMM may occupy (0: all; split3_set_max_sms)
     int prep_ok = 1;    // the cooperative one-launch front end is accepted (cleared on rejection)
     int64_t prep_max = split3::kPrepMaxElems;   // elements of A + B up to which it is used (env SPLIT3_PREP_MAX)
     int mn_major = 1;   // MN-major planes for a row-major B / a transposed A (no transposing split);
@@ -122,15 +124,23 @@ Carve carve(void* ws, int64_t M, int64_t N, int64_t K) {
     return c;
 }
 
+// Split-K partials the workspace reserves: the largest plan over every SM count up to kMaxSms (a
+// handle may run its GEMM on fewer SMs: split3_set_max_sms, MIG, green contexts), so the plan a
+// call makes always fits; a device with more SMs would fall back to whole tiles (not sm_100).
+constexpr int kMaxSms = 148;
+int64_t partial_elems_bound(int64_t M, int64_t N, int64_t K, int terms) {
+    int64_t mx = 0;
+    for (int sms = 2; sms <= kMaxSms; sms += 2)
+        mx = std::max(mx, split3::gemm3_partial_elems(split3::gemm3_split_plan(M, N, K, terms, sms, 0), terms));
+    return mx;
+}
+
 size_t ws_bytes_for(int64_t M, int64_t N, int64_t K, bool planesA, bool planesB, int terms_for_partials) {
     if (M < 0 || N < 0 || K < 0) return 0;
     (void)planesA; (void)planesB;   // plane regions are always carved (fixed layout)
     size_t b = kScalarBytes + 2 * align256(std::max((size_t)M * (size_t)plane_ld(K), (size_t)K * (size_t)plane_ld(M)) * 2) +
                2 * align256(std::max((size_t)N * (size_t)plane_ld(K), (size_t)K * (size_t)plane_ld(N)) * 2);
-    if (terms_for_partials) {
-        const split3::SplitPlan p = split3::gemm3_split_plan(M, N, K, terms_for_partials, 148, 0);
-        b += align256((size_t)split3::gemm3_partial_elems(p, terms_for_partials) * 4);
-    }
+    if (terms_for_partials) b += align256((size_t)partial_elems_bound(M, N, K, terms_for_partials) * 4);
     return b;
 }
 
@@ -158,7 +168,7 @@ CarveBF3 carve_bf3(void* ws, int64_t M, int64_t N, int64_t K) {
 size_t ws_bytes_bf3(int64_t M, int64_t N, int64_t K, bool partials) {
     size_t b = kScalarBytes + 3 * align256(std::max((size_t)M * (size_t)plane_ld(K), (size_t)K * (size_t)plane_ld(M)) * 2) +
                3 * align256(std::max((size_t)N * (size_t)plane_ld(K), (size_t)K * (size_t)plane_ld(N)) * 2);
-    if (partials) b += align256((size_t)split3::gemm3_partial_elems(split3::gemm3_split_plan(M, N, K, 6, 148, 0), 6) * 4);
+    if (partials) b += align256((size_t)partial_elems_bound(M, N, K, 6) * 4);
     return b;
 }
 
@@ -173,6 +183,11 @@ inline int terms_of(uint32_t flags) {
 
 int set_dev(split3_ctx* h) {
     return cudaSetDevice(h->device) == cudaSuccess ? SPLIT3_OK : SPLIT3_ERR_CUDA;
+}
+
+// SMs the GEMM's persistent grid may occupy (split3_set_max_sms; an even count, >= 2)
+int gemm_sms(const split3_ctx* h) {
+    return h->max_sms > 0 && h->max_sms < h->num_sms ? h->max_sms : h->num_sms;
 }
 
 }  // namespace
@@ -206,8 +221,17 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
     c->stream = static_cast<cudaStream_t>(cuda_stream);
-    if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(&c->d_counters, kCounterBytes) != cudaSuccess ||
-        cudaMemset(c->d_counters, 0, kCounterBytes) != cudaSuccess) {
+    // creation may happen while another stream of this thread is being captured into a CUDA graph
+    // (a binding creating the handle of a new stream lazily): relaxed mode lets the allocation and
+    // the synchronous zeroing of the handle's counters through
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    const bool ok = cudaSetDevice(device) == cudaSuccess && cudaMalloc(&c->d_counters, kCounterBytes) == cudaSuccess &&
+                    cudaMemset(c->d_counters, 0, kCounterBytes) == cudaSuccess &&
+                    cudaStreamSynchronize(cudaStreamLegacy) == cudaSuccess;   // zeroed before any stream uses it
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    if (!ok) {
+        if (c->d_counters) cudaFree(c->d_counters);
         delete c;
         return SPLIT3_ERR_CUDA;
     }
@@ -250,6 +274,13 @@ size_t split3_sgemm_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t fla
     if (M < 0 || N < 0 || K < 0) return 0;
     if (flags & SPLIT3_BF16X3) return ws_bytes_bf3(M, N, K, true);
     return ws_bytes_for(M, N, K, true, true, terms_of(flags));
+}
+
+size_t split3_sgemm_ex_workspace_size(int64_t M, int64_t N, int64_t K, uint32_t flags, int a_presplit,
+                                      int b_presplit) {
+    if (M < 0 || N < 0 || K < 0) return 0;
+    if (!(a_presplit && b_presplit) || (flags & SPLIT3_BF16X3)) return split3_sgemm_workspace_size(M, N, K, flags);
+    return kScalarBytes + align256((size_t)partial_elems_bound(M, N, K, terms_of(flags)) * 4);
 }
 
 int split3_sgemm_set_workspace(split3_handle_t h, void* dptr, size_t bytes) {
@@ -339,7 +370,7 @@ int split3_gemm_planes(split3_handle_t h, int64_t M, int64_t N, int64_t K, const
     }
     int err = 0;
     int n = split3::launch_gemm3(h->stream, M, N, K, A1, A2, ldpa, d_sA, B1t, B2t, ldpb, d_sB, C,
-                                 ldc, terms, h->num_sms, h->promo_kb,
+                                 ldc, terms, gemm_sms(h), h->promo_kb,
                                  h->wave_sync ? h->d_counters : nullptr, h->tune, nullptr, 0, &err);
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
@@ -434,8 +465,9 @@ static int sgemm_bf16x3(split3_ctx* h, int64_t M, int64_t N, int64_t K, const sp
     if (reserved > h->ws_bytes - w.end) reserved = h->ws_bytes - w.end;
     int err = 0;
     n = split3::launch_gemm3(h->stream, M, N, K, w.A[0], w.A[1], a_mn ? w.ldpa_mn : w.ldp, sc.sA, w.B[0], w.B[1],
-                             b_mn ? w.ldpb_mn : w.ldp, sc.sB, C, ldc, 6, h->num_sms, h->promo_kb,
-                             h->wave_sync ? h->d_counters : nullptr, h->tune, partial, (int64_t)(reserved / 4), &err,
+                             b_mn ? w.ldpb_mn : w.ldp, sc.sB, C, ldc, 6, gemm_sms(h), h->promo_kb,
+                             h->wave_sync ? h->d_counters : nullptr, h->tune, h->split_k ? partial : nullptr,
+                             (int64_t)(reserved / 4), &err,
                              w.A[2], w.B[2], (b_mn ? 1 : 0) | (a_mn ? 2 : 0));
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
@@ -465,7 +497,10 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     if (!h->ws || h->ws_bytes < kScalarBytes) return SPLIT3_ERR_WORKSPACE;
     if (flags & SPLIT3_BF16X3) return sgemm_bf16x3(h, M, N, K, A, B, C, ldc, flags);
     const bool needA = A->hi == nullptr, needB = B->hi == nullptr;
-    const size_t need = ws_bytes_for(M, N, K, needA, needB, 0);
+    // planes carved only when an operand is split here; two pre-split operands need the scalars
+    // block (and split-K partials right after it)
+    const bool planes_ws = needA || needB;
+    const size_t need = planes_ws ? ws_bytes_for(M, N, K, needA, needB, 0) : kScalarBytes;
     if (h->ws_bytes < need) return SPLIT3_ERR_WORKSPACE;
     Carve w = carve(h->ws, M, N, K);
     const bool check = (flags & SPLIT3_CHECK_FINITE) != 0;
@@ -590,14 +625,16 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     // a3 + a4: tensor-core products with the fused epilogue (split-K partials after the planes)
     // split-K partials: only the region split3_sgemm_workspace_size reserves for them (whatever
     // follows it in the workspace may be staging buffers of split3_sgemm_host)
-    float* partial = reinterpret_cast<float*>(static_cast<uint8_t*>(h->ws) + w.end);
-    size_t reserved = ws_bytes_for(M, N, K, true, true, terms) - w.end;
-    if (reserved > h->ws_bytes - w.end) reserved = h->ws_bytes - w.end;
+    const size_t pend = planes_ws ? w.end : kScalarBytes;
+    float* partial = reinterpret_cast<float*>(static_cast<uint8_t*>(h->ws) + pend);
+    size_t reserved = planes_ws ? ws_bytes_for(M, N, K, true, true, terms) - w.end
+                                : align256((size_t)partial_elems_bound(M, N, K, terms) * 4);
+    if (reserved > h->ws_bytes - pend) reserved = h->ws_bytes - pend;
     const int64_t partial_elems = (int64_t)(reserved / 4);
     int err = 0;
     n = split3::launch_gemm3(h->stream, M, N, K, A1, A2, ldpa, sA, B1t, B2t, ldpb, sB, C, ldc, terms,
-                             h->num_sms, h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune, partial,
-                             partial_elems, &err, nullptr, nullptr, (b_mn ? 1 : 0) | (a_mn ? 2 : 0),
+                             gemm_sms(h), h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune,
+                             h->split_k ? partial : nullptr, partial_elems, &err, nullptr, nullptr, (b_mn ? 1 : 0) | (a_mn ? 2 : 0),
                              fuse_b ? B->data : nullptr, B->ld, w.maxB);
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
@@ -732,6 +769,18 @@ int split3_set_schedule(split3_handle_t h, int group_m, int l2_policy_a, int l2_
 int split3_set_wave_sync(split3_handle_t h, int enable) {
     if (!h) return SPLIT3_ERR_INVALID_VALUE;
     h->wave_sync = enable != 0;
+    return SPLIT3_OK;
+}
+
+int split3_set_split_k(split3_handle_t h, int enable) {
+    if (!h) return SPLIT3_ERR_INVALID_VALUE;
+    h->split_k = enable != 0;
+    return SPLIT3_OK;
+}
+
+int split3_set_max_sms(split3_handle_t h, int sms) {
+    if (!h || sms < 0 || sms == 1 || (sms & 1)) return SPLIT3_ERR_INVALID_VALUE;
+    h->max_sms = sms;
     return SPLIT3_OK;
 }
 
@@ -937,7 +986,7 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
         int err = 0;
         // MN-major B planes: columns [c0, c0 + nc) of the K x N planes; K-major (one panel): all
         int r = split3::launch_gemm3(s0, mr, nc, K, w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa, w.ldpa, d_sA, w.B1t + c0,
-                                     w.B2t + c0, ldpb, d_sB, dC + r0 * N + c0, N, terms_of(flags), h->num_sms,
+                                     w.B2t + c0, ldpb, d_sB, dC + r0 * N + c0, N, terms_of(flags), gemm_sms(h),
                                      h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune, nullptr, 0, &err,
                                      nullptr, nullptr, b_mn ? 1 : 0);
         return r < 0 ? -(err ? err : SPLIT3_ERR_CUDA) : r;

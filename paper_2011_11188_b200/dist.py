@@ -13,13 +13,15 @@ One step (the only exchanges are 2 floats and the plane panels; there is no redu
   1. a1 local max-abs of the owned A block and B block;
   2. all_reduce(MAX) of [maxA, maxB] over all ranks: the global per-matrix scale (reading R1;
      max is exact and order-free, so every rank derives the same sA, sB as one GPU would);
-  3. a2 local split of the owned blocks with the global scale (B's block transposed: N/P x K);
-  4. all_gather of the FP16 planes: A planes over the row group -> an m x K panel; B^T planes
-     over the column group -> an n x K panel (B's column blocks are row blocks of B^T, so the
-     gather concatenates contiguously);
-  5. a3+a4 the local tcgen05 GEMM on the m x n tile.
-With m and n multiples of the GEMM tile (128), every C element is computed by the same kernel
-over the same K order as on one GPU: the P-GPU C equals the 1-GPU C bitwise.
+  3. a2 local split of the owned blocks with the global scale (plain splits: A's block into
+     K-major (M/P) x K planes, B's block into MN-major K x (N/P) planes);
+  4. all_gather of the FP16 planes: A planes over the row group -> the m x K panel; B planes over
+     the column group -> pr stacked K x (N/P) blocks (the column panel, block by block);
+  5. a3+a4 the local tcgen05 GEMMs: one piece per (A row block, B column block) of the tile.
+Every piece is a GEMM over whole tiles (CudaOps turns split-K off), and an element of C is
+accumulated over K in the same order whatever piece or problem it belongs to, so the P-GPU C
+equals the 1-GPU split3_sgemm C (split-K off) bitwise — tested with the real kernels at world 2
+and 4 (tests/test_gpu_dist_gloo_cuda.py), besides the oracle tolerance.
 
 Replicated inputs (every rank holds all of A and B; sgemm_2d_replicated): no plane exchange.
 Rank (i, j) reads only its A row panel and B column panel — their max-abs, all_reduce(MAX) over
@@ -80,11 +82,30 @@ def c_tile(M: int, N: int, world: int, rank: int) -> tuple[int, int, int, int]:
     return i * m, (i + 1) * m, j * n, (j + 1) * n
 
 
-def make_groups(world: int):
-    """Row groups and column groups (every rank must call this, in the same order)."""
+_GROUPS: dict = {}
+# CTA budget of the NCCL plane all-gathers (config max_ctas); the GEMM pieces that overlap them run
+# on the SMs left over
+GATHER_CTAS = 8
+
+
+def make_groups(world: int, gather_ctas: int | None = None):
+    """Row groups and column groups (every rank must call this, in the same order).  Cached per
+    (default process group, world, gather_ctas): a step loop reuses its communicators.
+    gather_ctas: with NCCL, the CTA budget of the plane all-gathers (NCCL config max_ctas)."""
+    key = (id(dist.group.WORLD), world, gather_ctas)
+    g = _GROUPS.get(key)
+    if g is not None:
+        return g
     pr, pc = grid_for(world)
-    rows = [dist.new_group([i * pc + j for j in range(pc)]) for i in range(pr)]
-    cols = [dist.new_group([i * pc + j for i in range(pr)]) for j in range(pc)]
+    kw = {}
+    if gather_ctas and dist.get_backend() == "nccl":
+        opts = dist.ProcessGroupNCCL.Options()
+        opts.config.max_ctas = int(gather_ctas)
+        opts.config.min_ctas = 1
+        kw["pg_options"] = opts
+    rows = [dist.new_group([i * pc + j for j in range(pc)], **kw) for i in range(pr)]
+    cols = [dist.new_group([i * pc + j for i in range(pr)], **kw) for j in range(pc)]
+    _GROUPS[key] = (rows, cols)
     return rows, cols
 
 
@@ -112,24 +133,44 @@ def _all_gather_rows(t: torch.Tensor, group, group_size: int) -> torch.Tensor:
 
 
 class CudaOps:
-    """The product's local steps: the CUDA library through its binding."""
+    """The product's local steps: the CUDA library through its binding.
 
-    def __init__(self, h):
+    The handle runs whole tiles only (split3_set_split_k(h, 0)): every C element is accumulated
+    over K in the same order as in a one-GPU split3_sgemm call with split-K off, so the 2-D
+    partition reproduces that call's C bitwise (SURVEY §8e invariant).  gemm_sms_during_gather:
+    the SM budget of the GEMM pieces that run while plane all-gathers are in flight (the rest is
+    left to the gather kernels; the full-width GEMM holds ~225 KB of shared memory per SM)."""
+
+    def __init__(self, h, gemm_sms_during_gather: int = 0):
         self.h = h
         self.launches = 0          # library kernels launched through these ops (NCCL's not counted)
+        self.gather_sms = int(gemm_sms_during_gather)
+        h.set_split_k(False)
 
     def maxabs_into(self, X, d_max1):
         self.h.maxabs(X, d_max1)
         self.launches += self.h.last_launch_count()
 
-    def split(self, X, d_max1, transpose):
-        hi, lo, sexp = self.h.split(X, d_max1, transpose=transpose)
+    def split(self, X, d_max1):
+        """plain split of the stored block (no transpose): A rows -> K-major M x K planes,
+        B columns -> MN-major K x N planes"""
+        hi, lo, sexp = self.h.split(X, d_max1, transpose=False)
         self.launches += self.h.last_launch_count()
         return hi, lo, sexp
 
-    def gemm(self, m, n, K, A1, A2, sA, B1t, B2t, sB, out, four_term, one_term):
-        res = self.h.gemm_planes(m, n, K, A1, A2, sA, B1t, B2t, sB, out=out,
-                                 four_term=four_term, one_term=one_term)
+    def gemm(self, m, n, K, A1, A2, sA, B1, B2, sB, out, four_term, one_term, overlapped=False):
+        """C piece (m x n) = A planes (m x K, K-major) times B planes (K x n, MN-major)"""
+        from .split3 import Planes
+
+        if overlapped and self.gather_sms:
+            self.h.set_max_sms(self.gather_sms)
+        try:
+            res = self.h.sgemm_ex(Planes(A1, A2, sA, None, m, K, stored=True),
+                                  Planes(B1, B2, sB, None, K, n, stored=True), out=out,
+                                  four_term=four_term, one_term=one_term)
+        finally:
+            if overlapped and self.gather_sms:
+                self.h.set_max_sms(0)
         self.launches += self.h.last_launch_count()
         return res
 
@@ -140,13 +181,18 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
     """One rank's share of C = A*B.  A_blk: its (M/P) x K block of A; B_blk: its K x (N/P)
     block of B.  Returns the rank's m x n C tile (see the module docstring).
 
-    overlap: the rank's own A rows are multiplied first — by its own B block's columns before the
-    B^T panel has landed, then by the rest of the panel — while (NCCL) the panels are all-gathered
-    on a communication stream; the other row blocks follow when the A panel lands.  Each piece is
-    a separate GEMM over whole tiles, so every C element is computed exactly as in the
-    non-overlapped schedule.
+    Planes: A's block -> K-major (M/P) x K planes, gathered over the row group into the m x K
+    panel; B's block -> MN-major K x (N/P) planes (the plain split, no transpose), gathered over the
+    column group into pr stacked K x (N/P) blocks.  The tile is computed as pieces (A row block) x
+    (B column block), each a GEMM over whole tiles written into its slice of `out`.
 
-    on_block(rows): called after the GEMM of each row block of the tile is enqueued (rows = a
+    overlap: the rank's own A rows are multiplied first — by its own B block before the B panel
+    has landed, then by the other blocks of the panel — while (NCCL) the panels are all-gathered
+    on a communication stream; the other row blocks follow when the A panel lands.  Pieces that
+    run under a gather use the ops' reduced SM budget (CudaOps.gather_sms) so the gather kernels
+    find free SMs.
+
+    on_block(rows): called after the GEMMs of each row block of the tile are enqueued (rows = a
     slice of `out`'s rows), e.g. to copy that part of C out while the next block computes.
     streams: gather on a side stream (default: with NCCL only; True also with gloo + CUDA
     tensors — tests of the stream schedule on one GPU).
@@ -162,92 +208,98 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
     dev = A_blk.device
     m, n = M // pr, N // pc
     mb = M // world                      # rows of one A block
+    nbk = N // world                     # columns of one B block
     # 1-2: global max-abs of A and B (exact, order-free)
     mx = torch.zeros(2, dtype=torch.float32, device=dev)
     ops.maxabs_into(A_blk, mx[0:1])
     ops.maxabs_into(B_blk, mx[1:2])
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-    # 3: local split with the global scale
-    a_hi, a_lo, sA = ops.split(A_blk, mx[0:1], False)
-    b_hi, b_lo, sB = ops.split(B_blk, mx[1:2], True)
-    rowblocks = overlap and pc > 1
-    use_streams = rowblocks and dev.type == "cuda" and (
-        dist.get_backend() == "nccl" if streams is None else bool(streams))
+    # 3: local split with the global scale (plain splits: A K-major, B MN-major)
+    a_hi, a_lo, sA = ops.split(A_blk, mx[0:1])
+    b_hi, b_lo, sB = ops.split(B_blk, mx[1:2])
     a_lo2 = a_hi if one_term else a_lo
     b_lo2 = b_hi if one_term else b_lo
     if out is None:
         out = torch.empty((m, n), dtype=torch.float32, device=dev)
+    exchange = pr > 1 or pc > 1
+    use_streams = overlap and exchange and dev.type == "cuda" and (
+        dist.get_backend() == "nccl" if streams is None else bool(streams))
 
     def put(dst, res):
         if res is not None and res.data_ptr() != dst.data_ptr():
             dst.copy_(res)
 
-    if not rowblocks:
-        # 4 + 5: both panels, then one GEMM on the whole tile
-        B1t = _gather_rows(b_hi, col_groups[j], pr)
-        B2t = B1t if one_term else _gather_rows(b_lo, col_groups[j], pr)
+    def gather_b():
+        B1 = _gather_rows(b_hi, col_groups[j], pr)
+        return B1, (B1 if one_term else _gather_rows(b_lo, col_groups[j], pr))
+
+    def gather_a():
         A1 = _gather_rows(a_hi, row_groups[i], pc)
-        A2 = A1 if one_term else _gather_rows(a_lo, row_groups[i], pc)
-        put(out, ops.gemm(m, n, K, A1, A2, sA, B1t, B2t, sB, out, four_term, one_term))
+        return A1, (A1 if one_term else _gather_rows(a_lo, row_groups[i], pc))
+
+    def bblock(P1, P2, q):               # B block q of the gathered panel: K x nbk planes
+        return P1[q * K:(q + 1) * K], P2[q * K:(q + 1) * K]
+
+    def row_block(rs, A1r, A2r, B1, B2, overlapped):
+        """C[rs, :] = A rows x each B block of the column panel"""
+        for q in range(pr):
+            cs = slice(q * nbk, (q + 1) * nbk)
+            b1, b2 = bblock(B1, B2, q)
+            put(out[rs, cs], ops.gemm(A1r.shape[0], nbk, K, A1r, A2r, sA, b1, b2, sB, out[rs, cs],
+                                      four_term, one_term, overlapped=overlapped))
         if on_block is not None:
-            on_block(slice(0, m))
+            on_block(rs)
+
+    if not overlap or not exchange:
+        # 4 + 5: both panels, then the pieces
+        B1, B2 = gather_b()
+        A1, A2 = gather_a()
+        for q in range(pc):
+            rs = slice(q * mb, (q + 1) * mb)
+            row_block(rs, A1[rs], A2[rs], B1, B2, False)
         return out
-    # 4 under 5: the B^T panel and then the A panel are gathered on a communication stream (NCCL)
+    # 4 under 5: the B panel and then the A panel are gathered on a communication stream (NCCL)
     # while the compute stream multiplies what is already local — the own A rows times the own
-    # B block's columns first (no exchange at all), then the own rows times the other B blocks of
-    # the column panel, then the other row blocks of the A panel.  Every piece is a GEMM over whole
-    # tiles (block widths are multiples of the tile), so C is the same as without the overlap.
+    # B block first (no exchange at all), then times the other B blocks of the column panel, then
+    # the other row blocks of the A panel.  Every piece is a GEMM over whole tiles, so C is the
+    # same as without the overlap.
     compute = torch.cuda.current_stream(dev) if use_streams else None
     comm = torch.cuda.Stream(device=dev) if use_streams else None
     if use_streams:
         comm.wait_stream(compute)
         with torch.cuda.stream(comm):
-            B1t = _gather_rows(b_hi, col_groups[j], pr)
-            B2t = B1t if one_term else _gather_rows(b_lo, col_groups[j], pr)
+            B1, B2 = gather_b()
             ev_b = torch.cuda.Event()
             ev_b.record(comm)
-            A1 = _gather_rows(a_hi, row_groups[i], pc)
-            A2 = A1 if one_term else _gather_rows(a_lo, row_groups[i], pc)
-
-    def panel_b():
-        nonlocal B1t, B2t
-        if use_streams:
-            compute.wait_event(ev_b)
-        else:
-            B1t = _gather_rows(b_hi, col_groups[j], pr)
-            B2t = B1t if one_term else _gather_rows(b_lo, col_groups[j], pr)
-
+            A1, A2 = gather_a()
     own = slice(j * mb, (j + 1) * mb)
-    if pr > 1:
-        nbk = n // pr                         # columns of one B block in the column panel
-        oc = slice(i * nbk, (i + 1) * nbk)    # this rank's own block (position i in the panel)
-        put(out[own, oc], ops.gemm(mb, nbk, K, a_hi, a_lo2, sA, b_hi, b_lo2, sB, out[own, oc], four_term, one_term))
-        panel_b()
-        for q in range(pr):
-            if q == i:
-                continue
-            cs = slice(q * nbk, (q + 1) * nbk)
-            put(out[own, cs], ops.gemm(mb, nbk, K, a_hi, a_lo2, sA, B1t[cs], B2t[cs], sB, out[own, cs],
-                                       four_term, one_term))
+    oc = slice(i * nbk, (i + 1) * nbk)           # this rank's own B block (position i in the panel)
+    put(out[own, oc], ops.gemm(mb, nbk, K, a_hi, a_lo2, sA, b_hi, b_lo2, sB, out[own, oc], four_term, one_term,
+                               overlapped=use_streams))
+    if use_streams:
+        compute.wait_event(ev_b)
     else:
-        panel_b()
-        put(out[own], ops.gemm(mb, n, K, a_hi, a_lo2, sA, B1t, B2t, sB, out[own], four_term, one_term))
+        B1, B2 = gather_b()
+    for q in range(pr):
+        if q == i:
+            continue
+        cs = slice(q * nbk, (q + 1) * nbk)
+        b1, b2 = bblock(B1, B2, q)
+        put(out[own, cs], ops.gemm(mb, nbk, K, a_hi, a_lo2, sA, b1, b2, sB, out[own, cs], four_term, one_term,
+                                   overlapped=use_streams))
     if on_block is not None:
         on_block(own)
     if use_streams:
         compute.wait_stream(comm)
     else:
-        A1 = _gather_rows(a_hi, row_groups[i], pc)
-        A2 = A1 if one_term else _gather_rows(a_lo, row_groups[i], pc)
+        A1, A2 = gather_a()
     for q in range(pc):
         if q == j:
             continue
         rs = slice(q * mb, (q + 1) * mb)
-        put(out[rs], ops.gemm(mb, n, K, A1[rs], A2[rs], sA, B1t, B2t, sB, out[rs], four_term, one_term))
-        if on_block is not None:
-            on_block(rs)
+        row_block(rs, A1[rs], A2[rs], B1, B2, False)
     if use_streams:
-        for t in (A1, A2, B1t, B2t):
+        for t in (A1, A2, B1, B2):
             t.record_stream(compute)
     return out
 
@@ -266,8 +318,8 @@ def sgemm_2d_replicated(A: torch.Tensor, B: torch.Tensor, ops, out: torch.Tensor
     ops.maxabs_into(Ap, mx[0:1])
     ops.maxabs_into(Bp, mx[1:2])
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-    a_hi, a_lo, sA = ops.split(Ap, mx[0:1], False)
-    b_hi, b_lo, sB = ops.split(Bp, mx[1:2], True)
+    a_hi, a_lo, sA = ops.split(Ap, mx[0:1])
+    b_hi, b_lo, sB = ops.split(Bp, mx[1:2])
     m, n = r1 - r0, c1 - c0
     if out is None:
         out = torch.empty((m, n), dtype=torch.float32, device=A.device)
@@ -288,7 +340,7 @@ class TileGemm:
 
     def __init__(self, h, n: int, world: int, rank: int, four_term=False, one_term=False, seed=0,
                  ops=None, device=None, replicated: bool = False, global_n: int | None = None,
-                 streams: bool | None = None):
+                 streams: bool | None = None, gather_ctas: int | None = None):
         from workloads import numpy_matrix, torch_matrix
 
         self.replicated = replicated
@@ -301,8 +353,16 @@ class TileGemm:
         else:
             self.M, self.N, self.K = self.pr * n, self.pc * n, n
         self.h = h
-        self.ops = ops if ops is not None else CudaOps(h)
-        self.groups = make_groups(world)
+        nccl = dist.get_backend() == "nccl"
+        if gather_ctas is None:
+            gather_ctas = GATHER_CTAS if (nccl and world > 1 and not replicated) else 0
+        if ops is None:
+            # pieces under a gather leave 2 SMs per gather CTA free: a CTA on one SM of a TPC
+            # would otherwise break that TPC's GEMM CTA pair (cluster of 2)
+            sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+            ops = CudaOps(h, gemm_sms_during_gather=max(sms - 2 * gather_ctas, 2) if gather_ctas else 0)
+        self.ops = ops
+        self.groups = make_groups(world, gather_ctas or None)
         r0, r1 = a_block_rows(self.M, world, rank)
         c0, c1 = b_block_cols(self.N, world, rank)
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -341,9 +401,10 @@ class TileGemm:
 
     def launches_per_step(self) -> int:
         """library kernels of the last run() (counted by the ops; NCCL's not counted), else the
-        plan: 2 max-abs + 2 splits + one GEMM per row block of the tile (one with replicated inputs)"""
+        plan: 2 max-abs + 2 splits + one GEMM per (row block, column block) piece of the tile
+        (one GEMM with replicated inputs)"""
         if getattr(self, "_last_launches", None) is not None:
             return self._last_launches
         if self.replicated:
             return 5
-        return 4 + (self.pc if self.pc > 1 else 1)
+        return 4 + self.pc * self.pr

@@ -117,10 +117,11 @@ class DenseNet:
     def capture_step(self, X, y, lr: float):
         """CUDA-graph the training step on the static batch buffers X, y (refill them in place
         between replays).  Returns (replay, loss_tensor)."""
-        self.step_device(X, y, lr)          # warm-up: workspace and allocator pools
-        torch.cuda.synchronize()
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):          # warm-up on the capture stream: its handle + workspace
+            self.step_device(X, y, lr)
+        torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(s):
             with torch.cuda.graph(g, stream=s):

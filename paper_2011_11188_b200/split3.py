@@ -15,9 +15,7 @@ import torch
 
 from . import _build
 
-# SPLIT3_EXPERIMENT_LIB: load an experimental build of the same sources (tools/exp_ab.py) instead
-# of the in-tree library — for A/B timing experiments only.
-LIB_PATH = os.environ.get("SPLIT3_EXPERIMENT_LIB") or _build.LIB
+LIB_PATH = _build.LIB
 
 OK = 0
 ERR_INVALID_VALUE = 1
@@ -36,11 +34,11 @@ BF16X3 = 1 << 3
 # every symbol include/split3.h declares (checked by tests/test_capi.py)
 EXPORTS = (
     "split3_sgemm_create", "split3_set_stream", "split3_sgemm_destroy",
-    "split3_sgemm_workspace_size", "split3_sgemm_set_workspace", "split3_sgemm",
+    "split3_sgemm_workspace_size", "split3_sgemm_ex_workspace_size", "split3_sgemm_set_workspace", "split3_sgemm",
     "split3_sgemm_host_workspace_size", "split3_sgemm_host", "split3_last_bad_index", "split3_host_redo_count",
     "split3_status_string", "split3_maxabs", "split3_split", "split3_gemm_planes",
     "split3_last_launch_count", "split3_timing_enable", "split3_timing_read",
-    "split3_set_promotion", "split3_set_wave_sync", "split3_set_schedule", "split3_set_fused_split",
+    "split3_set_promotion", "split3_set_wave_sync", "split3_set_split_k", "split3_set_max_sms", "split3_set_schedule", "split3_set_fused_split",
     "split3_sgemm_ex", "split3_presplit", "split3_presplit_stored", "split3_split_bf16x3", "split3_bias_act", "split3_relu_backward",
     "split3_softmax_xent", "split3_bias_grad", "split3_sgd_update",
 )
@@ -102,6 +100,8 @@ def load() -> ctypes.CDLL:
         lib.split3_sgemm_destroy.argtypes = [_p]
         lib.split3_sgemm_workspace_size.restype = ctypes.c_size_t
         lib.split3_sgemm_workspace_size.argtypes = [_i64, _i64, _i64, ctypes.c_uint32]
+        lib.split3_sgemm_ex_workspace_size.restype = ctypes.c_size_t
+        lib.split3_sgemm_ex_workspace_size.argtypes = [_i64, _i64, _i64, ctypes.c_uint32, ctypes.c_int, ctypes.c_int]
         lib.split3_sgemm_host_workspace_size.restype = ctypes.c_size_t
         lib.split3_sgemm_host_workspace_size.argtypes = [_i64, _i64, _i64, ctypes.c_uint32]
         lib.split3_sgemm_set_workspace.argtypes = [_p, _p, ctypes.c_size_t]
@@ -115,6 +115,8 @@ def load() -> ctypes.CDLL:
         lib.split3_timing_enable.argtypes = [_p, ctypes.c_int]
         lib.split3_set_promotion.argtypes = [_p, ctypes.c_int]
         lib.split3_set_wave_sync.argtypes = [_p, ctypes.c_int]
+        lib.split3_set_split_k.argtypes = [_p, ctypes.c_int]
+        lib.split3_set_max_sms.argtypes = [_p, ctypes.c_int]
         lib.split3_set_schedule.argtypes = [_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         lib.split3_set_fused_split.argtypes = [_p, ctypes.c_int, _i64]
         lib.split3_sgemm_ex.argtypes = [_p, _i64, _i64, _i64, ctypes.POINTER(split3_matrix),
@@ -164,8 +166,24 @@ def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+class _StreamState:
+    """The library handle and workspace of one CUDA stream (include/split3.h: a handle is not
+    thread-safe and serves one stream; its workspace and device counters are per call chain)."""
+
+    __slots__ = ("h", "ws", "pinned", "captured")
+
+    def __init__(self, h):
+        self.h = h
+        self.ws = None          # torch uint8 tensor attached as the workspace
+        self.pinned = []        # retired workspaces a captured CUDA graph may still point into
+        self.captured = False   # the current workspace was used under stream capture
+
+
 class Handle:
-    """One split3 handle bound to a CUDA device; uses torch's current stream per call."""
+    """split3 on one CUDA device.  Every call runs on torch's current stream; each stream gets its
+    own library handle (device counters) and workspace, so calls on different streams never share
+    scratch memory.  A workspace that a CUDA graph captured is never freed while the Handle lives
+    (a later, larger call attaches a new one and keeps the old one alive for the graph's replays)."""
 
     def __init__(self, device=None):
         lib = load()
@@ -173,17 +191,19 @@ class Handle:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", torch.device("cuda", device).index
                                    if not isinstance(device, int) else device)
-        self._h = _p()
-        st = lib.split3_sgemm_create(ctypes.byref(self._h), self.device.index, None)
-        if st != OK:
-            raise Split3Error(st, "split3_sgemm_create")
-        self._ws = None
         self._lib = lib
+        self._states: dict[int, _StreamState] = {}
+        self._settings: dict[str, tuple] = {}     # knob -> args, applied to every stream's handle
+        self._closed = False
+        self._state()                             # create the current stream's handle (errors here)
 
     def close(self):
-        if self._h:
-            self._lib.split3_sgemm_destroy(self._h)
-            self._h = _p()
+        for stt in self._states.values():
+            if stt.h:
+                self._lib.split3_sgemm_destroy(stt.h)
+                stt.h = _p()
+        self._states = {}
+        self._closed = True
 
     def __del__(self):
         try:
@@ -192,43 +212,94 @@ class Handle:
             pass
 
     # -- plumbing ---------------------------------------------------------------
-    def _bind_stream(self):
+    def _state(self) -> _StreamState:
+        if self._closed:
+            raise RuntimeError("split3 Handle is closed")
         s = torch.cuda.current_stream(self.device).cuda_stream
-        self._lib.split3_set_stream(self._h, s)
+        stt = self._states.get(s)
+        if stt is None:
+            hp = _p()
+            st = self._lib.split3_sgemm_create(ctypes.byref(hp), self.device.index, _p(s))
+            if st != OK:
+                raise Split3Error(st, "split3_sgemm_create")
+            stt = _StreamState(hp)
+            for name, args in self._settings.items():
+                st = getattr(self._lib, name)(hp, *args)
+                if st != OK:
+                    raise Split3Error(st, name)
+            self._states[s] = stt
+        return stt
+
+    @property
+    def _h(self):
+        """the library handle of torch's current stream"""
+        return self._state().h
+
+    @property
+    def _ws(self):
+        return self._state().ws
+
+    @_ws.setter
+    def _ws(self, t):
+        self._state().ws = t
+
+    def _bind_stream(self):
+        """Kept for the call sites: the handle of the current stream is created bound to it."""
+        stt = self._state()
+        if torch.cuda.is_current_stream_capturing():
+            stt.captured = True
+        return stt
+
+    def _set(self, name: str, *args):
+        """Apply a knob to every stream's handle, present and future."""
+        self._settings[name] = args
+        for stt in self._states.values():
+            st = getattr(self._lib, name)(stt.h, *args)
+            if st != OK:
+                raise Split3Error(st, name)
 
     def _ensure_ws(self, nbytes: int):
-        if self._ws is None or self._ws.numel() < nbytes:
-            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
-            st = self._lib.split3_sgemm_set_workspace(self._h, self._ws.data_ptr(), self._ws.numel())
+        stt = self._state()
+        if stt.ws is None or stt.ws.numel() < nbytes:
+            if stt.ws is not None and (stt.captured or torch.cuda.is_current_stream_capturing()):
+                stt.pinned.append(stt.ws)     # a captured graph may replay into it: keep it alive
+            stt.captured = False
+            # allocated on this stream: the caching allocator reuses a freed block only in this
+            # stream's order, so a replaced (uncaptured) workspace is safe to drop
+            stt.ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            st = self._lib.split3_sgemm_set_workspace(stt.h, stt.ws.data_ptr(), stt.ws.numel())
             if st != OK:
                 raise Split3Error(st, "split3_sgemm_set_workspace")
+        if torch.cuda.is_current_stream_capturing():
+            stt.captured = True
 
     def workspace_size(self, M, N, K, flags=0) -> int:
         return int(self._lib.split3_sgemm_workspace_size(M, N, K, flags))
 
     def set_promotion(self, kblocks: int):
         """D_hi promotion period in 64-wide k-blocks (0 = library default)."""
-        st = self._lib.split3_set_promotion(self._h, int(kblocks))
-        if st != OK:
-            raise Split3Error(st, "split3_set_promotion")
+        self._set("split3_set_promotion", int(kblocks))
 
     def set_wave_sync(self, enable: bool):
-        st = self._lib.split3_set_wave_sync(self._h, int(enable))
-        if st != OK:
-            raise Split3Error(st, "split3_set_wave_sync")
+        self._set("split3_set_wave_sync", int(enable))
+
+    def set_split_k(self, enable: bool):
+        """Split-K tail on (default) or whole tiles only (deterministic per-element K order)."""
+        self._set("split3_set_split_k", int(enable))
+
+    def set_max_sms(self, sms: int):
+        """Cap the SMs the GEMM occupies (0 = all; even)."""
+        self._set("split3_set_max_sms", int(sms))
 
     def set_schedule(self, group_m: int = 0, l2_policy_a: int = 0, l2_policy_b: int = 0):
-        st = self._lib.split3_set_schedule(self._h, group_m, l2_policy_a, l2_policy_b)
-        if st != OK:
-            raise Split3Error(st, "split3_set_schedule")
+        self._set("split3_set_schedule", int(group_m), int(l2_policy_a), int(l2_policy_b))
 
     def set_fused_split(self, mode: int, max_m: int = 0):
         """Fused split of an fp32 B inside the GEMM (NEXT #2): 0 off, 1 auto (M <= max_m), 2 always."""
-        st = self._lib.split3_set_fused_split(self._h, int(mode), int(max_m))
-        if st != OK:
-            raise Split3Error(st, "split3_set_fused_split")
+        self._set("split3_set_fused_split", int(mode), int(max_m))
 
     def timing_enable(self, enable: bool = True):
+        """CUDA-event timing of the split and GEMM phases of later calls (current stream's handle)."""
         self._lib.split3_timing_enable(self._h, int(enable))
 
     def timing_read(self):
@@ -330,7 +401,8 @@ class Handle:
             out = torch.empty((M, N), dtype=torch.float32, device=dev)
         _check_mat(out, "C")
         flags = _flags(four_term, one_term, check_finite, bf16x3)
-        self._ensure_ws(self.workspace_size(M, N, K, flags))
+        self._ensure_ws(int(self._lib.split3_sgemm_ex_workspace_size(
+            M, N, K, flags, int(isinstance(A, Planes)), int(isinstance(B, Planes)))))
         self._bind_stream()
         st = self._lib.split3_sgemm_ex(self._h, M, N, K, ctypes.byref(da), ctypes.byref(db),
                                        _ptr(out), _ld(out), flags)

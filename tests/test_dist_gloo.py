@@ -55,18 +55,16 @@ class OracleOps:
         assert bad < 0
         d_max1[0] = max(float(d_max1[0]), m)
 
-    def split(self, X, d_max1, transpose):
+    def split(self, X, d_max1):
         s = self.o.scale_exp(float(d_max1[0]))
         hi, lo, _ = self.o.split(np.ascontiguousarray(X.numpy()), s=s)
-        if transpose:
-            hi, lo = hi.T.copy(), lo.T.copy()
         return (torch.from_numpy(hi.view(np.int16)), torch.from_numpy(lo.view(np.int16)),
                 torch.tensor([s], dtype=torch.int32))
 
-    def gemm(self, m, n, K, A1, A2, sA, B1t, B2t, sB, out, four_term, one_term):
+    def gemm(self, m, n, K, A1, A2, sA, B1, B2, sB, out, four_term, one_term, overlapped=False):
         terms = 1 if one_term else (4 if four_term else 3)
-        np16 = lambda t: t.numpy().view(np.uint16)
-        C = self.o.split_gemm(np16(A1), np16(A2), int(sA[0]), np16(B1t).T, np16(B2t).T, int(sB[0]), terms)
+        np16 = lambda t: np.ascontiguousarray(t.numpy()).view(np.uint16)
+        C = self.o.split_gemm(np16(A1), np16(A2), int(sA[0]), np16(B1), np16(B2), int(sB[0]), terms)
         return torch.from_numpy(C)
 
 

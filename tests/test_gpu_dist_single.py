@@ -22,8 +22,27 @@ def nccl_one_rank():
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,kw", [(1024, {}), (2048, {}), (1536, {"four_term": True})])
+def _oracle_errors(C, A, B, terms=3, R=192):
+    """E_or / E64 of C on R x R seeded sampled outputs (oracle: scales from the whole matrices)"""
+    import oracle
+
+    An, Bn = A.cpu().numpy(), B.cpu().numpy()
+    rng = np.random.default_rng(11)
+    rows = np.sort(rng.choice(An.shape[0], size=min(R, An.shape[0]), replace=False))
+    cols = np.sort(rng.choice(Bn.shape[1], size=min(R, Bn.shape[1]), replace=False))
+    Cs, _, _ = oracle.sgemm_sampled(An, Bn, rows, cols, terms=terms)
+    C64 = oracle.gemm64(np.ascontiguousarray(An[rows]), np.ascontiguousarray(Bn[:, cols]))
+    T = C.cpu().double().numpy()[np.ix_(rows, cols)]
+    e_or = float(np.linalg.norm(T - Cs) / np.linalg.norm(Cs))
+    e64 = float(np.linalg.norm(T - C64) / (np.linalg.norm(An[rows].astype(np.float64)) *
+                                          np.linalg.norm(Bn[:, cols].astype(np.float64))))
+    return e_or, e64
+
+
+@pytest.mark.parametrize("n,kw", [(1024, {}), (2304, {}), (1536, {"four_term": True})])
 def test_tile_gemm_one_rank_matches_single_call(nccl_one_rank, n, kw):
+    """sharded-input driver on a one-rank NCCL group: bitwise the one-GPU call with split-K off,
+    and within the oracle tolerance"""
     import paper_2011_11188_b200 as s3
     from paper_2011_11188_b200.dist import TileGemm
 
@@ -32,20 +51,19 @@ def test_tile_gemm_one_rank_matches_single_call(nccl_one_rank, n, kw):
     C = tg.run()
     torch.cuda.synchronize()
     assert C.shape == (n, n)
-    ref = h.sgemm(tg.A_blk, tg.B_blk, **kw).double()
-    # same planes and scales; the row-block schedule may change the split-K plan (summation order)
-    e = float((C.double() - ref).norm() / ref.norm())
-    assert e < 1e-6, e
-    C64 = tg.A_blk.double() @ tg.B_blk.double()
-    e64 = float((C.double() - C64).norm() / C64.norm())
-    assert e64 < 2e-6, e64
-    assert tg.launches_per_step() >= 5       # counted: + the split-K tail reduction when planned
+    h1 = s3.Handle(0)
+    h1.set_split_k(False)
+    ref = h1.sgemm(tg.A_blk, tg.B_blk, **kw)
+    assert torch.equal(C.view(torch.int32), ref.view(torch.int32))
+    e_or, e64 = _oracle_errors(C, tg.A_blk, tg.B_blk, terms=4 if kw.get("four_term") else 3)
+    assert e_or <= 1e-6 and e64 <= 2e-6, (e_or, e64)
+    assert tg.launches_per_step() == 5       # 2 max-abs + 2 splits + 1 GEMM piece, counted
     assert np.isfinite(C.cpu().numpy()).all()
 
 
-@pytest.mark.parametrize("n", [1024, 2048])
+@pytest.mark.parametrize("n", [1024, 2304])
 def test_tile_gemm_replicated_one_rank(nccl_one_rank, n):
-    """replicated inputs (no plane exchange): same planes and scales as the single-GPU call"""
+    """replicated inputs (no plane exchange): bitwise the one-GPU call with split-K off"""
     import paper_2011_11188_b200 as s3
     from paper_2011_11188_b200.dist import TileGemm
 
@@ -53,37 +71,68 @@ def test_tile_gemm_replicated_one_rank(nccl_one_rank, n):
     tg = TileGemm(h, n, 1, 0, seed=6, replicated=True)
     C = tg.run()
     torch.cuda.synchronize()
-    ref = h.sgemm_ex(tg.A, tg.B)
-    assert torch.equal(C.view(torch.int32), ref.view(torch.int32)) or \
-        float((C.double() - ref.double()).norm() / ref.double().norm()) < 1e-6
+    h1 = s3.Handle(0)
+    h1.set_split_k(False)
+    ref = h1.sgemm_ex(tg.A, tg.B)
+    assert torch.equal(C.view(torch.int32), ref.view(torch.int32))
+    e_or, e64 = _oracle_errors(C, tg.A, tg.B)
+    assert e_or <= 1e-6 and e64 <= 2e-6, (e_or, e64)
     assert tg.launches_per_step() >= 5
 
 
-def test_gemm_planes_column_pieces_equal_whole():
-    """the 2-D driver's column pieces (own rows x one B block of the panel, written into a column
-    slice of the tile): gemm_planes on B^T plane row slices into strided C views == one whole call
-    (to the oracle tolerance: the pieces' split-K plans, and so summation orders, differ)"""
+def test_gemm_pieces_equal_whole_bitwise():
+    """the 2-D driver's pieces (row block x column block of the tile, written into strided C views
+    from row slices of the K-major A planes and of stacked MN-major B blocks) == one whole call,
+    BITWISE with split-K off (every element accumulates over K in the same order)"""
     import paper_2011_11188_b200 as s3
+    from paper_2011_11188_b200.split3 import Planes
     from workloads import torch_matrix
 
     h = s3.Handle(0)
-    m, n, K, pr = 1024, 2048, 1536, 2
+    h.set_split_k(False)
+    m, n, K, pr, pc = 1024, 2048, 1536, 2, 4
     A = torch_matrix("uniform", m, K, seed=61)
     B = torch_matrix("loguni", K, n, seed=62)
     mx = torch.zeros(2, dtype=torch.float32, device="cuda")
     h.maxabs(A, mx[0:1])
     h.maxabs(B, mx[1:2])
     a_hi, a_lo, sA = h.split(A, mx[0:1])
-    b_hi, b_lo, sB = h.split(B, mx[1:2], transpose=True)          # B^T planes: n x K
-    whole = h.gemm_planes(m, n, K, a_hi, a_lo, sA, b_hi, b_lo, sB).clone()
+    nbk, mb = n // pr, m // pc
+    blocks = [h.split(B[:, q * nbk:(q + 1) * nbk].contiguous(), mx[1:2]) for q in range(pr)]
+    b_hi = torch.cat([b[0] for b in blocks])       # pr stacked K x nbk MN-major blocks
+    b_lo = torch.cat([b[1] for b in blocks])
+    sB = blocks[0][2]
+    whole = h.sgemm(A, B).clone()
     C = torch.full((m, n), 7.0, device="cuda")
-    nbk = n // pr
-    for q in range(pr):
-        cs = slice(q * nbk, (q + 1) * nbk)
-        h.gemm_planes(m, nbk, K, a_hi, a_lo, sA, b_hi[cs], b_lo[cs], sB, out=C[:, cs])
+    for r in range(pc):
+        rs = slice(r * mb, (r + 1) * mb)
+        for q in range(pr):
+            cs = slice(q * nbk, (q + 1) * nbk)
+            h.sgemm_ex(Planes(a_hi[rs], a_lo[rs], sA, None, mb, K, stored=True),
+                       Planes(b_hi[q * K:(q + 1) * K], b_lo[q * K:(q + 1) * K], sB, None, K, nbk, stored=True),
+                       out=C[rs, cs])
     torch.cuda.synchronize()
-    assert torch.isfinite(C).all()
-    assert float((C.double() - whole.double()).norm() / whole.double().norm()) < 1e-6
+    assert torch.equal(C.view(torch.int32), whole.view(torch.int32))
+
+
+def test_max_sms_cap_bitwise():
+    """the GEMM on a reduced SM budget (the pieces that overlap a gather) gives the same bits"""
+    import paper_2011_11188_b200 as s3
+    from workloads import torch_matrix
+
+    h = s3.Handle(0)
+    h.set_split_k(False)
+    A = torch_matrix("uniform", 2304, 1536, seed=71)
+    B = torch_matrix("uniform", 1536, 2560, seed=72)
+    ref = h.sgemm(A, B).clone()
+    for sms in (132, 64, 2):
+        h.set_max_sms(sms)
+        C = h.sgemm(A, B)
+        torch.cuda.synchronize()
+        assert torch.equal(C.view(torch.int32), ref.view(torch.int32)), sms
+    h.set_max_sms(0)
+    with pytest.raises(s3.Split3Error):
+        h.set_max_sms(3)
 
 
 def test_nccl_plane_all_gather_dtype(nccl_one_rank):

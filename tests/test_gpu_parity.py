@@ -50,6 +50,40 @@ def _metrics(C, Csplit, C64, A, B):
     return e_or, e64, e64rel
 
 
+def _elementwise_bound(orc, A, B, terms, slices=16):
+    """Per-element bound on |C_gpu - C_split| (C_split: the oracle's fp64 Eq. A_2), from the
+    measured accumulator semantics (DESIGN.md §3 R9): one kind::f16 MMA sums 16 exact products
+    into the FP32 accumulator with truncation, losing < 1 ulp of the largest addend per addend
+    (<= 18 u M per MMA, u = 2^-23, M <= the partial sum of |products|); D_hi is promoted with
+    round-to-nearest every 8 MMAs (library default), D_mid (D_lo) accumulate over the whole K;
+    split-K slices are added with RN; the epilogue fma rounds once, the 2^(sA+sB) scale is exact.
+        |err_ij| <= 2^(sA+sB) [ (144 u + (K/128 + 1 + slices) u/2) S_hi
+                               + 2^-11 (18 ceil(K/16) + 1) u S_mid + 2^-22 (18 ceil(K/16) + 1) u S_lo ]
+                    + u/2 |C_split|
+    with S_hi = |A1| |B1|, S_mid = |A1||B2| + |A2||B1|, S_lo = |A2||B2| (decoded planes)."""
+    K = A.shape[1]
+    a1, a2, sA = orc.split(A)
+    b1, b2, sB = orc.split(B)
+    A1, A2 = np.abs(orc.dec16(a1)), np.abs(orc.dec16(a2))
+    B1, B2 = np.abs(orc.dec16(b1)), np.abs(orc.dec16(b2))
+    u = 2.0 ** -23
+    nk = -(-K // 16)
+    bnd = (144 * u + (K / 128 + 1 + slices) * u / 2) * (A1 @ B1)
+    if terms != 1:
+        bnd += 2.0 ** -11 * (18 * nk + 1) * u * (A1 @ B2 + A2 @ B1)
+    if terms == 4:
+        bnd += 2.0 ** -22 * (18 * nk + 1) * u * (A2 @ B2)
+    return np.ldexp(bnd, sA + sB)
+
+
+def _assert_elementwise(orc, C, Cs, A, B, terms):
+    bound = _elementwise_bound(orc, A, B, terms) + 2.0 ** -24 * np.abs(Cs)
+    err = np.abs(C.astype(np.float64) - Cs)
+    bad = np.argwhere(err > bound)
+    assert bad.size == 0, (bad[:5].tolist(), err[tuple(bad[0])], bound[tuple(bad[0])])
+    return float(np.max(err / np.maximum(bound, 1e-300)))
+
+
 # ----------------------------------------------------------- a1 + a2: planes -----
 
 SPLIT_SHAPES = [(1, 1), (3, 5), (64, 64), (65, 129), (200, 333), (256, 1000), (1000, 72)]
@@ -135,6 +169,7 @@ def test_sgemm_vs_oracle(h, orc, shape, terms):
     assert e_or <= E_OR_TOL, (e_or, e64, e64rel)
     if terms != 1:
         assert e64 <= E64_TOL and e64rel <= 1e-6, (e_or, e64, e64rel)
+    _assert_elementwise(orc, C, Cs, A, B, terms)     # every element, not only the norm
 
 
 @pytest.mark.parametrize("kind", ["loguni", "glorot", "fp16"])
@@ -146,6 +181,31 @@ def test_sgemm_distributions(h, orc, kind):
     Cs = orc.sgemm(A, B, terms=3)
     e_or, _, _ = _metrics(C, Cs, orc.gemm64(A, B), A, B)
     assert e_or <= E_OR_TOL
+    _assert_elementwise(orc, C, Cs, A, B, 3)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "loguni"])
+def test_full_4096_every_element_vs_oracle(h, orc, kind):
+    """N = 4096 (configs[1] small size), launched as bench.py does: EVERY element of C against the
+    oracle's full fp64 emulation (no sampling) — E_or, E64 and the per-element bound"""
+    N = 4096
+    A = torch_matrix(kind, N, N, seed=41, device="cuda")
+    B = torch_matrix(kind, N, N, seed=42, device="cuda")
+    C = h.sgemm(A, B).cpu().numpy()
+    An, Bn = A.cpu().numpy(), B.cpu().numpy()
+    Cs = orc.sgemm(An, Bn, terms=3)
+    C64 = orc.gemm64(An, Bn)
+    e_or, e64, e64rel = _metrics(C, Cs, C64, An, Bn)
+    worst = _assert_elementwise(orc, C, Cs, An, Bn, 3)
+    rec = {"N": N, "kind": kind, "E_or": e_or, "E64": e64, "E64rel": e64rel, "max_err_over_bound": worst,
+           "elements": N * N}
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, f"parity_full4096_{kind}.json"), "w") as f:
+        json.dump(rec, f)
+    print(rec)
+    assert e_or <= E_OR_TOL, rec
+    if kind == "uniform":
+        assert e64 <= E64_TOL, rec
 
 
 @pytest.mark.parametrize("M,N,K", [(64, 64, 64), (300, 200, 4096), (256, 256, 16384)])

@@ -25,7 +25,7 @@ if len(tags) > 1 or os.environ.get("EXP_CHILD") is None:
     for tag in tags:
         env = dict(os.environ, EXP_CHILD="1")
         if tag != "base":
-            env["SPLIT3_EXPERIMENT_LIB"] = os.path.join(ROOT, "tools", "exp", f"libsplit3_{tag}.so")
+            env["EXP_LIB"] = os.path.join(ROOT, "tools", "exp", f"libsplit3_{tag}.so")
         out = subprocess.run([sys.executable, __file__, "time", str(M), str(N), str(K), tag], env=env,
                              capture_output=True, text=True)
         print(out.stdout.strip() or out.stderr[-2000:])
@@ -34,6 +34,8 @@ if len(tags) > 1 or os.environ.get("EXP_CHILD") is None:
 import torch  # noqa: E402
 
 import paper_2011_11188_b200 as s3  # noqa: E402
+if os.environ.get("EXP_LIB"):   # experimental build of the same sources (A/B runs only)
+    s3.split3.LIB_PATH = os.environ["EXP_LIB"]
 from workloads import torch_matrix  # noqa: E402
 
 h = s3.Handle(0)

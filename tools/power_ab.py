@@ -21,6 +21,8 @@ if os.environ.get("PAB_CHILD"):
     import torch
 
     import paper_2011_11188_b200 as s3
+    if os.environ.get("EXP_LIB"):   # experimental build of the same sources (A/B runs only)
+        s3.split3.LIB_PATH = os.environ["EXP_LIB"]
     from workloads import torch_matrix
 
     n, secs = int(os.environ["PAB_N"]), float(os.environ["PAB_SECS"])
@@ -83,7 +85,7 @@ for r in range(a.rounds):
             k, v = item.split("=")
             env[k] = v
         if lib != "base":
-            env["SPLIT3_EXPERIMENT_LIB"] = os.path.join(ROOT, "tools", "exp", f"libsplit3_{lib}.so")
+            env["EXP_LIB"] = os.path.join(ROOT, "tools", "exp", f"libsplit3_{lib}.so")
         out = subprocess.run([sys.executable, __file__], env=env, capture_output=True, text=True)
         try:
             res[tag].append(json.loads(out.stdout.strip().splitlines()[-1]))
