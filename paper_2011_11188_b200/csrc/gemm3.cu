@@ -13,17 +13,22 @@
 // with one round-to-nearest FP32 add, into a master copy held in registers ("promotion").
 // D_mid (weight 2^-11) and D_lo (2^-22) accumulate over the whole K in TMEM.
 //
-// sm_100a design:
-//  * CTA pairs (cluster of 2, tcgen05 cta_group::2): one 256 x 128 C tile per pair; CTA r of
-//    the pair loads A rows [m0 + 128 r, +128) and B^T rows [n0 + 64 r, +64); the leader's
-//    single thread issues M=256, N=128, K=16 MMAs that read both CTAs' shared memory, and
-//    each CTA's TMEM holds its 128 rows of the accumulators;
-//  * persistent: gridDim.x/2 pairs walk the tiles with a static, grouped raster;
-//  * warp 0 = TMA producer, warp 1 = MMA issuer (leader CTA) + TMEM owner, warps 2..5 =
-//    epilogue (promotion + final combine + masked stores);
-//  * TMEM (512 columns per CTA): D_hi ping-pong chunk buffers [0,128) and [128,256);
-//    D_mid double-buffered across tiles at [256,384) and [384,512) (3-term).  4-term: one
-//    D_mid buffer at 256 and D_lo at 384.
+// sm_100a design, v3:
+//  * CTA pairs (cluster of 2, tcgen05 cta_group::2): one 256 x 256 C tile per pair (4-term:
+//    256 x 128); CTA r of the pair TMA-loads A rows [m0 + 128 r, +128) and B rows
+//    [n0 + 128 r, +128) of each 64-wide k-block (128-B swizzle; B K-major or MN-major), and the
+//    leader's single elected thread issues the M = 256, K = 16 MMAs that read both CTAs' shared
+//    memory; each CTA's TMEM holds its 128 rows of the accumulators;
+//  * persistent: gridDim.x / 2 pairs walk the work units (whole tiles, then the split-K slices of
+//    the tail wave) with a grouped raster; a bounded wave lockstep keeps the concurrent tiles in
+//    the same K window of L2;
+//  * warp 0 = TMA producer, warp 1 = MMA issuer (leader CTA) + TMEM owner, warps 2..9 = 8
+//    epilogue warps (two per TMEM lane quadrant, 128 columns each: D_hi promotion into an FP32
+//    master in registers, the final fma with D_mid, the exact 2^(sA+sB) rescale and TMA stores);
+//    fused-B builds add warps 10..11, converters that split B's fp32 tiles in shared memory;
+//  * TMEM (512 columns per CTA): 3-term D_hi [0,256) + D_mid [256,512) (one D_hi buffer: the MMA
+//    warp issues a k-block's D_mid MMAs before waiting for the drained D_hi); 4-term (BN = 128)
+//    D_hi ping-pong [0,256) + D_mid [256,384) + D_lo [384,512); 1-term D_hi ping-pong.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -52,16 +57,6 @@ constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;         // shared::cluster address o
 constexpr uint64_t kPolicyNormal = 0x1000000000000000ull;
 constexpr uint64_t kPolicyFirst = 0x12F0000000000000ull;
 constexpr uint64_t kPolicyLast = 0x14F0000000000000ull;
-
-#ifdef SPLIT3_EXP_TRACE
-// experiment only (tools/exp_ab.py trace): per-CTA cycle counters of the barrier waits
-__device__ unsigned long long g_trace[160][16];
-#define TRACE_T0() const long long _t0 = clock64()
-#define TRACE_ADD(slot) atomicAdd(&g_trace[blockIdx.x][slot], (unsigned long long)(clock64() - _t0))
-#else
-#define TRACE_T0()
-#define TRACE_ADD(slot)
-#endif
 
 // ------------------------------------------------------------------ PTX wrappers -------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -127,38 +122,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             : "r"(bar), "r"(parity)
             : "memory");
     } while (!done);
-}
-// Epilogue-side wait (the epilogue warps idle most of a k-block period between promotions):
-// experiment builds try a suspend-time hint (SPLIT3_EXP_EPI_HINT_NS) or a back-off sleep
-// (SPLIT3_EXP_EPI_SLEEP_NS) instead of re-polling, to cut the issue slots (power) of spinning.
-__device__ __forceinline__ void mbar_wait_epi(uint32_t bar, uint32_t parity) {
-#if defined(SPLIT3_EXP_EPI_HINT_NS)
-    uint32_t done;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(bar), "r"(parity), "n"(SPLIT3_EXP_EPI_HINT_NS)
-            : "memory");
-    } while (!done);
-#elif defined(SPLIT3_EXP_EPI_SLEEP_NS)
-    uint32_t done;
-    for (;;) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(bar), "r"(parity)
-            : "memory");
-        if (done) break;
-        __nanosleep(SPLIT3_EXP_EPI_SLEEP_NS);
-    }
-#else
-    mbar_wait(bar, parity);
-#endif
 }
 // 2-SM TMA: data lands in this CTA's smem, the transaction bytes on the leader's barrier.
 __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar,
@@ -514,9 +477,6 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_wait();   // prologue above overlaps the predecessor's tail; no global access before here
-#ifdef SPLIT3_EXP_TRACE
-    const long long _tkernel = clock64();
-#endif
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs; warp-uniform, one elected lane) =====
@@ -531,18 +491,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             if (wave_counter && idx > 0) {
                 int64_t active = num_units - idx * num_pairs;   // pairs with an idx-th unit
                 if (active > num_pairs) active = num_pairs;
-#ifdef SPLIT3_EXP_WAVE_SLACK
-                const unsigned wait_target = wave_target;   // everyone started the previous unit
-#endif
                 wave_target += 2u * (unsigned)active;
-#ifndef SPLIT3_EXP_WAVE_SLACK
-                const unsigned wait_target = wave_target;
-#endif
-                if (elect_one()) {
-                    TRACE_T0();
-                    wave_sync(wave_counter, wait_target);
-                    TRACE_ADD(8);
-                }
+                if (elect_one()) wave_sync(wave_counter, wave_target);
                 __syncwarp();
             }
             int64_t mb, nb;
@@ -550,11 +500,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             const int32_t y_a = (int32_t)(mb * 2 * BM + crank * BM);
             const int32_t y_b = (int32_t)(nb * BN_ + crank * BNH);
             for (int kb = kb_begin; kb < kb_end; kb++) {
-                {
-                    TRACE_T0();
-                    mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
-                    if (lane == 0) TRACE_ADD(9);
-                }
+                mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
                 const uint32_t fb = smem_u32(&full_bar[stage]);
                 uint8_t* st = smem + stage * STAGE_BYTES;
                 const int32_t x = kb * BK;
@@ -628,11 +574,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     const uint32_t hb = HB == 2 ? (cc & 1) : 0;
                     const uint32_t hphase = HB == 2 ? ((cc >> 1) & 1) : (cc & 1);
                     const uint32_t t_hi = tmem_base + hb * BN_;
-                    {
-                        TRACE_T0();
-                        mbar_wait(smem_u32(&full_bar[stage]), phase);
-                        TRACE_ADD(0);
-                    }
+                    mbar_wait(smem_u32(&full_bar[stage]), phase);
                     tc_fence_after();
                     uint8_t* st = smem + stage * STAGE_BYTES;
                     auto adesc = [&](int off) {
@@ -655,9 +597,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     auto issue_mid = [&]() {
                         if (!HAS_MID) return;
                         if (!mid_ready) {
-                            TRACE_T0();
                             mbar_wait(smem_u32(&mempty_bar[0]), (tc & 1) ^ 1);
-                            TRACE_ADD(1);
                             tc_fence_after();
                             mid_ready = true;
                         }
@@ -680,9 +620,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     };
                     auto issue_hi = [&]() {
                         if (chunk_start) {
-                            TRACE_T0();
                             mbar_wait(smem_u32(&hempty_bar[hb]), hphase ^ 1);
-                            TRACE_ADD(2);
                             tc_fence_after();
                         }
                         if (elect_one()) {
@@ -726,7 +664,6 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             for (int kb = kb_begin; kb < kb_end; kb++) {
                 mbar_wait(smem_u32(&ffull_bar[stage]), phase);
                 uint8_t* breg = smem + stage * STAGE_BYTES + B_OFF;
-#ifndef SPLIT3_EXP_NO_CONVERT   // experiment only: time the fused-B pipeline without the conversion
                 if (BMN) {
                     convert_step(breg + cw * FB_STEP_BYTES, lane, f);
                     convert_step(breg + (cw + 2) * FB_STEP_BYTES, lane, f);
@@ -737,9 +674,6 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     convert_kgroups<4>(breg + (cw + 4 * NUM_CONV_WARPS) * FBK_GROUP_BYTES, NUM_CONV_WARPS * FBK_GROUP_BYTES,
                                        lane, f);
                 }
-#else
-                (void)breg; (void)f;
-#endif
                 fence_async_smem();   // generic-proxy plane stores -> visible to the MMA (async proxy)
                 __syncwarp();
                 if (lane == 0) mbar_arrive_leader(smem_u32(&full_bar[stage]));
@@ -770,26 +704,15 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             for (int kb0 = kb_begin; kb0 < kb_end; kb0 += promo_kb, cc++) {
                 const uint32_t hb = HB == 2 ? (cc & 1) : 0;
                 const uint32_t hphase = HB == 2 ? ((cc >> 1) & 1) : (cc & 1);
-                {
-                    TRACE_T0();
-                    mbar_wait_epi(smem_u32(&hfull_bar[hb]), hphase);
-                    if (warp == 2 && lane == 0) TRACE_ADD(3);
-                }
+                mbar_wait(smem_u32(&hfull_bar[hb]), hphase);
                 tc_fence_after();
-                {
-                    TRACE_T0();
-                    promote_all<NCOL>(lane_base + hb * BN_, master);
-                    if (warp == 2 && lane == 0) TRACE_ADD(4);
-                }
+                promote_all<NCOL>(lane_base + hb * BN_, master);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_leader(smem_u32(&hempty_bar[hb]));
             }
-#ifdef SPLIT3_EXP_TRACE
-            const long long _tend = clock64();
-#endif
             if (HAS_MID) {
-                mbar_wait_epi(smem_u32(&mfull_bar[0]), tc & 1);
+                mbar_wait(smem_u32(&mfull_bar[0]), tc & 1);
                 tc_fence_after();
 #pragma unroll
                 for (int c = 0; c < NCOL / 16; c++) {
@@ -840,10 +763,6 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             }
             const int64_t row = mb * 2 * BM + crank * BM + quad * 32 + lane;
             const int64_t col0 = nb * BN_ + half * NCOL;
-#ifdef SPLIT3_EXP_TRACE
-            if (warp == 2 && lane == 0) atomicAdd(&g_trace[blockIdx.x][5], (unsigned long long)(clock64() - _tend));
-            const long long _tst = clock64();
-#endif
             if (tma_store) {
                 // stage 32 rows x 32 columns per step (row = lane, 16-B chunks XOR-swizzled by
                 // row % 8 as the map's SWIZZLE_128B expects: 4 wavefronts per warp store), then one
@@ -866,16 +785,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                         bulk_commit();
                     }
                 }
-#ifdef SPLIT3_EXP_TRACE
-                if (warp == 2 && lane == 0) atomicAdd(&g_trace[blockIdx.x][6], (unsigned long long)(clock64() - _tst));
-#endif
                 continue;
             }
-#ifdef SPLIT3_EXP_NO_STORE
-            if (row == -1)   // experiment only: time the kernel without the C stores
-#else
             if (row < M)
-#endif
             {
                 float* crow = C + row * ldc + col0;
                 if (vec_ok && col0 + NCOL <= N) {
@@ -893,16 +805,6 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     }
 
     if (warp >= 2 && warp < 2 + NUM_EPI_WARPS && tma_store && lane == 0) bulk_wait0();   // C stores done
-#ifdef SPLIT3_EXP_TRACE
-    if (threadIdx.x == 0) {
-        atomicAdd(&g_trace[blockIdx.x][7], (unsigned long long)(clock64() - _tkernel));
-        unsigned smid, nsmid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        asm volatile("mov.u32 %0, %%nsmid;" : "=r"(nsmid));
-        g_trace[blockIdx.x][10] = smid;
-        g_trace[blockIdx.x][11] = nsmid;
-    }
-#endif
     tc_fence_before();
     cluster_sync();
     // Wave-lockstep counter reset: the last CTA to get here (exit ticket, word 3) zeroes the
@@ -1038,7 +940,7 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
              const CUtensorMap& b3, const CUtensorMap& mc, int tma_store,
              const int32_t* d_sA, const int32_t* d_sB, float* C, int64_t ldc, int num_sms,
              int promo_kb, unsigned* wave_counter, const GemmTune& tune, const SplitPlan& plan,
-             float* partial, const float* fb_maxB = nullptr, int32_t* fb_sB = nullptr) {
+             float* partial, const float* fb_maxB, int32_t* fb_sB) {
     constexpr int SMEM_BYTES = Geo<BN_, TERMS == 6 ? 3 : 2>::SMEM;
     // the dynamic-smem opt-in is per device: remember it per device ordinal
     static std::atomic<uint64_t> attr_set{0};
@@ -1059,6 +961,19 @@ int launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, const CUtensorMap
                  tune, plan, partial, fb_maxB, fb_sB) != cudaSuccess)
         return -1;
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+using LaunchFn = int (*)(cudaStream_t, int64_t, int64_t, int64_t, const CUtensorMap&, const CUtensorMap&,
+                         const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                         const CUtensorMap&, int, const int32_t*, const int32_t*, float*, int64_t, int, int,
+                         unsigned*, const GemmTune&, const SplitPlan&, float*, const float*, int32_t*);
+
+// the four operand layouts (mn bit 0: B MN-major, bit 1: A MN-major) of one kernel family
+template <int TERMS, int BN_, int FB>
+LaunchFn pick(int mn) {
+    static constexpr LaunchFn table[4] = {launch_t<TERMS, BN_, FB | 0>, launch_t<TERMS, BN_, FB | 1>,
+                                          launch_t<TERMS, BN_, FB | 2>, launch_t<TERMS, BN_, FB | 3>};
+    return table[mn & 3];
 }
 
 }  // namespace
@@ -1137,9 +1052,7 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     // TMA-store epilogue when C allows it (else per-thread float4 / scalar stores)
     CUtensorMap mc = ma1;
     int tma_store = 0;
-#ifndef SPLIT3_EXP_NO_STORE
     if ((ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(C) & 15u) == 0 && make_c_map(&mc, C, M, N, ldc)) tma_store = 1;
-#endif
     const int promo = promo_kb > 0 ? promo_kb : kDefaultPromoKb;
     GemmTune tune;
     tune.group_m = tin.group_m > 0 ? tin.group_m : kDefaultGroupM;
@@ -1152,19 +1065,16 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
         plan.nsplit = 0;
         plan.slices = 1;
     }
-    int r;
-    if (terms == 1) {
-        switch (mn & 3) { case 1: r = launch_t<1, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 2: r = launch_t<1, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 3: r = launch_t<1, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; default: r = launch_t<1, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); }
-    } else if (terms == 4) {
-        switch (mn & 3) { case 1: r = launch_t<4, 128, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 2: r = launch_t<4, 128, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 3: r = launch_t<4, 128, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; default: r = launch_t<4, 128, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); }
-    } else if (terms == 6) {
-        switch (mn & 3) { case 1: r = launch_t<6, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 2: r = launch_t<6, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 3: r = launch_t<6, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; default: r = launch_t<6, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); }
-    } else if (Bf) {
-        int32_t* sBw = const_cast<int32_t*>(d_sB);
-        switch (mn & 3) { case 1: r = launch_t<3, 256, 5>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial, d_maxB, sBw); break; case 2: r = launch_t<3, 256, 6>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial, d_maxB, sBw); break; case 3: r = launch_t<3, 256, 7>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial, d_maxB, sBw); break; default: r = launch_t<3, 256, 4>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial, d_maxB, sBw); }
-    } else {
-        switch (mn & 3) { case 1: r = launch_t<3, 256, 1>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 2: r = launch_t<3, 256, 2>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; case 3: r = launch_t<3, 256, 3>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); break; default: r = launch_t<3, 256, 0>(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo, wave_counter, tune, plan, partial); }
-    }
+    // instantiation table: TERMS x tile width x operand layout (LAY bits: B MN-major, A MN-major,
+    // fused B)
+    LaunchFn fn;
+    if (terms == 1) fn = pick<1, 256, 0>(mn);
+    else if (terms == 4) fn = pick<4, 128, 0>(mn);
+    else if (terms == 6) fn = pick<6, 256, 0>(mn);
+    else if (Bf) fn = pick<3, 256, LAY_FB>(mn);
+    else fn = pick<3, 256, 0>(mn);
+    int r = fn(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo,
+               wave_counter, tune, plan, partial, Bf ? d_maxB : nullptr, Bf ? const_cast<int32_t*>(d_sB) : nullptr);
     if (r < 0) { *err = 4; return -1; }
     if (plan.slices > 1) {
         const int bn = terms == 4 ? 128 : 256;
@@ -1178,13 +1088,3 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
 
 }  // namespace split3
 
-#ifdef SPLIT3_EXP_TRACE
-extern "C" int split3_exp_trace(unsigned long long* host, int reset) {
-    if (cudaMemcpyFromSymbol(host, split3::g_trace, sizeof(split3::g_trace)) != cudaSuccess) return 4;
-    if (reset) {
-        static unsigned long long zeros[160][16];
-        cudaMemcpyToSymbol(split3::g_trace, zeros, sizeof(zeros));
-    }
-    return 0;
-}
-#endif

@@ -35,45 +35,49 @@ comm = torch.cuda.Stream()
 sms = torch.cuda.get_device_properties(0).multi_processor_count
 
 
-def run(cap):
-    h.set_max_sms(cap)
+def run(cap, kind):
     cur = torch.cuda.current_stream()
-    h.sgemm(A, B, out=C)                 # the GEMM piece (compute stream)
+    pa = h.presplit_stored(A)            # a1 + a2 of the local blocks (compute stream)
+    pb = h.presplit_stored(B)
     ev = torch.cuda.Event()
     ev.record(cur)
-    comm.wait_event(ev)                  # issued after the GEMM was enqueued, like the gathers
-    with torch.cuda.stream(comm):
-        dst.copy_(src)                   # the gather stand-in
-    cur.wait_stream(comm)
+    comm.wait_event(ev)                  # the gather waits for the split, as in dist.sgemm_2d
+    with torch.cuda.stream(comm):        # the gather stand-in, issued first (as the driver does)
+        if kind == "sm_kernel":
+            torch.add(src, 0.0, out=dst)     # an SM copy kernel (NCCL's gathers are SM kernels)
+        else:
+            dst.copy_(src)                   # cudaMemcpyAsync D2D
+    h.set_max_sms(cap)
+    h.sgemm_ex(pa, pb, out=C)            # the GEMM piece (compute stream)
     h.set_max_sms(0)
+    cur.wait_stream(comm)
 
 
 res = {"shape": [M, N, K], "copy_mb": COPY_MB, "sms": sms, "cases": {}}
-for name, cap in (("uncapped", 0), (f"capped_{sms - RESERVE}", sms - RESERVE)):
-    for _ in range(3):
-        run(cap)
-    torch.cuda.synchronize()
-    with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        run(cap)
+for kind in ("sm_kernel", "memcpy"):
+    for name, cap in (("uncapped", 0), (f"capped_{sms - RESERVE}", sms - RESERVE)):
+        for _ in range(3):
+            run(cap, kind)
         torch.cuda.synchronize()
-    evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
-    t0 = min(e.time_range.start for e in evs)
-    rows = sorted(((e.time_range.start - t0) / 1e3, (e.time_range.end - t0) / 1e3, e.name) for e in evs)
-    print(f"--- {name}")
-    for s, e, nm in rows:
-        print(f"{s:9.3f} {e:9.3f} {e - s:8.3f}  {nm[:60]}")
-    g = [(s, e) for s, e, nm in rows if "gemm3" in nm]
-    cp = [(s, e) for s, e, nm in rows if "gemm3" not in nm and ("copy" in nm.lower() or "elementwise" in nm.lower()
-                                                                or "vectorized" in nm.lower())]
-    case = {"timeline_ms": [[round(s, 4), round(e, 4), nm] for s, e, nm in rows]}
-    if g and cp:
-        gs, ge = g[0]
-        cs, ce = cp[-1]
-        case.update(gemm_ms=ge - gs, copy_ms=ce - cs,
-                    overlap_ms=max(0.0, min(ge, ce) - max(gs, cs)),
-                    copy_start_after_gemm_start_ms=cs - gs, end_to_end_ms=max(ge, ce) - min(gs, cs))
-    res["cases"][name] = case
-    print({k: v for k, v in case.items() if k != "timeline_ms"})
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            run(cap, kind)
+            torch.cuda.synchronize()
+        evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
+        t0 = min(e.time_range.start for e in evs)
+        rows = sorted(((e.time_range.start - t0) / 1e3, (e.time_range.end - t0) / 1e3, e.name) for e in evs)
+        print(f"--- {kind} {name}")
+        for s0, e0, nm in rows:
+            print(f"{s0:9.3f} {e0:9.3f} {e0 - s0:8.3f}  {nm[:70]}")
+        g = [(s0, e0) for s0, e0, nm in rows if "gemm3" in nm]
+        cp = [(s0, e0) for s0, e0, nm in rows if ("Memcpy" in nm if kind == "memcpy" else "elementwise" in nm.lower())]
+        case = {"timeline_ms": [[round(s0, 4), round(e0, 4), nm] for s0, e0, nm in rows]}
+        if g and cp:
+            gs, ge = g[0]
+            cs, ce = cp[-1]
+            case.update(gemm_ms=ge - gs, copy_ms=ce - cs, overlap_ms=max(0.0, min(ge, ce) - max(gs, cs)),
+                        copy_end_before_gemm_end=ce < ge, span_ms=max(ge, ce) - min(gs, cs))
+        res["cases"][f"{kind}_{name}"] = case
+        print({k: v for k, v in case.items() if k != "timeline_ms"})
 os.makedirs("gpurun_out", exist_ok=True)
 with open("gpurun_out/overlap_timeline.json", "w") as f:
     json.dump(res, f, indent=1)
