@@ -9,7 +9,9 @@ Patches (results of these builds are WRONG by design; they time the machine, not
          whatever the stage holds: the GEMM without B's L2->SMEM traffic (upper bound of what TMA
          multicast of B over a cluster of pairs could save);
   halfb  B's planes loaded on every other k-block only (models a 2-pair cluster sharing B);
-  halfab both A's and B's planes on every other k-block (models a 2 x 2 cluster of pairs).
+  halfab both A's and B's planes on every other k-block (models a 2 x 2 cluster of pairs);
+  dupab  every odd k-block re-loads the previous k-block's A and B tiles (L2 hits): DRAM traffic
+         halves, L2->SMEM traffic unchanged (separates the two in the A/B above).
 """
 import os
 import shutil
@@ -29,7 +31,13 @@ ANCHOR_ADV = "                __syncwarp();\n                if (++stage == STAG
 ANCHOR_DECL = "        int64_t idx = 0;\n        for (int64_t unit = pair; unit < num_units; unit += num_pairs, idx++) {"
 
 
-def patch(src: str, skip_a: str, skip_b: str) -> str:
+ANCHOR_X = "                const int32_t x = kb * BK;\n"
+
+
+def patch(src: str, skip_a: str, skip_b: str, dup: bool = False) -> str:
+    if dup:
+        assert src.count(ANCHOR_X) == 1
+        src = src.replace(ANCHOR_X, "                const int32_t x = ((kb > kb_begin && ((kb - kb_begin) & 1)) ? kb - 1 : kb) * BK;\n")
     for a in (ANCHOR_TX, ANCHOR_A1, ANCHOR_LO, ANCHOR_ADV, ANCHOR_DECL):
         assert src.count(a) == 1, a
     src = src.replace(ANCHOR_DECL, "        int64_t idx = 0;\n        int64_t gkb = 0;\n"
@@ -53,11 +61,12 @@ PATCHES = {
     "nob": ("false", "true"),
     "halfb": ("false", "(gkb & 1) != 0"),
     "halfab": ("(gkb & 1) != 0", "(gkb & 1) != 0"),
+    "dupab": ("false", "false", True),
 }
 
 if __name__ == "__main__":
     tag = sys.argv[1]
-    skip_a, skip_b = PATCHES[tag]
+    skip_a, skip_b, *dup = PATCHES[tag]
     tmp = tempfile.mkdtemp()
     csrc = os.path.join(tmp, "pkg", "csrc")          # csrc/ includes ../../include/split3.h
     shutil.copytree(_build.CSRC, csrc)
@@ -66,7 +75,7 @@ if __name__ == "__main__":
     with open(g) as f:
         s = f.read()
     with open(g, "w") as f:
-        f.write(patch(s, skip_a, skip_b))
+        f.write(patch(s, skip_a, skip_b, bool(dup and dup[0])))
     out = os.path.join(ROOT, "tools", "exp", f"libsplit3_{tag}.so")
     cmd = [_build.NVCC, *_build.NVCC_FLAGS, "-shared", "-o", out,
            *sorted(os.path.join(csrc, x) for x in os.listdir(csrc) if x.endswith(".cu")),
