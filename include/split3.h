@@ -81,8 +81,7 @@ int split3_sgemm_destroy(split3_handle_t h);
 /* Bytes of device workspace split3_sgemm / split3_sgemm_ex need for (M, N, K): 256 bytes of
  * scalars, the four FP16 planes with padded leading dimensions (a multiple of 8 elements; B's
  * region fits either its K-major N x K planes or the MN-major K x N planes a row-major B is split
- * into), the block-scaled split's scratch (split3_set_block_scale: about
- * 4.7 KB per 128-row block of A and 128-column block of B) and,
+ * into) and,
  * when the problem has fewer 256-wide C tiles than CTA pairs, S*M*N floats of split-K partials
  * (S <= 16 slices of K, reduced in a fixed order: results are deterministic), sized for the
  * largest plan over every GEMM SM count up to 148 (split3_set_max_sms). */
@@ -208,18 +207,6 @@ int split3_split(split3_handle_t h, int64_t rows, int64_t cols, const float *X, 
                  const float *d_maxabs, uint16_t *hi, uint16_t *lo, int64_t ldp, int transpose,
                  int32_t *d_sexp);
 
-/* Block-scaled split of both operands in one pass (split3_set_block_scale): A
- * (M x K, lda) into K-major M x K planes A1/A2 (ldpa), B (K x N, ldb) into MN-major K x N planes
- * B1/B2 (ldpb), each 128-row block of A and 128-column block of B with its own exponent (rule R1 on
- * the block max; a block holding a nonzero |x| < 2^(s_matrix - 12) gets the per-matrix exponent).
- * d_sblk (device int32, ceil(M/128) + ceil(N/128) entries) receives the block exponents, A's
- * first; d_smat (2 entries) the per-matrix exponents of A and B.  ldpa, ldpb multiples of 8,
- * planes 16-byte aligned.  Uses the attached workspace as scratch (split3_sgemm_workspace_size
- * suffices).  NOT_IMPLEMENTED when ceil(M/128) + ceil(N/128) > 4096 or K >= 2^26. */
-int split3_split_blocks(split3_handle_t h, int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
-                        const float *B, int64_t ldb, uint16_t *A1, uint16_t *A2, int64_t ldpa, uint16_t *B1,
-                        uint16_t *B2, int64_t ldpb, int32_t *d_sblk, int32_t *d_smat);
-
 /* bf16 x 3 planes of X (SPLIT3_BF16X3's split, no scale): p1..p3 rows x cols (transpose = 0) or
  * cols x rows (transpose = 1), bfloat16 bit patterns, ldp a multiple of 8, 16-byte aligned. */
 int split3_split_bf16x3(split3_handle_t h, int64_t rows, int64_t cols, const float *X, int64_t ldx,
@@ -295,18 +282,6 @@ int split3_set_schedule(split3_handle_t h, int group_m, int l2_policy_a, int l2_
  * split3_sgemm call are bitwise equal (SURVEY §8e invariant; tests/test_gpu_dist_gloo_cuda.py).
  * Scheduling only for the numerics contract: both modes meet the oracle tolerance. */
 int split3_set_split_k(split3_handle_t h, int enable);
-
-/* Block-scaled single-pass split (default on; env SPLIT3_BLOCK_SCALE=0 at handle creation turns
- * it off): split3_sgemm (and split3_sgemm_ex with both operands fp32, not transposed, no
- * SPLIT3_CHECK_FINITE, not fused, not a one-launch small call) computes the scale exponent of every
- * 128-row block of A and every 128-column block of B (rule R1 on the block's max) and splits each
- * block right after its max in one pass over HBM (8 B/element instead of the two-pass 12); the
- * GEMM epilogue applies 2^(sA_i + sB_j) per 128 x 128 piece.  C is BITWISE the per-matrix-scale
- * result: a block exponent below the per-matrix one scales the block's planes and
- * every partial sum by an exact power of two, and a block that holds a nonzero
- * |x| < 2^(s_matrix - 12) (where fp16-subnormal rounding would differ) is re-split with the
- * per-matrix exponent before the GEMM.  Needs M/128 + N/128 <= 4096; else two-pass. */
-int split3_set_block_scale(split3_handle_t h, int enable);
 
 /* Cap on the SMs the persistent GEMM occupies (0 = all, else an even count >= 2; counts above
  * the device's are ignored).  The multi-GPU driver leaves SMs free this way while its plane

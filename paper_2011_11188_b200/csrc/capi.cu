@@ -17,12 +17,9 @@
 // [12] GEMM exit ticket (the last CTA zeroes [0] and [12]), [16] presplit max, [20] dummy max of
 // the one-matrix ticketed max-abs, [48..55] grid barrier (arrival count, sense) of the one-launch
 // front end,
-// [64..] max-abs block partials (2 x kMaxPartials floats), then the block-scaled split's ticket
-// (one word, 64-B slot) and its per-block barrier counters (kMaxBsplitBlocks words)
+// [64..] max-abs block partials (2 x kMaxPartials floats)
 constexpr size_t kMaxPartials = 2048;
-constexpr size_t kBsplitOff = 64 + 2 * kMaxPartials * 4;
-constexpr int64_t kMaxBsplitBlocks = 4096;   // M/128 + N/128 (larger problems: two-pass split)
-constexpr size_t kCounterBytes = kBsplitOff + 64 + kMaxBsplitBlocks * 4;
+constexpr size_t kCounterBytes = 64 + 2 * kMaxPartials * 4;
 
 struct split3_ctx {
     int device = 0;
@@ -36,8 +33,6 @@ struct split3_ctx {
     int wave_sync = 1;  // GEMM wave lockstep hint (L2 locality)
     int split_k = 1;    // split-K tail for partial last waves (0: whole tiles only, split3_set_split_k)
     int max_sms = 0;    // SMs the GEMM may occupy (0: all; split3_set_max_sms)
-    int block_scale = 1;   // block-scaled single-pass split (split3_set_block_scale; env SPLIT3_BLOCK_SCALE)
-    int64_t l2_bytes = 0;  // device L2 size (sizes the block-scaled split's blocks in flight)
     int prep_ok = 1;    // the cooperative one-launch front end is accepted (cleared on rejection)
     int64_t prep_max = split3::kPrepMaxElems;   // elements of A + B up to which it is used (env SPLIT3_PREP_MAX)
     int mn_major = 1;   // MN-major planes for a row-major B / a transposed A (no transposing split);
@@ -98,16 +93,8 @@ struct Carve {
     uint16_t* B1t;
     uint16_t* B2t;
     int64_t ldpa, ldpb, ldpa_mn, ldpb_mn;
-    void* bs;     // block-scaled split scratch
     size_t end;   // bytes used
 };
-
-constexpr int kMaxSmsSized = 148;   // workspace sizing (split-K partials, block-split scratch)
-inline size_t bsplit_region(int64_t M, int64_t N) {
-    return split3::bsplit_blocks(M, N) <= kMaxBsplitBlocks
-               ? ((split3::bsplit_scratch_bytes(M, N, kMaxSmsSized) + 255) & ~(size_t)255)
-               : 0;
-}
 
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -133,7 +120,6 @@ Carve carve(void* ws, int64_t M, int64_t N, int64_t K) {
     c.A2 = reinterpret_cast<uint16_t*>(b + off); off += pa;
     c.B1t = reinterpret_cast<uint16_t*>(b + off); off += pb;
     c.B2t = reinterpret_cast<uint16_t*>(b + off); off += pb;
-    c.bs = b + off; off += bsplit_region(M, N);   // block-scaled split scratch
     c.end = off;
     return c;
 }
@@ -141,9 +127,10 @@ Carve carve(void* ws, int64_t M, int64_t N, int64_t K) {
 // Split-K partials the workspace reserves: the largest plan over every SM count up to kMaxSms (a
 // handle may run its GEMM on fewer SMs: split3_set_max_sms, MIG, green contexts), so the plan a
 // call makes always fits; a device with more SMs would fall back to whole tiles (not sm_100).
+constexpr int kMaxSms = 148;
 int64_t partial_elems_bound(int64_t M, int64_t N, int64_t K, int terms) {
     int64_t mx = 0;
-    for (int sms = 2; sms <= kMaxSmsSized; sms += 2)
+    for (int sms = 2; sms <= kMaxSms; sms += 2)
         mx = std::max(mx, split3::gemm3_partial_elems(split3::gemm3_split_plan(M, N, K, terms, sms, 0), terms));
     return mx;
 }
@@ -152,8 +139,7 @@ size_t ws_bytes_for(int64_t M, int64_t N, int64_t K, bool planesA, bool planesB,
     if (M < 0 || N < 0 || K < 0) return 0;
     (void)planesA; (void)planesB;   // plane regions are always carved (fixed layout)
     size_t b = kScalarBytes + 2 * align256(std::max((size_t)M * (size_t)plane_ld(K), (size_t)K * (size_t)plane_ld(M)) * 2) +
-               2 * align256(std::max((size_t)N * (size_t)plane_ld(K), (size_t)K * (size_t)plane_ld(N)) * 2) +
-               bsplit_region(M, N);
+               2 * align256(std::max((size_t)N * (size_t)plane_ld(K), (size_t)K * (size_t)plane_ld(N)) * 2);
     if (terms_for_partials) b += align256((size_t)partial_elems_bound(M, N, K, terms_for_partials) * 4);
     return b;
 }
@@ -187,13 +173,6 @@ size_t ws_bytes_bf3(int64_t M, int64_t N, int64_t K, bool partials) {
 }
 
 inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
-
-unsigned* bsplit_ticket(split3_ctx* h) {
-    return reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(h->d_counters) + kBsplitOff);
-}
-unsigned* bsplit_cnt(split3_ctx* h) {
-    return reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(h->d_counters) + kBsplitOff + 64);
-}
 
 inline int terms_of(uint32_t flags) {
     if (flags & SPLIT3_BF16X3) return 6;
@@ -257,8 +236,6 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
         return SPLIT3_ERR_CUDA;
     }
     if (const char* e = getenv("SPLIT3_MN_MAJOR")) c->mn_major = atoi(e) != 0;
-    if (const char* e = getenv("SPLIT3_BLOCK_SCALE")) c->block_scale = atoi(e) != 0;
-    c->l2_bytes = prop.l2CacheSize;
     if (const char* e = getenv("SPLIT3_PREP_MAX")) c->prep_max = atoll(e);
     if (const char* e = getenv("SPLIT3_FUSE_B")) c->fuse_b = atoi(e);
     if (const char* e = getenv("SPLIT3_HOST_BLOCKS")) c->host_blocks = std::min(std::max(atoi(e), 0), 16);
@@ -346,25 +323,6 @@ int split3_split(split3_handle_t h, int64_t rows, int64_t cols, const float* X, 
     int n = transpose
                 ? split3::launch_split_t(h->stream, rows, cols, X, ldx, d_maxabs, hi, lo, ldp, d_sexp, h->num_sms)
                 : split3::launch_split(h->stream, rows, cols, X, ldx, d_maxabs, hi, lo, ldp, d_sexp, h->num_sms);
-    if (n < 0) return SPLIT3_ERR_CUDA;
-    h->last_launches = n;
-    return SPLIT3_OK;
-}
-
-int split3_split_blocks(split3_handle_t h, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
-                        const float* B, int64_t ldb, uint16_t* A1, uint16_t* A2, int64_t ldpa, uint16_t* B1,
-                        uint16_t* B2, int64_t ldpb, int32_t* d_sblk, int32_t* d_smat) {
-    if (!h || M < 0 || N < 0 || K < 0) return SPLIT3_ERR_INVALID_VALUE;
-    if (M == 0 || N == 0 || K == 0) { h->last_launches = 0; return SPLIT3_OK; }
-    if (!A || !B || !A1 || !A2 || !B1 || !B2 || !d_sblk || !d_smat || lda < K || ldb < N || ldpa < K || ldpb < N ||
-        ldpa % 8 || ldpb % 8 || !aligned(A1, 16) || !aligned(A2, 16) || !aligned(B1, 16) || !aligned(B2, 16))
-        return SPLIT3_ERR_INVALID_VALUE;
-    if (split3::bsplit_blocks(M, N) > kMaxBsplitBlocks) return SPLIT3_ERR_NOT_IMPLEMENTED;
-    if (!h->ws || h->ws_bytes < split3::bsplit_scratch_bytes(M, N, h->num_sms)) return SPLIT3_ERR_WORKSPACE;
-    if (set_dev(h)) return SPLIT3_ERR_CUDA;
-    int n = split3::launch_bsplit(h->stream, A, lda, M, K, B, ldb, N, A1, A2, ldpa, B1, B2, ldpb, h->ws, d_sblk, d_smat,
-                                  bsplit_cnt(h), bsplit_ticket(h), h->num_sms, h->l2_bytes);
-    if (n == -2) return SPLIT3_ERR_NOT_IMPLEMENTED;
     if (n < 0) return SPLIT3_ERR_CUDA;
     h->last_launches = n;
     return SPLIT3_OK;
@@ -593,23 +551,8 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
             prepped = true;
         }
     }
-    // a1 + a2 in one pass with block exponents: both operands fp32 and stored
-    // row-major (A K-major planes, B MN-major planes), not fused, not a one-launch small call
-    int32_t* sblk = nullptr;
-    if (!prepped && fast_max && !fuse_b && h->block_scale && h->mn_major && !A->trans && !B->trans && !small_call &&
-        split3::bsplit_blocks(M, N) <= kMaxBsplitBlocks) {
-        // block exponents after the scratch's own arrays (the GEMM reads them)
-        sblk = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(w.bs) + bsplit_region(M, N)) -
-               (split3::bsplit_blocks(M, N) + 2);
-        n = split3::launch_bsplit(h->stream, A->data, A->ld, M, K, B->data, B->ld, N, w.A1, w.A2, w.ldpa, w.B1t, w.B2t,
-                                  w.ldpb_mn, w.bs, sblk, sblk + split3::bsplit_blocks(M, N), bsplit_cnt(h),
-                                  bsplit_ticket(h), h->num_sms, h->l2_bytes);
-        if (n == -1) return SPLIT3_ERR_CUDA;
-        if (n == -2) sblk = nullptr;   // not co-residable / too large: the two-pass split below
-        else launches += n;
-    }
     // a1: per-matrix max-abs (reading R1) of the fp32 operands (max|op(X)| = max|X|)
-    if (prepped || sblk) {
+    if (prepped) {
     } else if (fast_max) {
         const int64_t ra = A->trans ? K : M, ca = A->trans ? M : K;
         const int64_t rb = B->trans ? N : K, cb = B->trans ? K : N;
@@ -625,7 +568,7 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
             return SPLIT3_ERR_CUDA;
         launches += n;
     }
-    if (needB && !(needA && !check) && !prepped && !sblk) {
+    if (needB && !(needA && !check) && !prepped) {
         const int64_t r = B->trans ? N : K, c = B->trans ? K : N;
         if ((n = split3::launch_maxabs(h->stream, r, c, B->data, B->ld, w.maxB, check ? w.badB : nullptr, h->num_sms)) < 0)
             return SPLIT3_ERR_CUDA;
@@ -649,9 +592,7 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     // pre-split planes of the stored matrix: A stored K x M (trans) is MN-major, B stored K x N
     // (not trans) is MN-major; the other two cases are K-major
     const bool a_mn = (needA && A->trans && h->mn_major) || (!needA && A->stored && A->trans);
-    if (sblk) {
-        A1 = w.A1; A2 = w.A2; sA = sblk; ldpa = w.ldpa;
-    } else if (prepped) {
+    if (prepped) {
         A1 = w.A1; A2 = w.A2; sA = w.sA; ldpa = a_mn ? w.ldpa_mn : w.ldpa;
     } else if (needA && a_mn) {
         if ((n = split3::launch_split(h->stream, K, M, A->data, A->ld, w.maxA, w.A1, w.A2, w.ldpa_mn, w.sA,
@@ -667,8 +608,6 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     const bool b_mn = (needB && !B->trans && (h->mn_major || fuse_b)) || (!needB && B->stored && !B->trans);
     if (fuse_b) {
         sB = w.sB;   // written by the GEMM (the planes never reach HBM)
-    } else if (sblk) {
-        B1t = w.B1t; B2t = w.B2t; sB = sblk + (M + 127) / 128; ldpb = w.ldpb_mn;
     } else if (prepped) {
         B1t = w.B1t; B2t = w.B2t; sB = w.sB; ldpb = b_mn ? w.ldpb_mn : w.ldpb;
     } else if (needB && b_mn) {
@@ -696,7 +635,7 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     n = split3::launch_gemm3(h->stream, M, N, K, A1, A2, ldpa, sA, B1t, B2t, ldpb, sB, C, ldc, terms,
                              gemm_sms(h), h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune,
                              h->split_k ? partial : nullptr, partial_elems, &err, nullptr, nullptr, (b_mn ? 1 : 0) | (a_mn ? 2 : 0),
-                             fuse_b ? B->data : nullptr, B->ld, w.maxB, sblk ? 3 : 0);
+                             fuse_b ? B->data : nullptr, B->ld, w.maxB);
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
     launches += n;
@@ -836,12 +775,6 @@ int split3_set_wave_sync(split3_handle_t h, int enable) {
 int split3_set_split_k(split3_handle_t h, int enable) {
     if (!h) return SPLIT3_ERR_INVALID_VALUE;
     h->split_k = enable != 0;
-    return SPLIT3_OK;
-}
-
-int split3_set_block_scale(split3_handle_t h, int enable) {
-    if (!h) return SPLIT3_ERR_INVALID_VALUE;
-    h->block_scale = enable != 0;
     return SPLIT3_OK;
 }
 

@@ -686,9 +686,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         // warp w reads TMEM lane quadrant (w % 4) and columns [NCOL * half, + NCOL).
         const int quad = warp & 3;
         const int half = (warp - 2) >> 2;
-        // scale exponents: per matrix, or (tune.sblk, the block-scaled split) per 128-row block of
-        // A (this CTA's half of the tile) and per 128-column block of B (this warp's columns)
-        const int sAB0 = tune.sblk ? 0 : *d_sA + (FB ? scale_exp_dev(*fb_maxB) : *d_sB);
+        const int sAB = *d_sA + (FB ? scale_exp_dev(*fb_maxB) : *d_sB);
+        const bool fast = sAB >= -126 && sAB <= 127;
+        const float fscale = fast ? __uint_as_float((unsigned)(sAB + 127) << 23) : 1.0f;
         const bool vec_ok = (ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(C) & 15u) == 0);
         const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * NCOL);
         uint32_t cc = 0, tc = 0;
@@ -753,11 +753,6 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                         make_float4(master[4 * j], master[4 * j + 1], master[4 * j + 2], master[4 * j + 3]);
                 continue;
             }
-            const int sAB = tune.sblk ? d_sA[(tune.sblk & 1) ? mb * 2 + crank : 0] +
-                                            d_sB[(tune.sblk & 2) ? ((nb * BN_ + half * NCOL) >> 7) : 0]
-                                      : sAB0;
-            const bool fast = sAB >= -126 && sAB <= 127;
-            const float fscale = fast ? __uint_as_float((unsigned)(sAB + 127) << 23) : 1.0f;
             if (fast) {                                  // warp-uniform branch
 #pragma unroll
                 for (int j = 0; j < NCOL; j++) master[j] = master[j] * fscale;
@@ -838,22 +833,18 @@ __global__ void __launch_bounds__(256) ksplit_reduce_kernel(const float* __restr
                                                             int64_t M, int64_t N, int group_m,
                                                             float* __restrict__ C, int64_t ldc,
                                                             const int32_t* __restrict__ d_sA,
-                                                            const int32_t* __restrict__ d_sB, int sblk) {
+                                                            const int32_t* __restrict__ d_sB) {
     pdl_enter();
+    const int sAB = *d_sA + *d_sB;
+    const bool fast = sAB >= -126 && sAB <= 127;
+    const float f = fast ? __uint_as_float((unsigned)(sAB + 127) << 23) : 1.0f;
+    const double fd = __longlong_as_double((long long)(sAB + 1023) << 52);
+    auto scale = [&](float a) { return fast ? a * f : __double2float_rn(__dmul_rn((double)a, fd)); };
     const int64_t blk = (int64_t)(2 * BM) * bn;
     const int64_t t = blockIdx.y;
     const int64_t num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + bn - 1) / bn;
     int64_t mb, nb;
     tile_coords(plan.whole + t, num_m, num_n, group_m, mb, nb);
-    // per-matrix exponents, or per 128-row block of A / 128-column block of B (block-scaled split;
-    // a thread's rows all lie in one 128-row half: blockIdx.x * kReduceRows .. + kReduceRows)
-    const int r_first = blockIdx.x * kReduceRows;
-    const int64_t col0 = nb * bn + 4 * (threadIdx.x % (bn / 4));
-    const int sAB = d_sA[(sblk & 1) ? mb * 2 + r_first / BM : 0] + d_sB[(sblk & 2) ? (col0 >> 7) : 0];
-    const bool fast = sAB >= -126 && sAB <= 127;
-    const float f = fast ? __uint_as_float((unsigned)(sAB + 127) << 23) : 1.0f;
-    const double fd = __longlong_as_double((long long)(sAB + 1023) << 52);
-    auto scale = [&](float a) { return fast ? a * f : __double2float_rn(__dmul_rn((double)a, fd)); };
     const int groups = bn / 4;                       // float4 column groups per row
     const int rows_per_pass = 256 / groups;
     const int g = threadIdx.x % groups;
@@ -1025,7 +1016,7 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
                  const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB, float* C, int64_t ldc,
                  int terms, int num_sms, int promo_kb, unsigned* wave_counter, const GemmTuneIn& tin,
                  float* partial, int64_t partial_elems, int* err, const uint16_t* A3, const uint16_t* B3t,
-                 int mn, const float* Bf, int64_t ldb, const float* d_maxB, int sblk) {
+                 int mn, const float* Bf, int64_t ldb, const float* d_maxB) {
     const bool b_mn = (mn & 1) != 0, a_mn = (mn & 2) != 0;
     CUtensorMap ma1, ma2, mb1, mb2, ma3, mb3;
     if (Bf) {   // fused B (3-term): fp32 B map in place of the B plane maps
@@ -1068,7 +1059,6 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     auto pol = [](int p) { return p == 1 ? kPolicyFirst : (p == 2 ? kPolicyLast : kPolicyNormal); };
     tune.pol_a = pol(tin.pol_a);
     tune.pol_b = pol(tin.pol_b);
-    tune.sblk = Bf ? 0 : sblk;
     SplitPlan plan = gemm3_split_plan(M, N, K, terms, num_sms, promo);
     if (plan.slices > 1 && (!partial || gemm3_partial_elems(plan, terms) > partial_elems)) {
         plan.whole += plan.nsplit;   // no room for partials: whole tiles only
@@ -1089,8 +1079,7 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     if (plan.slices > 1) {
         const int bn = terms == 4 ? 128 : 256;
         const dim3 grid((unsigned)(2 * BM / kReduceRows), (unsigned)plan.nsplit);
-        launch_k(ksplit_reduce_kernel, grid, dim3(256), 0, st, partial, plan, bn, M, N, tune.group_m, C, ldc, d_sA, d_sB,
-                 tune.sblk);
+        launch_k(ksplit_reduce_kernel, grid, dim3(256), 0, st, partial, plan, bn, M, N, tune.group_m, C, ldc, d_sA, d_sB);
         if (cudaPeekAtLastError() != cudaSuccess) { *err = 4; return -1; }
         r += 1;
     }

@@ -102,19 +102,6 @@ int launch_host_scale_check(cudaStream_t s, const unsigned* maxblk, const unsign
 int launch_split(cudaStream_t s, int64_t rows, int64_t cols, const float* X, int64_t ld,
                  const float* d_max, uint16_t* hi, uint16_t* lo, int64_t ldp, int32_t* d_sexp,
                  int num_sms);
-// Block-scaled single-pass split: A row blocks and B column blocks of 128, each
-// with its own scale exponent; planes as launch_split (A K-major M x K, B MN-major K x N).
-// scratch: bsplit_scratch_bytes(); sblk receives the block exponents (A blocks, then B blocks),
-// s_mat the per-matrix exponents [sA, sB] (both may be NULL: kept in the scratch); cnt:
-// bsplit_blocks() zeroed words and ticket one zeroed word (left zero).  Returns 2 (bsplit + fixup kernels), -2 if the cooperative
-// launch was rejected (nothing enqueued), -1 on a launch error.
-constexpr int kBsplitCtasPerSm = 4;
-int64_t bsplit_blocks(int64_t M, int64_t N);
-size_t bsplit_scratch_bytes(int64_t M, int64_t N, int num_sms);
-int launch_bsplit(cudaStream_t s, const float* A, int64_t lda, int64_t M, int64_t K, const float* B, int64_t ldb,
-                  int64_t N, uint16_t* A1, uint16_t* A2, int64_t ldpa, uint16_t* B1, uint16_t* B2, int64_t ldpb,
-                  void* scratch, int32_t* sblk, int32_t* s_mat, unsigned* cnt, unsigned* ticket,
-                  int num_sms, int64_t l2_bytes);
 // bf16 x 3 planes (no scale); transpose as for launch_split_t
 int launch_split_bf16x3(cudaStream_t s, int64_t rows, int64_t cols, const float* X, int64_t ld, uint16_t* p1,
                         uint16_t* p2, uint16_t* p3, int64_t ldp, int transpose, int num_sms);
@@ -136,7 +123,6 @@ struct GemmTuneIn {
 struct GemmTune {
     int group_m;
     uint64_t pol_a, pol_b;
-    int sblk;   // bit 0: d_sA holds one exponent per 128-row block of A; bit 1: d_sB per 128-column block of B
 };
 
 // Work split of the persistent GEMM: `whole` tiles run over the full K; the last `nsplit` tiles
@@ -157,8 +143,6 @@ int64_t gemm3_partial_elems(const SplitPlan& p, int terms);   // floats of parti
 // Fused B (terms == 3 only): Bf != NULL is the fp32 B itself (mn bit 0: K x N
 // row-major, else stored N x K; ldb % 4 == 0, 16-B aligned) and d_maxB its max-abs; the GEMM splits
 // it in shared memory (B1t/B2t are ignored) and writes the scale exponent to d_sB.
-// sblk (block-scaled split): bit 0 -> d_sA[i] is the exponent of A's rows
-// [128 i, 128 i + 128), bit 1 -> d_sB[j] that of B's columns [128 j, 128 j + 128).
 // Returns kernels launched (1, or 2 with the split-K reduction) or -1 (*err set to a status).
 int launch_gemm3(cudaStream_t s, int64_t M, int64_t N, int64_t K,
                  const uint16_t* A1, const uint16_t* A2, int64_t ldpa, const int32_t* d_sA,
@@ -166,7 +150,7 @@ int launch_gemm3(cudaStream_t s, int64_t M, int64_t N, int64_t K,
                  float* C, int64_t ldc, int terms, int num_sms, int promo_kb,
                  unsigned* wave_counter, const GemmTuneIn& tune, float* partial, int64_t partial_elems,
                  int* err, const uint16_t* A3 = nullptr, const uint16_t* B3t = nullptr, int mn = 0,
-                 const float* Bf = nullptr, int64_t ldb = 0, const float* d_maxB = nullptr, int sblk = 0);
+                 const float* Bf = nullptr, int64_t ldb = 0, const float* d_maxB = nullptr);
 
 // ---- mlp_kernels.cu (NEXT #3: the non-GEMM steps of a dense-network training step) --------
 int launch_bias_act(cudaStream_t s, int64_t M, int64_t N, const float* Z, int64_t ldz, const float* b, float* H,

@@ -624,239 +624,6 @@ __global__ void __launch_bounds__(256) split_bf3_t_kernel(const float* __restric
     }
 }
 
-
-// ---- block-scaled single-pass split --------------------------------------
-// a1 + a2 of both operands in ONE pass over HBM: every 128-row block of A (128 x K) and every
-// 128-column block of B (K x 128) gets its own scale exponent s_b (rule R1 applied to the block's
-// max), so the block can be split right after its max is known — its data is re-read from L2, not
-// HBM (8 B/element instead of 12).  The GEMM epilogue applies 2^(sA_i + sB_j) per 128 x 128 piece
-// of each tile.  A block exponent below the per-matrix one scales the block's x', planes and every
-// partial sum by an exact power of two, so C keeps the per-matrix bits — unless the block holds a
-// nonzero |x| < 2^(s - 12) (s the per-matrix exponent), whose fp16-subnormal rounding would differ:
-// the last CTA flags such blocks and gives them the per-matrix exponent, and bsplit_fixup_kernel
-// re-splits them before the GEMM.
-//
-// Work: the grid (cooperative: all CTAs co-resident) is cut into G groups of gs CTAs; group g
-// takes blocks g, g + G, ...  Per block: phase 1 folds max |x| and min nonzero |x| over the group
-// (partials + a counter barrier), phase 2 re-reads the block and writes both planes.  G is chosen
-// so that G blocks in flight fit in L2 (launch_bsplit).
-struct BSplitArgs {
-    const float* A; int64_t lda, M, K;   // A row blocks: rows [128 b, +128) x all K columns
-    const float* B; int64_t ldb, N;      // B column blocks: all K rows x columns [128 b, +128)
-    uint16_t *A1, *A2; int64_t ldpa;     // K-major M x K planes
-    uint16_t *B1, *B2; int64_t ldpb;     // MN-major K x N planes
-    int nbA, nbB, groups;
-    unsigned* part;       // [nb][gs][2] CTA partials (max bits, min-nonzero bits)
-    int32_t* sblk;        // [nbA + nbB] block exponents (A blocks first)
-    unsigned* blk;        // [nb][2] block max / min-nonzero bits
-    int32_t* flags;       // [0] count, [1..] flagged blocks
-    int32_t* s_mat;       // [2] per-matrix exponents of A and B
-    unsigned* cnt;        // [nb] barrier counters (zero on entry; the last CTA re-zeroes them)
-    unsigned* ticket;     // zero on entry, left zero
-};
-
-struct BlockGeom {
-    const float* X; int64_t ld; uint16_t *hi, *lo; int64_t ldp;
-    int64_t r0, nr, c0, nc;
-};
-__device__ __forceinline__ BlockGeom bsplit_geom(const BSplitArgs& a, int b) {
-    BlockGeom g;
-    if (b < a.nbA) {
-        g.X = a.A; g.ld = a.lda; g.hi = a.A1; g.lo = a.A2; g.ldp = a.ldpa;
-        g.r0 = 128 * (int64_t)b; g.nr = min((int64_t)128, a.M - g.r0); g.c0 = 0; g.nc = a.K;
-    } else {
-        g.X = a.B; g.ld = a.ldb; g.hi = a.B1; g.lo = a.B2; g.ldp = a.ldpb;
-        g.r0 = 0; g.nr = a.K; g.c0 = 128 * (int64_t)(b - a.nbA); g.nc = min((int64_t)128, a.N - g.c0);
-    }
-    return g;
-}
-
-// visit the block's quads (4 consecutive columns of a row) i = first, first + stride, ... with
-// U loads in flight; fn(row, col, v, nvalid) gets the quad's values (nvalid < 4 at a ragged edge).
-// 32-bit quad indices: launch_bsplit requires 128 * ceil(K / 4) < 2^31.
-template <bool VEC, int U, typename Fn>
-__device__ __forceinline__ void bsplit_walk(const BlockGeom& g, int first, int stride, bool last_use, Fn fn) {
-    const int nq = (int)((g.nc + 3) / 4);
-    const int total = (int)g.nr * nq;
-    const int sdiv = stride / nq, smod = stride % nq;
-    const int ncol = (int)g.nc;
-    const float* base = g.X + g.r0 * g.ld + g.c0;
-    int row = first / nq, q = first % nq;
-    for (int i = first; i < total; i += U * stride) {
-        float4 v[U];
-        int rr[U], cq[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            rr[u] = row;
-            cq[u] = i + u * stride < total ? q : -1;
-            if (cq[u] >= 0) {
-                const float* p = base + (int64_t)row * g.ld + 4 * q;
-                const int left = ncol - 4 * q;
-                if (VEC && left >= 4) {
-                    v[u] = last_use ? __ldcs(reinterpret_cast<const float4*>(p)) : *reinterpret_cast<const float4*>(p);
-                } else {
-                    v[u].x = p[0];
-                    v[u].y = left > 1 ? p[1] : 0.0f;
-                    v[u].z = left > 2 ? p[2] : 0.0f;
-                    v[u].w = left > 3 ? p[3] : 0.0f;
-                }
-            }
-            row += sdiv;
-            q += smod;
-            if (q >= nq) { q -= nq; row++; }
-        }
-#pragma unroll
-        for (int u = 0; u < U; u++)
-            if (cq[u] >= 0) {
-                const int left = ncol - 4 * cq[u];
-                fn(rr[u], 4 * cq[u], v[u], left < 4 ? left : 4);
-            }
-    }
-}
-
-__device__ __forceinline__ void fold_maxmin(float x, unsigned& mx, unsigned& mn) {
-    const unsigned u = __float_as_uint(x) & 0x7FFFFFFFu;
-    if (u < kFiniteLimit) {
-        mx = max(mx, u);
-        if (u) mn = min(mn, u);
-    }
-}
-
-__device__ __forceinline__ void bsplit_store(const BlockGeom& g, int row, int col, float4 v, int nv, float f) {
-    uint16_t* h = g.hi + (g.r0 + row) * g.ldp + g.c0 + col;   // col: relative to the block
-    uint16_t* l = g.lo + (g.r0 + row) * g.ldp + g.c0 + col;
-    if (nv == 4) {
-        uint2 hv, lv;
-        split4(v, f, hv, lv);
-        __stcs(reinterpret_cast<uint2*>(h), hv);
-        __stcs(reinterpret_cast<uint2*>(l), lv);
-    } else {
-        const float xs[4] = {v.x, v.y, v.z, v.w};
-        for (int j = 0; j < nv; j++) {
-            unsigned short a, b;
-            split1(xs[j], f, a, b);
-            h[j] = a;
-            l[j] = b;
-        }
-    }
-}
-
-template <bool VEC>
-__global__ void __launch_bounds__(256, kBsplitCtasPerSm) bsplit_kernel(const BSplitArgs a) {
-    pdl_wait();
-    __shared__ unsigned red[2][8];
-    __shared__ int s_exp;
-    __shared__ bool last;
-    const int nb = a.nbA + a.nbB;
-    const int gs = (int)gridDim.x / a.groups;
-    const int grp = (int)blockIdx.x / gs, c = (int)blockIdx.x % gs;
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    if (grp < a.groups) {
-        for (int b = grp; b < nb; b += a.groups) {
-            const BlockGeom g = bsplit_geom(a, b);
-            const int first = c * (int)blockDim.x + t, stride = gs * (int)blockDim.x;
-            // phase 1: max |x| and min nonzero |x| over finite entries (L2 keeps the block)
-            unsigned mx = 0, mn = 0xFFFFFFFFu;
-            bsplit_walk<VEC, 4>(g, first, stride, false, [&](int, int, float4 v, int nv) {
-                fold_maxmin(v.x, mx, mn);
-                if (nv > 1) fold_maxmin(v.y, mx, mn);
-                if (nv > 2) fold_maxmin(v.z, mx, mn);
-                if (nv > 3) fold_maxmin(v.w, mx, mn);
-            });
-            for (int o = 16; o > 0; o >>= 1) {
-                mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-                mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-            }
-            if (lane == 0) { red[0][w] = mx; red[1][w] = mn; }
-            __syncthreads();
-            if (t == 0) {
-                for (int i = 1; i < (int)(blockDim.x >> 5); i++) { mx = max(mx, red[0][i]); mn = min(mn, red[1][i]); }
-                a.part[((int64_t)b * gs + c) * 2] = mx;
-                a.part[((int64_t)b * gs + c) * 2 + 1] = mn;
-                __threadfence();
-                atomicAdd(&a.cnt[b], 1u);
-                unsigned v;
-                do {   // group barrier: all gs CTAs of the group are co-resident (cooperative launch)
-                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.cnt + b) : "memory");
-                    if (v < (unsigned)gs) __nanosleep(32);
-                } while (v < (unsigned)gs);
-            }
-            __syncthreads();
-            if (w == 0) {   // fold the group's partials (L2 loads: written by other SMs)
-                mx = 0; mn = 0xFFFFFFFFu;
-                for (int i = lane; i < gs; i += 32) {
-                    mx = max(mx, __ldcg(a.part + ((int64_t)b * gs + i) * 2));
-                    mn = min(mn, __ldcg(a.part + ((int64_t)b * gs + i) * 2 + 1));
-                }
-                for (int o = 16; o > 0; o >>= 1) {
-                    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-                    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-                }
-                if (lane == 0) {
-                    s_exp = scale_exp_dev(__uint_as_float(mx));
-                    if (c == 0) {
-                        a.sblk[b] = s_exp;
-                        a.blk[2 * b] = mx;
-                        a.blk[2 * b + 1] = mn;
-                    }
-                }
-            }
-            __syncthreads();
-            const float f = pow2_neg(s_exp);
-            // phase 2: split with the block's exponent (last use of the fp32 data)
-            bsplit_walk<VEC, 4>(g, first, stride, true,
-                                [&](int r, int col, float4 v, int nv) { bsplit_store(g, r, col, v, nv, f); });
-            __syncthreads();   // s_exp / red reused by the next block
-        }
-    }
-    // the last CTA: per-matrix exponents, the fp16-subnormal check, counters back to zero
-    if (t == 0) {
-        __threadfence();
-        last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!last) {
-        pdl_trigger();
-        return;
-    }
-    __shared__ unsigned gmax[2];
-    if (t < 2) gmax[t] = 0;
-    if (t == 0) a.flags[0] = 0;
-    __syncthreads();
-    for (int b = t; b < nb; b += blockDim.x) atomicMax(&gmax[b < a.nbA ? 0 : 1], __ldcg(a.blk + 2 * b));
-    __syncthreads();
-    const int sA = scale_exp_dev(__uint_as_float(gmax[0])), sB = scale_exp_dev(__uint_as_float(gmax[1]));
-    if (t == 0) { a.s_mat[0] = sA; a.s_mat[1] = sB; }
-    for (int b = t; b < nb; b += blockDim.x) {
-        const int s = b < a.nbA ? sA : sB;
-        const int e = s - 12;                                   // threshold 2^(s - 12) as fp32 bits
-        const unsigned thr = e >= -126 ? (unsigned)(e + 127) << 23 : (e >= -149 ? 1u << (e + 149) : 0u);
-        if (__ldcg(a.sblk + b) != s && __ldcg(a.blk + 2 * b + 1) < thr) {
-            a.sblk[b] = s;                                       // redo with the per-matrix exponent
-            a.flags[1 + atomicAdd(&a.flags[0], 1)] = b;
-        }
-        a.cnt[b] = 0;
-    }
-    __threadfence();
-    __syncthreads();
-    if (t == 0) *a.ticket = 0;
-    pdl_trigger();
-}
-
-// re-split the flagged blocks with their (per-matrix) exponent; nothing to do in the common case
-template <bool VEC>
-__global__ void __launch_bounds__(256) bsplit_fixup_kernel(const BSplitArgs a) {
-    pdl_enter();
-    const int n = *reinterpret_cast<volatile const int32_t*>(a.flags);
-    for (int k = 0; k < n; k++) {
-        const int b = a.flags[1 + k];
-        const BlockGeom g = bsplit_geom(a, b);
-        const float f = pow2_neg(a.sblk[b]);
-        bsplit_walk<VEC, 4>(g, (int)(blockIdx.x * blockDim.x + threadIdx.x), (int)(gridDim.x * blockDim.x), true,
-                            [&](int r, int col, float4 v, int nv) { bsplit_store(g, r, col, v, nv, f); });
-    }
-}
-
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 inline int grid_rows(int64_t rows, int num_sms, int64_t blocks_x) {
@@ -868,60 +635,6 @@ inline int grid_rows(int64_t rows, int num_sms, int64_t blocks_x) {
 }
 
 }  // namespace
-
-int64_t bsplit_blocks(int64_t M, int64_t N) { return (M + 127) / 128 + (N + 127) / 128; }
-
-size_t bsplit_scratch_bytes(int64_t M, int64_t N, int num_sms) {
-    const int64_t nb = bsplit_blocks(M, N);
-    const int64_t maxgrid = (int64_t)num_sms * kBsplitCtasPerSm;
-    // part [nb][gs][2] (gs <= grid) + blk [nb][2] + flags [1 + nb] + (sblk [nb] + s_mat [2] when the
-    // caller does not provide them)
-    return (size_t)(nb * maxgrid * 2 + nb * 2 + 1 + nb + nb + 2) * 4 + 64;
-}
-
-int launch_bsplit(cudaStream_t st, const float* A, int64_t lda, int64_t M, int64_t K, const float* B, int64_t ldb,
-                  int64_t N, uint16_t* A1, uint16_t* A2, int64_t ldpa, uint16_t* B1, uint16_t* B2, int64_t ldpb,
-                  void* scratch, int32_t* sblk, int32_t* s_mat, unsigned* cnt, unsigned* ticket,
-                  int num_sms, int64_t l2_bytes) {
-    if (M <= 0 || N <= 0 || K <= 0) return 0;
-    if (128 * ((K + 3) / 4) >= (int64_t)INT32_MAX || 128 * K >= (int64_t)INT32_MAX) return -2;   // 32-bit quad indices
-    BSplitArgs a;
-    a.A = A; a.lda = lda; a.M = M; a.K = K;
-    a.B = B; a.ldb = ldb; a.N = N;
-    a.A1 = A1; a.A2 = A2; a.ldpa = ldpa;
-    a.B1 = B1; a.B2 = B2; a.ldpb = ldpb;
-    a.nbA = (int)((M + 127) / 128);
-    a.nbB = (int)((N + 127) / 128);
-    const int nb = a.nbA + a.nbB;
-    // blocks in flight: their fp32 data (512 K bytes each) must stay in L2 between the phases
-    const int64_t blk_bytes = 512 * K;
-    int64_t G = (l2_bytes / 2) / (blk_bytes > 0 ? blk_bytes : 1);
-    if (G > 16) G = 16;
-    if (G > nb) G = nb;
-    if (G < 1) G = 1;
-    int64_t grid = (int64_t)num_sms * kBsplitCtasPerSm;
-    grid = grid / G * G;
-    a.groups = (int)G;
-    const int64_t gs = grid / G;
-    unsigned* u = static_cast<unsigned*>(scratch);
-    a.part = u;                              u += nb * gs * 2;
-    a.blk = u;                               u += nb * 2;
-    a.flags = reinterpret_cast<int32_t*>(u); u += 1 + nb;
-    a.sblk = sblk ? sblk : reinterpret_cast<int32_t*>(u);   u += nb;
-    a.s_mat = s_mat ? s_mat : reinterpret_cast<int32_t*>(u);
-    a.cnt = cnt;
-    a.ticket = ticket;
-    const bool vec = lda % 4 == 0 && ldb % 4 == 0 && aligned16(A) && aligned16(B);
-    cudaError_t e = vec ? launch_k_coop(bsplit_kernel<true>, dim3((unsigned)grid), dim3(256), 0, st, a)
-                        : launch_k_coop(bsplit_kernel<false>, dim3((unsigned)grid), dim3(256), 0, st, a);
-    if (e != cudaSuccess) {
-        (void)cudaGetLastError();
-        return -2;   // rejected cooperative launch: the caller uses the two-pass split
-    }
-    if (vec) launch_k(bsplit_fixup_kernel<true>, dim3((unsigned)num_sms * 4), dim3(256), 0, st, a);
-    else launch_k(bsplit_fixup_kernel<false>, dim3((unsigned)num_sms * 4), dim3(256), 0, st, a);
-    return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
-}
 
 int launch_prep2(cudaStream_t st, const PrepOperand& a, const PrepOperand& b, unsigned* partials,
                  unsigned* sync, int num_sms) {

@@ -38,8 +38,8 @@ EXPORTS = (
     "split3_sgemm_host_workspace_size", "split3_sgemm_host", "split3_last_bad_index", "split3_host_redo_count",
     "split3_status_string", "split3_maxabs", "split3_split", "split3_gemm_planes",
     "split3_last_launch_count", "split3_timing_enable", "split3_timing_read",
-    "split3_set_promotion", "split3_set_wave_sync", "split3_set_split_k", "split3_set_max_sms", "split3_set_block_scale", "split3_set_schedule", "split3_set_fused_split",
-    "split3_sgemm_ex", "split3_presplit", "split3_presplit_stored", "split3_split_bf16x3", "split3_split_blocks", "split3_bias_act", "split3_relu_backward",
+    "split3_set_promotion", "split3_set_wave_sync", "split3_set_split_k", "split3_set_max_sms", "split3_set_schedule", "split3_set_fused_split",
+    "split3_sgemm_ex", "split3_presplit", "split3_presplit_stored", "split3_split_bf16x3", "split3_bias_act", "split3_relu_backward",
     "split3_softmax_xent", "split3_bias_grad", "split3_sgd_update",
 )
 
@@ -117,13 +117,10 @@ def load() -> ctypes.CDLL:
         lib.split3_set_wave_sync.argtypes = [_p, ctypes.c_int]
         lib.split3_set_split_k.argtypes = [_p, ctypes.c_int]
         lib.split3_set_max_sms.argtypes = [_p, ctypes.c_int]
-        lib.split3_set_block_scale.argtypes = [_p, ctypes.c_int]
         lib.split3_set_schedule.argtypes = [_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         lib.split3_set_fused_split.argtypes = [_p, ctypes.c_int, _i64]
         lib.split3_sgemm_ex.argtypes = [_p, _i64, _i64, _i64, ctypes.POINTER(split3_matrix),
                                         ctypes.POINTER(split3_matrix), _p, _i64, ctypes.c_uint32]
-        lib.split3_split_blocks.argtypes = [_p, _i64, _i64, _i64, _p, _i64, _p, _i64, _p, _p, _i64, _p, _p, _i64,
-                                            _p, _p]
         lib.split3_split_bf16x3.argtypes = [_p, _i64, _i64, _p, _i64, _p, _p, _p, _i64, ctypes.c_int]
         lib.split3_bias_act.argtypes = [_p, _i64, _i64, _p, _i64, _p, _p, _i64, ctypes.c_int]
         lib.split3_relu_backward.argtypes = [_p, _i64, _i64, _p, _p, _p]
@@ -289,10 +286,6 @@ class Handle:
     def set_split_k(self, enable: bool):
         """Split-K tail on (default) or whole tiles only (deterministic per-element K order)."""
         self._set("split3_set_split_k", int(enable))
-
-    def set_block_scale(self, enable: bool):
-        """Block-scaled single-pass split (default on; C is bitwise the per-matrix-scale result)."""
-        self._set("split3_set_block_scale", int(enable))
 
     def set_max_sms(self, sms: int):
         """Cap the SMs the GEMM occupies (0 = all; even)."""
@@ -522,28 +515,6 @@ class Handle:
         if st != OK:
             raise Split3Error(st, "split3_split")
         return hi, lo, d_sexp
-
-    def split_blocks(self, A: torch.Tensor, B: torch.Tensor):
-        """Block-scaled split of both operands: (A1, A2, B1, B2, sblk, smat) with A's
-        planes M x ldp(K) (K-major), B's K x ldp(N) (MN-major), sblk the exponents of A's 128-row
-        blocks then B's 128-column blocks, smat the per-matrix exponents [sA, sB]."""
-        _check_mat(A, "A")
-        _check_mat(B, "B")
-        M, K = A.shape
-        N = B.shape[1]
-        A1 = torch.empty((M, plane_ld(K)), dtype=torch.int16, device=A.device)
-        A2 = torch.empty_like(A1)
-        B1 = torch.empty((K, plane_ld(N)), dtype=torch.int16, device=A.device)
-        B2 = torch.empty_like(B1)
-        sblk = torch.empty((M + 127) // 128 + (N + 127) // 128, dtype=torch.int32, device=A.device)
-        smat = torch.empty(2, dtype=torch.int32, device=A.device)
-        self._ensure_ws(self.workspace_size(M, N, K))
-        self._bind_stream()
-        st = self._lib.split3_split_blocks(self._h, M, N, K, _ptr(A), _ld(A), _ptr(B), _ld(B), _ptr(A1), _ptr(A2),
-                                           A1.stride(0), _ptr(B1), _ptr(B2), B1.stride(0), _ptr(sblk), _ptr(smat))
-        if st != OK:
-            raise Split3Error(st, "split3_split_blocks")
-        return A1, A2, B1, B2, sblk, smat
 
     def split_bf16x3(self, X: torch.Tensor, transpose: bool = False):
         """bf16 x 3 planes (int16 tensors holding bfloat16 bits) of X, padded leading dimension."""
