@@ -200,6 +200,27 @@ __device__ __forceinline__ void mma_pair(uint32_t d_tmem, uint64_t adesc, uint64
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// The same with the A operand kept in the tensor core's collector buffer (A_KEEP: read from shared
+// memory and keep) or taken from it (A_REUSE: no shared-memory read of A); for two consecutive
+// MMAs that multiply the same A tile (A1 * B1 into D_hi, then A1 * B2 into D_mid).
+__device__ __forceinline__ void mma_pair_keep_a(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16.collector::a::fill [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_pair_reuse_a(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 // arrive (once) on the barrier at this offset in BOTH CTAs of the pair when the MMAs complete
 __device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
     asm volatile(
@@ -635,7 +656,24 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                         }
                         __syncwarp();
                     };
-                    if (hi_first) { issue_hi(); issue_mid(); } else { issue_mid(); issue_hi(); }
+                    // Interleaved (3-term, inside a D_hi chunk, not a unit's last k-block: D_hi needs no
+                    // wait and D_mid is already owned): per K = 16 step A1*B1 -> D_hi keeps A1 in the
+                    // collector and A1*B2 -> D_mid reuses it, so A1 is read from shared memory once
+                    // instead of twice.  Same accumulators, same per-accumulator order: same bits.
+                    const bool interleave = TERMS == 3 && !BF3 && !chunk_start && kb + 1 != kb_end && mid_ready;
+                    if (interleave) {
+                        if (elect_one()) {
+#pragma unroll
+                            for (int k = 0; k < BK / 16; k++) {
+                                const uint64_t dk = DKA * k, dkb = DKB * k;
+                                mma_pair_keep_a(t_hi, a1 + dk, b1 + dkb, IDESC, 1u);
+                                mma_pair_reuse_a(t_mid, a1 + dk, b2 + dkb, IDESC, 1u);
+                                mma_pair(t_mid, a2 + dk, b1 + dkb, IDESC, 1u);
+                            }
+                            if (chunk_end) mma_commit_pair(smem_u32(&hfull_bar[hb]));
+                        }
+                        __syncwarp();
+                    } else if (hi_first) { issue_hi(); issue_mid(); } else { issue_mid(); issue_hi(); }
                     if (elect_one()) {
                         mma_commit_pair(smem_u32(&empty_bar[stage]));        // stage free in both CTAs
                         if (HAS_MID && kb + 1 == kb_end) mma_commit_pair(smem_u32(&mfull_bar[0]));

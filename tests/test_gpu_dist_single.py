@@ -146,3 +146,20 @@ def test_nccl_plane_all_gather_dtype(nccl_one_rank):
     out = _all_gather_rows(bits, dist.group.WORLD, 1)
     torch.cuda.synchronize()
     assert out.dtype == torch.int16 and torch.equal(out, bits)
+
+
+def test_gather_groups_with_cta_budget(nccl_one_rank):
+    """the NCCL sub-groups the driver gathers over are created with config max_ctas (the SMs the
+    overlapped GEMM pieces leave free): creation + an all-gather through one of them"""
+    import torch.distributed as dist
+
+    from paper_2011_11188_b200 import dist as d2
+
+    rows, cols = d2.make_groups(1, gather_ctas=d2.GATHER_CTAS)
+    assert d2.make_groups(1, gather_ctas=d2.GATHER_CTAS) == (rows, cols)      # cached
+    bits = torch.arange(4096, dtype=torch.int32, device="cuda").to(torch.int16).view(64, 64)
+    out = d2._all_gather_rows(bits, rows[0], 1)
+    out2 = d2._all_gather_rows(bits, cols[0], 1)
+    torch.cuda.synchronize()
+    assert torch.equal(out, bits) and torch.equal(out2, bits)
+    assert dist.get_backend(rows[0]) == "nccl"
