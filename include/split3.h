@@ -303,6 +303,20 @@ int split3_set_max_sms(split3_handle_t h, int sms);
  * SPLIT3_FUSE_B_MAX_M at handle creation.  INVALID_VALUE for mode outside 0..2 or max_m < 0. */
 int split3_set_fused_split(split3_handle_t h, int mode, int64_t max_m);
 
+/* ---- debug build (libsplit3_debug.so: the same sources with -DSPLIT3_DEBUG=1) ----------------
+ * The GEMM's synchronisation checks that compute-sanitizer would provide (it is not usable on this
+ * GPU pool), built in: a watchdog on every mbarrier wait (2 s), checks of the TMEM
+ * allocation, the shared-memory carve-out, tile coordinates and k-block ranges, D_hi chunks issued
+ * vs drained, and the wave-lockstep counter.  The first failure is recorded (out8[0] = code,
+ * [1] = detail, [2] = CTA, [3] = warp, [4] = number of failures); a watchdog trip makes every
+ * later wait return, so a broken pipeline ends the kernel instead of hanging the GPU (its C is
+ * garbage).  Results of the debug build are bitwise those of the release build.
+ * split3_debug_read copies the record (reset != 0 clears it); split3_debug_fault(1) injects a
+ * missing TMA load into the next GEMM launches (tests), 0 clears it.  Process-wide (device
+ * globals of the current device).  Release build: SPLIT3_ERR_NOT_IMPLEMENTED. */
+int split3_debug_read(uint64_t *out8, int reset);
+int split3_debug_fault(int fault);
+
 /* ---- measurement hooks (bench.py's roofline; no effect on results) ---------------------- */
 
 /* enable != 0: every following split3_sgemm records CUDA events on the handle's stream around

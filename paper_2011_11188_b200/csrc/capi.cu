@@ -772,6 +772,18 @@ int split3_set_wave_sync(split3_handle_t h, int enable) {
     return SPLIT3_OK;
 }
 
+int split3_debug_read(uint64_t* out8, int reset) {
+    if (!out8) return SPLIT3_ERR_INVALID_VALUE;
+    const int r = split3::gemm3_debug_read(reinterpret_cast<unsigned long long*>(out8), reset);
+    return r > 0 ? SPLIT3_OK : (r == 0 ? SPLIT3_ERR_NOT_IMPLEMENTED : SPLIT3_ERR_CUDA);
+}
+
+int split3_debug_fault(int fault) {
+    if (fault < 0 || fault > 1) return SPLIT3_ERR_INVALID_VALUE;
+    const int r = split3::gemm3_debug_fault(fault);
+    return r > 0 ? SPLIT3_OK : (r == 0 ? SPLIT3_ERR_NOT_IMPLEMENTED : SPLIT3_ERR_CUDA);
+}
+
 int split3_set_split_k(split3_handle_t h, int enable) {
     if (!h) return SPLIT3_ERR_INVALID_VALUE;
     h->split_k = enable != 0;

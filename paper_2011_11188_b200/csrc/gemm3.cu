@@ -111,8 +111,53 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar & PEER_MASK) : "memory");
 }
+// ---- debug build (SPLIT3_DEBUG=1: libsplit3_debug.so) ----------------------
+// What compute-sanitizer would check in this kernel's synchronisation, built in: every mbarrier
+// wait has a watchdog (kDbgWatchdogNs of globaltimer); the first failure is recorded in g_dbg
+// (code, detail, CTA, warp; count) and sets g_dbg_abort, after which every wait returns and every
+// role leaves its loop, so a broken pipeline ends the kernel with a report instead of hanging the
+// GPU.  Codes: 1 mbarrier watchdog (detail = barrier smem address << 32 | parity), 2 TMEM base
+// not column 0, 3 tile coordinates out of range, 4 shared-memory carve-out beyond the dynamic
+// allocation, 5 empty k-block range, 6 D_hi chunks issued != chunks drained, 7 wave counter not
+// back to 0.  g_dbg_fault (split3_debug_fault) injects a missing TMA load (1) for the tests.
+#ifndef SPLIT3_DEBUG
+#define SPLIT3_DEBUG 0
+#endif
+#if SPLIT3_DEBUG
+constexpr uint64_t kDbgWatchdogNs = 2000000000ull;
+__device__ unsigned long long g_dbg[8];
+__device__ unsigned g_dbg_abort;
+__device__ int g_dbg_fault;
+__device__ __noinline__ void dbg_report(unsigned code, unsigned long long detail) {
+    if (atomicCAS(&g_dbg[0], 0ull, (unsigned long long)code) == 0ull) {
+        g_dbg[1] = detail;
+        g_dbg[2] = blockIdx.x;
+        g_dbg[3] = threadIdx.x >> 5;
+    }
+    atomicAdd(&g_dbg[4], 1ull);
+}
+__device__ __forceinline__ bool dbg_aborted() { return *reinterpret_cast<volatile unsigned*>(&g_dbg_abort) != 0; }
+#define DBG_CHECK(cond, code, detail) \
+    do {                               \
+        if (!(cond)) dbg_report((code), (unsigned long long)(detail)); \
+    } while (0)
+#define DBG_BREAK_IF_ABORTED() \
+    if (dbg_aborted()) break
+#else
+#define DBG_CHECK(cond, code, detail) \
+    do {                               \
+    } while (0)
+#define DBG_BREAK_IF_ABORTED() \
+    do {                        \
+    } while (0)
+#endif
+
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     uint32_t done;
+#if SPLIT3_DEBUG
+    const uint64_t t0 = globaltimer_ns();
+    uint32_t spins = 0;
+#endif
     do {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
@@ -121,6 +166,16 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             : "=r"(done)
             : "r"(bar), "r"(parity)
             : "memory");
+#if SPLIT3_DEBUG
+        if (!done && (++spins & 255u) == 0) {
+            if (dbg_aborted()) return;
+            if (globaltimer_ns() - t0 > kDbgWatchdogNs) {
+                dbg_report(1, ((unsigned long long)bar << 32) | parity);
+                atomicExch(&g_dbg_abort, 1u);
+                return;
+            }
+        }
+#endif
     } while (!done);
 }
 // 2-SM TMA: data lands in this CTA's smem, the transaction bytes on the leader's barrier.
@@ -140,24 +195,6 @@ __device__ __forceinline__ void tma_load_2d_cta(uint32_t dst, const CUtensorMap*
         " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y), "l"(policy)
         : "memory");
-}
-// arrive on the LEADER's barrier, releasing this thread's prior writes at cluster scope (the
-// converters' plane stores, read by the leader-issued MMAs)
-__device__ __forceinline__ void mbar_arrive_leader_cluster(uint32_t bar) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar & PEER_MASK) : "memory");
-}
-// wait with acquire at cluster scope (pairs with mbar_arrive_leader_cluster)
-__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
-    uint32_t done;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    } while (!done);
 }
 // TMA store of a shared-memory box to global (bulk async group of the issuing thread)
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int32_t x, int32_t y) {
@@ -498,6 +535,16 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_wait();   // prologue above overlaps the predecessor's tail; no global access before here
+#if SPLIT3_DEBUG
+    if (threadIdx.x == 0) {
+        DBG_CHECK(tmem_base == 0, 2, tmem_base);   // all 512 columns allocated: base lane 0, column 0
+        uint32_t dyn;
+        asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+        const uint32_t used = (uint32_t)(reinterpret_cast<uint8_t*>(tmem_slot + 1) - smem_raw);
+        DBG_CHECK(used <= dyn, 4, ((unsigned long long)used << 32) | dyn);
+    }
+    __shared__ uint32_t dbg_chunks;                   // D_hi chunks the MMA warp committed (leader)
+#endif
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs; warp-uniform, one elected lane) =====
@@ -518,6 +565,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             }
             int64_t mb, nb;
             tile_coords(tile, num_m, num_n, tune.group_m, mb, nb);
+            DBG_CHECK(mb >= 0 && mb < num_m && nb >= 0 && nb < num_n, 3, ((unsigned long long)mb << 32) | (unsigned)nb);
+            DBG_CHECK(kb_begin < kb_end && kb_end <= num_kb, 5, ((unsigned long long)kb_begin << 32) | (unsigned)kb_end);
+            DBG_BREAK_IF_ABORTED();
             const int32_t y_a = (int32_t)(mb * 2 * BM + crank * BM);
             const int32_t y_b = (int32_t)(nb * BN_ + crank * BNH);
             for (int kb = kb_begin; kb < kb_end; kb++) {
@@ -554,6 +604,11 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                         if (BMN) tma_load_2d_cta(smem_u32(st + B_OFF), &mapB1, ffb, y_b, x, tune.pol_b);   // 128 N x 64 K
                         else tma_load_2d_cta(smem_u32(st + B_OFF), &mapB1, ffb, x, y_b, tune.pol_b);       // 64 K x 128 N
                     }
+#if SPLIT3_DEBUG
+                    // injected fault (tests): the first unit's second k-block loses its A1 load, so
+                    // the full barrier's transaction count is never reached
+                    if (!(g_dbg_fault == 1 && idx == 0 && kb == kb_begin + 1))
+#endif
                     load_a(0, &mapA1);
                     if (!FB) load_b(B_OFF, &mapB1);
                     if (LOAD_LO) {
@@ -682,7 +737,12 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 cc++;
+                DBG_BREAK_IF_ABORTED();
             }
+#if SPLIT3_DEBUG
+            if (elect_one()) dbg_chunks = cc;
+            __syncwarp();
+#endif
         }
     } else if (FB && warp >= 2 + NUM_EPI_WARPS) {
         // ===================== fused-B converters (warps 10..11, both CTAs) ================
@@ -718,6 +778,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                 __syncwarp();
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
+            DBG_BREAK_IF_ABORTED();
         }
     } else {
         // ===================== epilogue (warps 2..9, both CTAs) =====================
@@ -731,6 +792,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * NCOL);
         uint32_t cc = 0, tc = 0;
         for (int64_t unit = pair; unit < num_units; unit += num_pairs, tc++) {
+            DBG_BREAK_IF_ABORTED();
             int64_t tile;
             int kb_begin, kb_end, slot;
             decode_unit(unit, plan, num_kb, kps, tile, kb_begin, kb_end, slot);
@@ -843,13 +905,35 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     }
 
     if (warp >= 2 && warp < 2 + NUM_EPI_WARPS && tma_store && lane == 0) bulk_wait0();   // C stores done
+#if SPLIT3_DEBUG
+    uint32_t dbg_epi_chunks = 0;     // warp 2's drained D_hi chunk count (recomputed: same loop shape)
+    if (warp == 2 && leader) {
+        for (int64_t unit = pair; unit < num_units; unit += num_pairs) {
+            int64_t tile_unused;
+            int kb_begin, kb_end, slot;
+            decode_unit(unit, plan, num_kb, kps, tile_unused, kb_begin, kb_end, slot);
+            dbg_epi_chunks += (uint32_t)((kb_end - kb_begin + promo_kb - 1) / promo_kb);
+        }
+    }
+#endif
     tc_fence_before();
     cluster_sync();
+#if SPLIT3_DEBUG
+    if (warp == 2 && leader && lane == 0 && !dbg_aborted() && pair < num_units)
+        DBG_CHECK(dbg_chunks == dbg_epi_chunks, 6, ((unsigned long long)dbg_chunks << 32) | dbg_epi_chunks);
+#endif
     // Wave-lockstep counter reset: the last CTA to get here (exit ticket, word 3) zeroes the
     // counter, so every launch — eager or a CUDA-graph replay — starts from 0 with no memset.
     if (wave_counter && threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(wave_counter + 3, 1u) == gridDim.x - 1) {
+#if SPLIT3_DEBUG
+            // every producer announced each of its units but the first: 2 CTAs x (units - 1) per pair
+            const int64_t busy = num_units < num_pairs ? num_units : num_pairs;
+            const unsigned expect = (unsigned)(2 * (num_units - busy));
+            const unsigned got = atomicAdd(wave_counter, 0u);
+            if (!dbg_aborted()) DBG_CHECK(got == expect, 7, ((unsigned long long)got << 32) | expect);
+#endif
             atomicExch(wave_counter, 0u);
             atomicExch(wave_counter + 3, 0u);
         }
@@ -1015,6 +1099,32 @@ LaunchFn pick(int mn) {
 }
 
 }  // namespace
+
+int gemm3_debug_read(unsigned long long* out8, int reset) {
+#if SPLIT3_DEBUG
+    if (cudaMemcpyFromSymbol(out8, g_dbg, sizeof(g_dbg)) != cudaSuccess) return -1;
+    if (reset) {
+        const unsigned long long z[8] = {};
+        const unsigned zu = 0;
+        if (cudaMemcpyToSymbol(g_dbg, z, sizeof(z)) != cudaSuccess ||
+            cudaMemcpyToSymbol(g_dbg_abort, &zu, sizeof(zu)) != cudaSuccess)
+            return -1;
+    }
+    return 1;
+#else
+    (void)out8; (void)reset;
+    return 0;
+#endif
+}
+
+int gemm3_debug_fault(int fault) {
+#if SPLIT3_DEBUG
+    return cudaMemcpyToSymbol(g_dbg_fault, &fault, sizeof(fault)) == cudaSuccess ? 1 : -1;
+#else
+    (void)fault;
+    return 0;
+#endif
+}
 
 SplitPlan gemm3_split_plan(int64_t M, int64_t N, int64_t K, int terms, int num_sms, int promo_kb) {
     const int bn = terms == 4 ? 128 : 256;

@@ -39,7 +39,7 @@ EXPORTS = (
     "split3_status_string", "split3_maxabs", "split3_split", "split3_gemm_planes",
     "split3_last_launch_count", "split3_timing_enable", "split3_timing_read",
     "split3_set_promotion", "split3_set_wave_sync", "split3_set_split_k", "split3_set_max_sms", "split3_set_schedule", "split3_set_fused_split",
-    "split3_sgemm_ex", "split3_presplit", "split3_presplit_stored", "split3_split_bf16x3", "split3_bias_act", "split3_relu_backward",
+    "split3_sgemm_ex", "split3_presplit", "split3_presplit_stored", "split3_split_bf16x3", "split3_debug_read", "split3_debug_fault", "split3_bias_act", "split3_relu_backward",
     "split3_softmax_xent", "split3_bias_grad", "split3_sgd_update",
 )
 
@@ -121,6 +121,8 @@ def load() -> ctypes.CDLL:
         lib.split3_set_fused_split.argtypes = [_p, ctypes.c_int, _i64]
         lib.split3_sgemm_ex.argtypes = [_p, _i64, _i64, _i64, ctypes.POINTER(split3_matrix),
                                         ctypes.POINTER(split3_matrix), _p, _i64, ctypes.c_uint32]
+        lib.split3_debug_read.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
+        lib.split3_debug_fault.argtypes = [ctypes.c_int]
         lib.split3_split_bf16x3.argtypes = [_p, _i64, _i64, _p, _i64, _p, _p, _p, _i64, ctypes.c_int]
         lib.split3_bias_act.argtypes = [_p, _i64, _i64, _p, _i64, _p, _p, _i64, ctypes.c_int]
         lib.split3_relu_backward.argtypes = [_p, _i64, _i64, _p, _p, _p]
@@ -140,6 +142,22 @@ def load() -> ctypes.CDLL:
                                            _p, _i64, ctypes.c_uint32]
         _lib = lib
         return lib
+
+
+def debug_read(reset: bool = True):
+    """The debug build's GEMM check record (code, detail, CTA, warp, count, ...); raises
+    Split3Error(NOT_IMPLEMENTED) on a release library."""
+    buf = (ctypes.c_uint64 * 8)()
+    st = load().split3_debug_read(buf, int(reset))
+    if st != OK:
+        raise Split3Error(st, "split3_debug_read")
+    return list(buf)
+
+
+def debug_fault(fault: int):
+    st = load().split3_debug_fault(int(fault))
+    if st != OK:
+        raise Split3Error(st, "split3_debug_fault")
 
 
 def status_string(status: int) -> str:

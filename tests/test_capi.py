@@ -32,6 +32,24 @@ def test_library_exports_every_declared_symbol():
     assert sorted(split3.EXPORTS) == _declared()
 
 
+def test_debug_build_exports_and_release_reports_not_implemented():
+    """the checked build (-DSPLIT3_DEBUG=1) has the same ABI; the release build's
+    debug entry points answer NOT_IMPLEMENTED without touching a GPU"""
+    import ctypes
+
+    from paper_2011_11188_b200 import _build, split3
+
+    if not os.path.exists(_build.DEBUG_LIB):
+        _build.build(force=True, out=_build.DEBUG_LIB, defines=["SPLIT3_DEBUG=1"])
+    dbg = ctypes.CDLL(_build.DEBUG_LIB)
+    for n in _declared():
+        assert hasattr(dbg, n), n
+    with pytest.raises(split3.Split3Error) as e:
+        split3.debug_read()
+    assert e.value.status == split3.ERR_NOT_IMPLEMENTED
+    assert split3.load().split3_debug_fault(5) == split3.ERR_INVALID_VALUE
+
+
 def test_status_strings_without_gpu():
     from paper_2011_11188_b200 import split3
 
