@@ -308,9 +308,10 @@ int split3_set_fused_split(split3_handle_t h, int mode, int64_t max_m);
  * GPU pool), built in: a watchdog on every mbarrier wait (2 s), checks of the TMEM
  * allocation, the shared-memory carve-out, tile coordinates and k-block ranges, D_hi chunks issued
  * vs drained, and the wave-lockstep counter.  The first failure is recorded (out8[0] = code,
- * [1] = detail, [2] = CTA, [3] = warp, [4] = number of failures); a watchdog trip makes every
- * later wait return, so a broken pipeline ends the kernel instead of hanging the GPU (its C is
- * garbage).  Results of the debug build are bitwise those of the release build.
+ * [1] = detail, [2] = CTA, [3] = warp, [4] = number of failures) in host-mapped memory; a watchdog
+ * trip then traps the kernel, so a broken pipeline ends with a launch error (the context is lost;
+ * the record stays readable) instead of hanging the GPU.  Results of the debug build are bitwise
+ * those of the release build.
  * split3_debug_read copies the record (reset != 0 clears it); split3_debug_fault(1) injects a
  * missing TMA load into the next GEMM launches (tests), 0 clears it.  Process-wide (device
  * globals of the current device).  Release build: SPLIT3_ERR_NOT_IMPLEMENTED. */

@@ -229,8 +229,9 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
     const bool ok = cudaSetDevice(device) == cudaSuccess && cudaMalloc(&c->d_counters, kCounterBytes) == cudaSuccess &&
                     cudaMemset(c->d_counters, 0, kCounterBytes) == cudaSuccess &&
                     cudaStreamSynchronize(cudaStreamLegacy) == cudaSuccess;   // zeroed before any stream uses it
+    const bool dbg_ok = !ok || split3::gemm3_debug_init() >= 0;   // debug build: map the check record
     cudaThreadExchangeStreamCaptureMode(&mode);
-    if (!ok) {
+    if (!ok || !dbg_ok) {
         if (c->d_counters) cudaFree(c->d_counters);
         delete c;
         return SPLIT3_ERR_CUDA;

@@ -34,6 +34,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <string.h>
 
 #include "internal.h"
 #include "split_math.h"
@@ -112,43 +113,39 @@ __device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar & PEER_MASK) : "memory");
 }
 // ---- debug build (SPLIT3_DEBUG=1: libsplit3_debug.so) ----------------------
-// What compute-sanitizer would check in this kernel's synchronisation, built in: every mbarrier
-// wait has a watchdog (kDbgWatchdogNs of globaltimer); the first failure is recorded in g_dbg
-// (code, detail, CTA, warp; count) and sets g_dbg_abort, after which every wait returns and every
-// role leaves its loop, so a broken pipeline ends the kernel with a report instead of hanging the
-// GPU.  Codes: 1 mbarrier watchdog (detail = barrier smem address << 32 | parity), 2 TMEM base
-// not column 0, 3 tile coordinates out of range, 4 shared-memory carve-out beyond the dynamic
-// allocation, 5 empty k-block range, 6 D_hi chunks issued != chunks drained, 7 wave counter not
-// back to 0.  g_dbg_fault (split3_debug_fault) injects a missing TMA load (1) for the tests.
+// What compute-sanitizer would check in this kernel's synchronisation, built in.  Every mbarrier
+// wait has a watchdog (kDbgWatchdogNs of globaltimer): on expiry the failure is written to
+// host-mapped pinned memory (readable even after the context is lost) and the kernel traps, so a
+// broken pipeline ends with a report and a launch error instead of a hung GPU.  The other checks
+// record and continue.  Record: [0] first failure code, [1] detail, [2] CTA, [3] warp, [4] number
+// of failures.  Codes: 1 mbarrier watchdog (detail = barrier smem address << 32 | parity), 2 TMEM
+// base not column 0, 3 tile coordinates out of range, 4 shared-memory carve-out beyond the dynamic
+// allocation, 5 empty k-block range, 6 D_hi chunks committed != chunks drained, 7 wave counter not
+// 2 x (units - busy pairs).  g_dbg_fault (split3_debug_fault) injects a missing TMA load (1).
 #ifndef SPLIT3_DEBUG
 #define SPLIT3_DEBUG 0
 #endif
 #if SPLIT3_DEBUG
 constexpr uint64_t kDbgWatchdogNs = 2000000000ull;
-__device__ unsigned long long g_dbg[8];
-__device__ unsigned g_dbg_abort;
+__device__ unsigned long long* g_dbg;   // host-mapped record (gemm3_debug_init)
 __device__ int g_dbg_fault;
 __device__ __noinline__ void dbg_report(unsigned code, unsigned long long detail) {
-    if (atomicCAS(&g_dbg[0], 0ull, (unsigned long long)code) == 0ull) {
+    if (!g_dbg) return;
+    if (atomicCAS_system(&g_dbg[0], 0ull, (unsigned long long)code) == 0ull) {
         g_dbg[1] = detail;
         g_dbg[2] = blockIdx.x;
         g_dbg[3] = threadIdx.x >> 5;
     }
-    atomicAdd(&g_dbg[4], 1ull);
+    atomicAdd_system(&g_dbg[4], 1ull);
+    __threadfence_system();
 }
-__device__ __forceinline__ bool dbg_aborted() { return *reinterpret_cast<volatile unsigned*>(&g_dbg_abort) != 0; }
 #define DBG_CHECK(cond, code, detail) \
     do {                               \
         if (!(cond)) dbg_report((code), (unsigned long long)(detail)); \
     } while (0)
-#define DBG_BREAK_IF_ABORTED() \
-    if (dbg_aborted()) break
 #else
 #define DBG_CHECK(cond, code, detail) \
     do {                               \
-    } while (0)
-#define DBG_BREAK_IF_ABORTED() \
-    do {                        \
     } while (0)
 #endif
 
@@ -167,13 +164,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             : "r"(bar), "r"(parity)
             : "memory");
 #if SPLIT3_DEBUG
-        if (!done && (++spins & 255u) == 0) {
-            if (dbg_aborted()) return;
-            if (globaltimer_ns() - t0 > kDbgWatchdogNs) {
-                dbg_report(1, ((unsigned long long)bar << 32) | parity);
-                atomicExch(&g_dbg_abort, 1u);
-                return;
-            }
+        if (!done && (++spins & 255u) == 0 && globaltimer_ns() - t0 > kDbgWatchdogNs) {
+            dbg_report(1, ((unsigned long long)bar << 32) | parity);
+            __trap();
         }
 #endif
     } while (!done);
@@ -567,7 +560,6 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             tile_coords(tile, num_m, num_n, tune.group_m, mb, nb);
             DBG_CHECK(mb >= 0 && mb < num_m && nb >= 0 && nb < num_n, 3, ((unsigned long long)mb << 32) | (unsigned)nb);
             DBG_CHECK(kb_begin < kb_end && kb_end <= num_kb, 5, ((unsigned long long)kb_begin << 32) | (unsigned)kb_end);
-            DBG_BREAK_IF_ABORTED();
             const int32_t y_a = (int32_t)(mb * 2 * BM + crank * BM);
             const int32_t y_b = (int32_t)(nb * BN_ + crank * BNH);
             for (int kb = kb_begin; kb < kb_end; kb++) {
@@ -737,8 +729,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 cc++;
-                DBG_BREAK_IF_ABORTED();
-            }
+                }
 #if SPLIT3_DEBUG
             if (elect_one()) dbg_chunks = cc;
             __syncwarp();
@@ -778,7 +769,6 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                 __syncwarp();
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
-            DBG_BREAK_IF_ABORTED();
         }
     } else {
         // ===================== epilogue (warps 2..9, both CTAs) =====================
@@ -792,7 +782,6 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * NCOL);
         uint32_t cc = 0, tc = 0;
         for (int64_t unit = pair; unit < num_units; unit += num_pairs, tc++) {
-            DBG_BREAK_IF_ABORTED();
             int64_t tile;
             int kb_begin, kb_end, slot;
             decode_unit(unit, plan, num_kb, kps, tile, kb_begin, kb_end, slot);
@@ -919,7 +908,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     tc_fence_before();
     cluster_sync();
 #if SPLIT3_DEBUG
-    if (warp == 2 && leader && lane == 0 && !dbg_aborted() && pair < num_units)
+    if (warp == 2 && leader && lane == 0 && pair < num_units)
         DBG_CHECK(dbg_chunks == dbg_epi_chunks, 6, ((unsigned long long)dbg_chunks << 32) | dbg_epi_chunks);
 #endif
     // Wave-lockstep counter reset: the last CTA to get here (exit ticket, word 3) zeroes the
@@ -932,7 +921,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             const int64_t busy = num_units < num_pairs ? num_units : num_pairs;
             const unsigned expect = (unsigned)(2 * (num_units - busy));
             const unsigned got = atomicAdd(wave_counter, 0u);
-            if (!dbg_aborted()) DBG_CHECK(got == expect, 7, ((unsigned long long)got << 32) | expect);
+            DBG_CHECK(got == expect, 7, ((unsigned long long)got << 32) | expect);
 #endif
             atomicExch(wave_counter, 0u);
             atomicExch(wave_counter + 3, 0u);
@@ -1100,16 +1089,38 @@ LaunchFn pick(int mn) {
 
 }  // namespace
 
+#if SPLIT3_DEBUG
+namespace {
+unsigned long long* g_dbg_host = nullptr;   // the mapped record (host view)
+}
+#endif
+
+int gemm3_debug_init() {
+#if SPLIT3_DEBUG
+    if (g_dbg_host) return 1;
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, 64, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return -1;
+    memset(p, 0, 64);
+    void* d = nullptr;
+    if (cudaHostGetDevicePointer(&d, p, 0) != cudaSuccess) return -1;
+    if (cudaMemcpyToSymbol(g_dbg, &d, sizeof(d)) != cudaSuccess) return -1;
+    g_dbg_host = static_cast<unsigned long long*>(p);
+    return 1;
+#else
+    return 0;
+#endif
+}
+
 int gemm3_debug_read(unsigned long long* out8, int reset) {
 #if SPLIT3_DEBUG
-    if (cudaMemcpyFromSymbol(out8, g_dbg, sizeof(g_dbg)) != cudaSuccess) return -1;
-    if (reset) {
-        const unsigned long long z[8] = {};
-        const unsigned zu = 0;
-        if (cudaMemcpyToSymbol(g_dbg, z, sizeof(z)) != cudaSuccess ||
-            cudaMemcpyToSymbol(g_dbg_abort, &zu, sizeof(zu)) != cudaSuccess)
-            return -1;
+    if (!g_dbg_host) {
+        memset(out8, 0, 64);
+        return 1;
     }
+    volatile unsigned long long* r = g_dbg_host;   // host memory: readable after a device fault
+    for (int i = 0; i < 8; i++) out8[i] = r[i];
+    if (reset)
+        for (int i = 0; i < 8; i++) r[i] = 0;
     return 1;
 #else
     (void)out8; (void)reset;

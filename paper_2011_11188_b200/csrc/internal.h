@@ -136,6 +136,7 @@ struct SplitPlan {
 SplitPlan gemm3_split_plan(int64_t M, int64_t N, int64_t K, int terms, int num_sms, int promo_kb);
 // debug build (SPLIT3_DEBUG=1): read / reset the GEMM's check record, inject a fault; release
 // builds return 0 (not available), -1 on a CUDA error, 1 on success
+int gemm3_debug_init();   // map the host record (handle creation)
 int gemm3_debug_read(unsigned long long* out8, int reset);
 int gemm3_debug_fault(int fault);
 int64_t gemm3_partial_elems(const SplitPlan& p, int terms);   // floats of partial workspace
