@@ -13,6 +13,7 @@ import numpy as np
 import pytest
 import torch
 
+from split3_bounds import _assert_elementwise, _elementwise_bound  # noqa: F401
 from workloads import numpy_matrix, torch_matrix
 
 pytestmark = pytest.mark.gpu
@@ -48,40 +49,6 @@ def _metrics(C, Csplit, C64, A, B):
     e64 = np.linalg.norm(C - C64) / max(np.linalg.norm(A.astype(np.float64)) * np.linalg.norm(B.astype(np.float64)), 1e-300)
     e64rel = np.linalg.norm(C - C64) / max(np.linalg.norm(C64), 1e-300)
     return e_or, e64, e64rel
-
-
-def _elementwise_bound(orc, A, B, terms, slices=16):
-    """Per-element bound on |C_gpu - C_split| (C_split: the oracle's fp64 Eq. A_2), from the
-    measured accumulator semantics (DESIGN.md §3 R9): one kind::f16 MMA sums 16 exact products
-    into the FP32 accumulator with truncation, losing < 1 ulp of the largest addend per addend
-    (<= 18 u M per MMA, u = 2^-23, M <= the partial sum of |products|); D_hi is promoted with
-    round-to-nearest every 8 MMAs (library default), D_mid (D_lo) accumulate over the whole K;
-    split-K slices are added with RN; the epilogue fma rounds once, the 2^(sA+sB) scale is exact.
-        |err_ij| <= 2^(sA+sB) [ (144 u + (K/128 + 1 + slices) u/2) S_hi
-                               + 2^-11 (18 ceil(K/16) + 1) u S_mid + 2^-22 (18 ceil(K/16) + 1) u S_lo ]
-                    + u/2 |C_split|
-    with S_hi = |A1| |B1|, S_mid = |A1||B2| + |A2||B1|, S_lo = |A2||B2| (decoded planes)."""
-    K = A.shape[1]
-    a1, a2, sA = orc.split(A)
-    b1, b2, sB = orc.split(B)
-    A1, A2 = np.abs(orc.dec16(a1)), np.abs(orc.dec16(a2))
-    B1, B2 = np.abs(orc.dec16(b1)), np.abs(orc.dec16(b2))
-    u = 2.0 ** -23
-    nk = -(-K // 16)
-    bnd = (144 * u + (K / 128 + 1 + slices) * u / 2) * (A1 @ B1)
-    if terms != 1:
-        bnd += 2.0 ** -11 * (18 * nk + 1) * u * (A1 @ B2 + A2 @ B1)
-    if terms == 4:
-        bnd += 2.0 ** -22 * (18 * nk + 1) * u * (A2 @ B2)
-    return np.ldexp(bnd, sA + sB)
-
-
-def _assert_elementwise(orc, C, Cs, A, B, terms):
-    bound = _elementwise_bound(orc, A, B, terms) + 2.0 ** -24 * np.abs(Cs)
-    err = np.abs(C.astype(np.float64) - Cs)
-    bad = np.argwhere(err > bound)
-    assert bad.size == 0, (bad[:5].tolist(), err[tuple(bad[0])], bound[tuple(bad[0])])
-    return float(np.max(err / np.maximum(bound, 1e-300)))
 
 
 # ----------------------------------------------------------- a1 + a2: planes -----

@@ -1,0 +1,62 @@
+"""Few-tiles-per-pair problems (dense-layer shapes, config D3): the GEMM's tail split (split-K
+slices of the partial last wave, or of all tiles when there are fewer tiles than CTA pairs)
+against the oracle — E_or, E64 and the per-element bound — for 1/3/4 terms, the fused-B and
+separate-split paths, ragged shapes and several SM budgets (each gives another split plan), plus
+bitwise repeatability.  (A stream-K schedule was measured for these shapes and not adopted:
+DESIGN.md §9.)"""
+import numpy as np
+import pytest
+import torch
+
+from workloads import numpy_matrix
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(256, 8192, 8192), (1024, 4096, 8192), (300, 2000, 5000), (512, 1280, 3000), (768, 2304, 1536)]
+
+
+def _metrics(C, Cs, C64, A, B):
+    e_or = np.linalg.norm(C - Cs) / np.linalg.norm(Cs)
+    e64 = np.linalg.norm(C - C64) / (np.linalg.norm(A.astype(np.float64)) * np.linalg.norm(B.astype(np.float64)))
+    return float(e_or), float(e64)
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("mode", ["default", "separate", "four", "one"])
+def test_small_m_vs_oracle(orc, M, N, K, mode):
+    import paper_2011_11188_b200 as s3
+    from split3_bounds import _assert_elementwise
+
+    h = s3.Handle(0)
+    if mode == "separate":
+        h.set_fused_split(0)
+    terms = {"four": 4, "one": 1}.get(mode, 3)
+    A = numpy_matrix("uniform", M, K, seed=M + 7)
+    B = numpy_matrix("glorot", K, N, seed=N + 9)
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    C = h.sgemm(Ad, Bd, four_term=terms == 4, one_term=terms == 1)
+    C2 = h.sgemm(Ad, Bd, four_term=terms == 4, one_term=terms == 1)
+    torch.cuda.synchronize()
+    assert torch.equal(C.view(torch.int32), C2.view(torch.int32))          # deterministic
+    Cn = C.cpu().numpy()
+    Cs = orc.sgemm(A, B, terms=terms)
+    e_or, e64 = _metrics(Cn, Cs, orc.gemm64(A, B), A, B)
+    assert e_or <= 1e-6, e_or
+    if terms != 1:
+        assert e64 <= 2e-6, e64
+    _assert_elementwise(orc, Cn, Cs, A, B, terms)
+
+
+@pytest.mark.parametrize("sms", [132, 100, 64, 2])
+def test_small_m_sm_budgets(orc, sms):
+    """another SM budget -> another split plan (and another summation order): still the oracle"""
+    import paper_2011_11188_b200 as s3
+
+    h = s3.Handle(0)
+    h.set_max_sms(sms)
+    M, N, K = 512, 2048, 4000
+    A = numpy_matrix("loguni", M, K, seed=3)
+    B = numpy_matrix("uniform", K, N, seed=4)
+    C = h.sgemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+    Cs = orc.sgemm(A, B, terms=3)
+    assert np.linalg.norm(C - Cs) / np.linalg.norm(Cs) <= 1e-6
