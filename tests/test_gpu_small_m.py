@@ -13,6 +13,9 @@ from workloads import numpy_matrix
 pytestmark = pytest.mark.gpu
 
 SHAPES = [(256, 8192, 8192), (1024, 4096, 8192), (300, 2000, 5000), (512, 1280, 3000), (768, 2304, 1536)]
+# (the two largest shapes only in the default and separate-split modes: the fp64 oracle takes seconds)
+CASES = [(s, m) for s in SHAPES for m in ("default", "separate", "four", "one")
+         if m in ("default", "separate") or s[0] * s[1] * s[2] < 1 << 33]
 
 
 def _metrics(C, Cs, C64, A, B):
@@ -21,12 +24,12 @@ def _metrics(C, Cs, C64, A, B):
     return float(e_or), float(e64)
 
 
-@pytest.mark.parametrize("M,N,K", SHAPES)
-@pytest.mark.parametrize("mode", ["default", "separate", "four", "one"])
-def test_small_m_vs_oracle(orc, M, N, K, mode):
+@pytest.mark.parametrize("shape,mode", CASES)
+def test_small_m_vs_oracle(orc, shape, mode):
     import paper_2011_11188_b200 as s3
     from split3_bounds import _assert_elementwise
 
+    M, N, K = shape
     h = s3.Handle(0)
     if mode == "separate":
         h.set_fused_split(0)
