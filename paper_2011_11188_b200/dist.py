@@ -34,6 +34,7 @@ backend (tests/test_dist_gloo.py); the default ops are the CUDA library's.
 from __future__ import annotations
 
 import math
+import os
 
 import torch
 import torch.distributed as dist
@@ -354,8 +355,9 @@ class TileGemm:
             self.M, self.N, self.K = self.pr * n, self.pc * n, n
         self.h = h
         nccl = dist.get_backend() == "nccl"
-        if gather_ctas is None:
-            gather_ctas = GATHER_CTAS if (nccl and world > 1 and not replicated) else 0
+        if gather_ctas is None:   # env SPLIT3_GATHER_CTAS overrides (0: NCCL's own CTA count, no SM cap)
+            gather_ctas = int(os.environ.get("SPLIT3_GATHER_CTAS", GATHER_CTAS)) if (
+                nccl and world > 1 and not replicated) else 0
         if ops is None:
             # pieces under a gather leave 2 SMs per gather CTA free: a CTA on one SM of a TPC
             # would otherwise break that TPC's GEMM CTA pair (cluster of 2)
