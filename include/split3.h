@@ -121,6 +121,27 @@ size_t split3_sgemm_host_workspace_size(int64_t M, int64_t N, int64_t K, uint32_
 int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K,
                       const float *A_host, const float *B_host, float *C_host, uint32_t flags);
 
+/* Where the last split3_sgemm_host call of this handle left its FP16 planes (introspection for
+ * tests: DESIGN.md §5e).  A was split in `nblk` row blocks [blk_r0, + blk_rows), each with its own
+ * scale exponent d_sblk[b] — or the per-matrix *d_sA where d_redo[b] != 0 (the block was redone) —
+ * into K-major M x K planes A1/A2 (ldpa); B in `npan` column panels [pan_c0, + pan_cols) with
+ * exponents d_span[j] (or *d_sB where d_redo[32 + j] != 0) into MN-major K x N planes B1/B2
+ * (ldpb) when b_mn, else K-major N x K.  d_redo is NULL for a one-block, one-panel call (the
+ * per-matrix exponents were used).  All pointers are device pointers into the workspace, valid
+ * until the next call that uses it.  nblk == 0 before the first host call. */
+typedef struct split3_host_layout {
+    int nblk, npan;
+    int64_t blk_r0[32], blk_rows[32];
+    int64_t pan_c0[4], pan_cols[4];
+    const uint16_t *A1, *A2;
+    int64_t ldpa;
+    const uint16_t *B1, *B2;
+    int64_t ldpb;
+    int b_mn;
+    const int32_t *d_sblk, *d_span, *d_redo, *d_sA, *d_sB;
+} split3_host_layout;
+int split3_host_last_layout(split3_handle_t h, split3_host_layout *out);
+
 /* After SPLIT3_ERR_NOT_FINITE: first offending linear index (row*cols+col) of A, or
  * M*K + index within B; -1 if none recorded. */
 int64_t split3_last_bad_index(split3_handle_t h);

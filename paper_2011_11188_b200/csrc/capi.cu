@@ -53,6 +53,7 @@ struct split3_ctx {
     int host_blocks = 0;               // row blocks of the host pipeline (0 = automatic; env SPLIT3_HOST_BLOCKS)
     long long host_redo = 0;           // row blocks redone with the per-matrix scale (split3_host_redo_count)
     int host_panels = 0;               // B column panels of the 2-D host schedule (0 = automatic; env SPLIT3_HOST_PANELS)
+    split3_host_layout host_layout = {};   // the last host call's planes (split3_host_last_layout)
     // measurement hooks: event triples (start, after split, after gemm) per timed call
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -840,6 +841,9 @@ int split3_timing_read(split3_handle_t h, double* split_ms, double* gemm_ms, int
 // host pipeline: per-row-block scalars after the staging buffers
 constexpr int kMaxHostBlocks = 32;
 constexpr int kMaxPanels = 4;
+static_assert(sizeof(((split3_host_layout*)nullptr)->blk_r0) / sizeof(int64_t) == kMaxHostBlocks &&
+                  sizeof(((split3_host_layout*)nullptr)->pan_c0) / sizeof(int64_t) == kMaxPanels,
+              "split3_host_layout arrays match the host pipeline's limits");
 constexpr int kMaxPieceEvents = 64;   // ring of "C piece computed" events (ev_rows)
 constexpr size_t kHostScalarBytes = 4 * 4 * (kMaxHostBlocks + kMaxPanels);
 
@@ -1101,6 +1105,23 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
     if (cudaStreamSynchronize(h->s_out) != cudaSuccess || cudaStreamSynchronize(s0) != cudaSuccess)
         return SPLIT3_ERR_CUDA;
     h->last_launches = launches;
+    split3_host_layout& L = h->host_layout;   // where the planes of this call live (introspection)
+    L = split3_host_layout{};
+    L.nblk = nblk;
+    L.npan = nbp;
+    for (int b = 0; b < nblk; b++) { L.blk_r0[b] = blk_r0[b]; L.blk_rows[b] = blk_mr[b]; }
+    for (int j = 0; j < nbp; j++) { L.pan_c0[j] = pan_c0[j]; L.pan_cols[j] = pan_nc[j]; }
+    L.A1 = w.A1; L.A2 = w.A2; L.ldpa = w.ldpa;
+    L.B1 = w.B1t; L.B2 = w.B2t; L.ldpb = ldpb; L.b_mn = b_mn ? 1 : 0;
+    L.d_sblk = sblk; L.d_span = span;
+    L.d_redo = (nblk > 1 || nbp > 1) ? flags_d : nullptr;
+    L.d_sA = w.sA; L.d_sB = w.sB;
+    return SPLIT3_OK;
+}
+
+int split3_host_last_layout(split3_handle_t h, split3_host_layout* out) {
+    if (!h || !out) return SPLIT3_ERR_INVALID_VALUE;
+    *out = h->host_layout;
     return SPLIT3_OK;
 }
 

@@ -35,7 +35,7 @@ BF16X3 = 1 << 3
 EXPORTS = (
     "split3_sgemm_create", "split3_set_stream", "split3_sgemm_destroy",
     "split3_sgemm_workspace_size", "split3_sgemm_ex_workspace_size", "split3_sgemm_set_workspace", "split3_sgemm",
-    "split3_sgemm_host_workspace_size", "split3_sgemm_host", "split3_last_bad_index", "split3_host_redo_count",
+    "split3_sgemm_host_workspace_size", "split3_sgemm_host", "split3_last_bad_index", "split3_host_redo_count", "split3_host_last_layout",
     "split3_status_string", "split3_maxabs", "split3_split", "split3_gemm_planes",
     "split3_last_launch_count", "split3_timing_enable", "split3_timing_read",
     "split3_set_promotion", "split3_set_wave_sync", "split3_set_split_k", "split3_set_max_sms", "split3_set_schedule", "split3_set_fused_split",
@@ -48,6 +48,17 @@ class split3_matrix(ctypes.Structure):
     _fields_ = [("data", ctypes.c_void_p), ("ld", ctypes.c_int64), ("trans", ctypes.c_int),
                 ("hi", ctypes.c_void_p), ("lo", ctypes.c_void_p), ("ldp", ctypes.c_int64),
                 ("d_sexp", ctypes.c_void_p), ("stored", ctypes.c_int)]
+
+
+class split3_host_layout(ctypes.Structure):
+    """ctypes mirror of include/split3.h's split3_host_layout."""
+    _fields_ = [("nblk", ctypes.c_int), ("npan", ctypes.c_int),
+                ("blk_r0", ctypes.c_int64 * 32), ("blk_rows", ctypes.c_int64 * 32),
+                ("pan_c0", ctypes.c_int64 * 4), ("pan_cols", ctypes.c_int64 * 4),
+                ("A1", ctypes.c_void_p), ("A2", ctypes.c_void_p), ("ldpa", ctypes.c_int64),
+                ("B1", ctypes.c_void_p), ("B2", ctypes.c_void_p), ("ldpb", ctypes.c_int64), ("b_mn", ctypes.c_int),
+                ("d_sblk", ctypes.c_void_p), ("d_span", ctypes.c_void_p), ("d_redo", ctypes.c_void_p),
+                ("d_sA", ctypes.c_void_p), ("d_sB", ctypes.c_void_p)]
 
 
 class Planes:
@@ -109,6 +120,7 @@ def load() -> ctypes.CDLL:
         lib.split3_sgemm_host.argtypes = [_p, _i64, _i64, _i64, _p, _p, _p, ctypes.c_uint32]
         lib.split3_last_bad_index.restype = _i64
         lib.split3_last_bad_index.argtypes = [_p]
+        lib.split3_host_last_layout.argtypes = [_p, ctypes.POINTER(split3_host_layout)]
         lib.split3_host_redo_count.restype = _i64
         lib.split3_host_redo_count.argtypes = [_p]
         lib.split3_last_launch_count.argtypes = [_p]
@@ -331,6 +343,12 @@ class Handle:
     def host_redo_count(self) -> int:
         """row blocks the host pipeline redid with the per-matrix scale"""
         return int(self._lib.split3_host_redo_count(self._h))
+
+    def host_last_layout(self) -> split3_host_layout:
+        """where the last sgemm_host call left its planes (device pointers into the workspace)"""
+        out = split3_host_layout()
+        self._chk(self._lib.split3_host_last_layout(self._h, ctypes.byref(out)), "split3_host_last_layout")
+        return out
 
     def last_launch_count(self) -> int:
         return int(self._lib.split3_last_launch_count(self._h))

@@ -149,3 +149,86 @@ def test_2d_schedule_b_panels(hd, case):
     redo = h.host_redo_count() - r0
     assert redo == {"plain": 0, "b_panel_scaled": 0, "b_tiny": 1, "a_and_b_tiny": 2}[case], redo
     assert _same(C, hd.sgemm_host(A, B))
+
+
+def _dev_view(h, ptr, rows, ld, cols):
+    """rows x cols int16 plane view (ld elements per row) of the handle's workspace at device ptr"""
+    ws = h._ws
+    off = ptr - ws.data_ptr()
+    assert 0 <= off and off + rows * ld * 2 <= ws.numel()
+    return ws[off:off + rows * ld * 2].view(torch.int16).view(rows, ld)[:, :cols].cpu().numpy().view(np.uint16)
+
+
+def _dev_i32(h, ptr, n):
+    ws = h._ws
+    off = ptr - ws.data_ptr()
+    return ws[off:off + 4 * n].view(torch.int32).cpu().numpy()
+
+
+@pytest.mark.parametrize("case", ["uniform", "blocks_scaled", "tiny_redo", "loguni", "panels"])
+def test_host_planes_vs_oracle(orc, case):
+    """the planes the host pipeline multiplied (split3_host_last_layout): every A row block and B
+    column panel bit-exact vs the ORACLE's split of that block with the exponent the pipeline used
+    — its own R1 exponent, or the per-matrix one where the block was redone — and that choice
+    itself recomputed from oracle.maxabs / oracle.scale_exp"""
+    h = _handle(4)
+    if case == "panels":
+        h = s3.Handle(0)        # automatic blocks + 2 B panels (2-D schedule)
+    M, N, K = (8192, 8192, 320) if case == "panels" else (2048, 512, 700)
+    kind = "loguni" if case == "loguni" else "uniform"
+    A = numpy_matrix(kind, M, K, seed=60)
+    B = numpy_matrix("uniform" if case != "panels" else "loguni", K, N, seed=61)
+    if case in ("blocks_scaled", "tiny_redo"):
+        A[:512] *= np.float32(2.0 ** -6)
+    if case == "tiny_redo":
+        A[5, 9] = np.float32(2.0 ** -44)
+    if case == "panels":
+        B[:, N // 2:] *= np.float32(2.0 ** -9)
+    h.sgemm_host(A, B)
+    torch.cuda.synchronize()
+    L = h.host_last_layout()
+    assert L.nblk >= 1 and L.npan >= 1
+    sA = orc.scale_exp(orc.maxabs(A)[0])
+    sB = orc.scale_exp(orc.maxabs(B)[0])
+    assert _dev_i32(h, L.d_sA, 1)[0] == sA and _dev_i32(h, L.d_sB, 1)[0] == sB
+    sblk = _dev_i32(h, L.d_sblk, L.nblk)
+    span = _dev_i32(h, L.d_span, L.npan)
+    redo = _dev_i32(h, L.d_redo, 36) if L.d_redo else np.zeros(36, np.int32)
+
+    def rule(X, s_mat):
+        s_b = orc.scale_exp(orc.maxabs(np.ascontiguousarray(X))[0])
+        a = np.abs(X.astype(np.float64))
+        tiny = np.any((a > 0) & (a < 2.0 ** (s_mat - 12)))
+        return s_b, bool(s_b != s_mat and tiny)
+
+    A1 = _dev_view(h, L.A1, M, L.ldpa, K)
+    A2 = _dev_view(h, L.A2, M, L.ldpa, K)
+    n_redo = 0
+    for b in range(L.nblk):
+        r0, mr = L.blk_r0[b], L.blk_rows[b]
+        blk = A[r0:r0 + mr]
+        s_b, must_redo = rule(blk, sA)
+        if L.d_redo:
+            assert bool(redo[b]) == must_redo, (b, redo[b], must_redo)
+        assert sblk[b] == s_b, (b, sblk[b], s_b)
+        s_used = sA if (L.d_redo and redo[b]) else s_b
+        n_redo += int(bool(L.d_redo) and bool(redo[b]))
+        hi, lo, _ = orc.split(blk, s=s_used)
+        assert np.array_equal(A1[r0:r0 + mr], hi) and np.array_equal(A2[r0:r0 + mr], lo), b
+    assert L.b_mn == 1
+    B1 = _dev_view(h, L.B1, K, L.ldpb, N)
+    B2 = _dev_view(h, L.B2, K, L.ldpb, N)
+    for j in range(L.npan):
+        c0, nc = L.pan_c0[j], L.pan_cols[j]
+        pan = np.ascontiguousarray(B[:, c0:c0 + nc])
+        s_j, must_redo = rule(pan, sB)
+        if L.d_redo:
+            assert bool(redo[32 + j]) == must_redo, (j, must_redo)
+        assert span[j] == s_j
+        s_used = sB if (L.d_redo and redo[32 + j]) else s_j
+        hi, lo, _ = orc.split(pan, s=s_used)
+        assert np.array_equal(B1[:, c0:c0 + nc], hi) and np.array_equal(B2[:, c0:c0 + nc], lo), j
+    if case == "tiny_redo":
+        assert n_redo == 1
+    if case == "panels":
+        assert L.npan == 2 and L.nblk >= 4

@@ -1,4 +1,6 @@
-"""A/B timing of experimental builds (extra -D flags) of the same sources.
+"""A/B timing of experimental builds (extra -D flags, e.g. SPLIT3_PDL=0, of the same sources; or
+patched builds from tools/exp_patch_build.py).  Round 1's in-kernel cycle-counter trace build
+(profiles/gemm3_trace_r01.md) was removed from the product sources in round 2.
 
   python tools/exp_ab.py build TAG DEFINE...     (here: nvcc -> tools/exp/libsplit3_TAG.so)
   python tools/exp_ab.py time  M N K [TAG...]    (on the GPU: GEMM-kernel time per library)
@@ -60,31 +62,4 @@ if os.environ.get("EXP_ACC"):               # accuracy of this build vs fp64 (me
     C64 = A.double() @ B.double()
     rec["e64rel"] = float((C.double() - C64).norm() / C64.norm())
     del C64
-lib = s3.load()
-if hasattr(lib, "split3_exp_trace"):           # experiment build with -DSPLIT3_EXP_TRACE
-    import ctypes
-
-    import numpy as np
-
-    buf = np.zeros((160, 16), np.uint64)
-    lib.split3_exp_trace(ctypes.c_void_p(buf.ctypes.data), 1)
-    h.sgemm(A, B, out=C)
-    torch.cuda.synchronize()
-    lib.split3_exp_trace(ctypes.c_void_p(buf.ctypes.data), 0)
-    leaders = buf[0:148:2].astype(np.float64)            # leader CTAs (MMA waits are recorded there)
-    tot = leaders[:, 7].mean()
-    names = ["mma_wait_full", "mma_wait_mempty", "mma_wait_hempty", "epi_wait_hfull", "epi_promote",
-             "epi_unit_end_combine", "epi_store_issue", "kernel", "prod_wave_sync", "prod_wait_empty"]
-    lanes = [32, 32, 32, 1, 1, 1, 1, 1, 1, 1]          # MMA-warp waits are counted by every lane
-    rec["trace_fraction_of_kernel_cycles"] = {nm: round(leaders[:, i].mean() / tot / lanes[i], 4)
-                                              for i, nm in enumerate(names) if nm != "kernel"}
-    rec["trace_wave_sync_max_cta"] = round(float((buf[:148, 8] / buf[:148, 7]).max()), 4)
-    rec["kernel_cycles"] = tot
-    if os.environ.get("EXP_DUMP"):
-        np.save(os.environ["EXP_DUMP"], buf)
-        h.sgemm(A, B, out=C)          # a second launch: is the per-CTA pattern systematic?
-        torch.cuda.synchronize()
-        lib.split3_exp_trace(ctypes.c_void_p(buf.ctypes.data), 1)
-        lib.split3_exp_trace(ctypes.c_void_p(buf.ctypes.data), 0)
-        np.save(os.environ["EXP_DUMP"].replace(".npy", "_b.npy"), buf)
 print(json.dumps(rec))
