@@ -319,10 +319,28 @@ int split3_set_max_sms(split3_handle_t h, int sms);
  * the max-abs pass reads B beforehand).  The planes, and therefore C, are bit-identical to the separate split.
  * mode 0: off; 1 (default): when M <= max_m (default 2048: each B tile is converted once per
  * 256-row tile row, and the extra shared-memory traffic slows the GEMM ~11 %, which the saved
- * 8 B/element of B's split outweighs for small M) and the call is not a one-launch small call;
- * 2: whenever eligible.  max_m = 0 keeps the current threshold.  Env: SPLIT3_FUSE_B,
+ * 8 B/element of B's split outweighs for small M), or for any M when the call is small enough for
+ * the one-launch front end (SPLIT3_PREP_MAX; fused B is 5-25 % faster there); 2: whenever
+ * eligible.  max_m = 0 keeps the current threshold.  Env: SPLIT3_FUSE_B,
  * SPLIT3_FUSE_B_MAX_M at handle creation.  INVALID_VALUE for mode outside 0..2 or max_m < 0. */
 int split3_set_fused_split(split3_handle_t h, int mode, int64_t max_m);
+
+/* Fused split of A (SURVEY §8f NEXT #2 for the other operand; Eq. A_1 applied inside the GEMM):
+ * for a 3-term call whose A is an fp32 matrix (not pre-split; row-major M x K, or stored K x M
+ * with transA = 1), 16-byte aligned with ld % 4 == 0, and whose C is 16-byte aligned with
+ * ldc % 4 == 0, the call computes the transposed problem C^T = B^T A^T: B's planes are the GEMM's
+ * A operand, A's fp32 tiles are TMA-loaded and split in shared memory as the fused B operand
+ * above, and the epilogue writes each C^T tile transposed into C (TMA stores; the split-K tail
+ * reduction likewise).  A's planes never go through HBM.  The planes equal the separate split's
+ * bit for bit; C equals, bit for bit, C^T = B^T A^T computed with separately split planes, and
+ * is within the same oracle tolerance as the untransposed call (the tensor core may sum a K = 16
+ * step in another order when the operand roles swap).  mode 0 (default: every other path of
+ * this library reproduces the untransposed call's bits, and this one would not): off; 1: when
+ * N <= max_n (default 2048) and N < M (A is the larger operand: fused A is then chosen over fused
+ * B) and the call is not a one-launch small call; 2: whenever eligible (takes precedence over
+ * fused B).  max_n = 0 keeps the current threshold.  Env: SPLIT3_FUSE_A, SPLIT3_FUSE_A_MAX_N at
+ * handle creation.  INVALID_VALUE for mode outside 0..2 or max_n < 0. */
+int split3_set_fused_split_a(split3_handle_t h, int mode, int64_t max_n);
 
 /* ---- debug build (libsplit3_debug.so: the same sources with -DSPLIT3_DEBUG=1) ----------------
  * The GEMM's synchronisation checks that compute-sanitizer would provide (it is not usable on this

@@ -38,10 +38,17 @@ struct split3_ctx {
     int mn_major = 1;   // MN-major planes for a row-major B / a transposed A (no transposing split);
                         // env SPLIT3_MN_MAJOR=0: off (K-major planes, transposing split)
     // fused B: an fp32 B is split inside the GEMM (converter warps) instead of
-    // by a separate pass.  0 off, 1 auto (M <= fuse_b_max_m and not a one-launch small call),
+    // by a separate pass.  0 off, 1 auto (M <= fuse_b_max_m, or a small call of any M),
     // 2 whenever eligible (measured: profiles/fused_b_r01.md).  env SPLIT3_FUSE_B, SPLIT3_FUSE_B_MAX_M
     int fuse_b = 1;
     int64_t fuse_b_max_m = 2048;
+    // fused A: the same for an fp32 A, through the transposed problem C^T = B^T A^T (A^T is the
+    // fused operand; the epilogue stores C^T's tiles transposed into C).  0 off (default: the
+    // transposed product differs in the last bits from the untransposed one), 1 auto
+    // (N <= fuse_a_max_n and N < M: A is the larger operand; not a one-launch small call), 2
+    // whenever eligible (before fused B).  env SPLIT3_FUSE_A, SPLIT3_FUSE_A_MAX_N
+    int fuse_a = 0;
+    int64_t fuse_a_max_n = 2048;
     split3::GemmTuneIn tune;
     unsigned* d_counters = nullptr;   // 256 B of device scratch owned by the handle
     // host-buffer entry: copy-in / copy-out streams and events, created on first use
@@ -243,6 +250,8 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
     if (const char* e = getenv("SPLIT3_HOST_BLOCKS")) c->host_blocks = std::min(std::max(atoi(e), 0), 16);
     if (const char* e = getenv("SPLIT3_HOST_PANELS")) c->host_panels = std::min(std::max(atoi(e), 0), 4);
     if (const char* e = getenv("SPLIT3_FUSE_B_MAX_M")) c->fuse_b_max_m = atoll(e);
+    if (const char* e = getenv("SPLIT3_FUSE_A")) c->fuse_a = atoi(e);
+    if (const char* e = getenv("SPLIT3_FUSE_A_MAX_N")) c->fuse_a_max_n = atoll(e);
     *h = c;
     return SPLIT3_OK;
 }
@@ -512,8 +521,16 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     // fused B (NEXT #2): 3-term, fp32 B (row-major K x N, or stored N x K for transB) that TMA
     // can read (16-B aligned, ld % 4 == 0)
     const bool small_call = fast_max && h->mn_major && h->prep_ok && h->prep_max >= M * K + K * N;
-    const bool fuse_b = needB && terms == 3 && aligned(B->data, 16) && (B->ld % 4) == 0 &&
-                        (h->fuse_b == 2 || (h->fuse_b == 1 && M <= h->fuse_b_max_m && !small_call));
+    // fused A (NEXT #2 for A): the transposed problem C^T = B^T A^T with A^T as the fused operand
+    // (an fp32 A of either storage TMA can read) and C written transposed (TMA stores: C 16-B
+    // aligned, ldc % 4 == 0); preferred over fused B when A is the larger operand (N < M)
+    const bool fuse_a = needA && terms == 3 && aligned(A->data, 16) && (A->ld % 4) == 0 && aligned(C, 16) &&
+                        (ldc % 4) == 0 &&
+                        (h->fuse_a == 2 || (h->fuse_a == 1 && N <= h->fuse_a_max_n && N < M && !small_call));
+    // fused B: M <= fuse_b_max_m, or any M for a small call (measured faster than the one-launch
+    // front end at every small shape, 5-25 %: profiles/small_fused_bench_r02.json)
+    const bool fuse_b = !fuse_a && needB && terms == 3 && aligned(B->data, 16) && (B->ld % 4) == 0 &&
+                        (h->fuse_b == 2 || (h->fuse_b == 1 && (M <= h->fuse_b_max_m || small_call)));
     // (both operands pre-split: no max-abs at all, nothing to reset)
     if (!fast_max && (needA || needB) && cudaMemsetAsync(h->ws, 0, 32, h->stream) != cudaSuccess)
         return SPLIT3_ERR_CUDA;
@@ -536,7 +553,7 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     // replay faster than one cooperative node: 0.361 vs 0.403 ms per small-MLP step)
     bool prepped = false;
     cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
-    if (!fuse_b && small_call &&
+    if (!fuse_b && !fuse_a && small_call &&
         cudaStreamIsCapturing(h->stream, &cap_st) == cudaSuccess && cap_st == cudaStreamCaptureStatusNone) {
         const split3::PrepOperand pa{A->data, A->trans ? K : M, A->trans ? M : K, A->ld, w.A1, w.A2,
                                      A->trans ? w.ldpa_mn : w.ldpa, w.maxA, w.sA};
@@ -594,7 +611,9 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     // pre-split planes of the stored matrix: A stored K x M (trans) is MN-major, B stored K x N
     // (not trans) is MN-major; the other two cases are K-major
     const bool a_mn = (needA && A->trans && h->mn_major) || (!needA && A->stored && A->trans);
-    if (prepped) {
+    if (fuse_a) {
+        sA = w.sA;   // written by the GEMM (A's planes never reach HBM)
+    } else if (prepped) {
         A1 = w.A1; A2 = w.A2; sA = w.sA; ldpa = a_mn ? w.ldpa_mn : w.ldpa;
     } else if (needA && a_mn) {
         if ((n = split3::launch_split(h->stream, K, M, A->data, A->ld, w.maxA, w.A1, w.A2, w.ldpa_mn, w.sA,
@@ -634,10 +653,17 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     if (reserved > h->ws_bytes - pend) reserved = h->ws_bytes - pend;
     const int64_t partial_elems = (int64_t)(reserved / 4);
     int err = 0;
-    n = split3::launch_gemm3(h->stream, M, N, K, A1, A2, ldpa, sA, B1t, B2t, ldpb, sB, C, ldc, terms,
-                             gemm_sms(h), h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune,
-                             h->split_k ? partial : nullptr, partial_elems, &err, nullptr, nullptr, (b_mn ? 1 : 0) | (a_mn ? 2 : 0),
-                             fuse_b ? B->data : nullptr, B->ld, w.maxB);
+    if (fuse_a)   // C^T (N x M) = B^T A^T: B's planes are the A operand (MN-major iff B's are), the
+                  // fp32 A is the fused B operand (MN-major iff A is stored K x M), C stored transposed
+        n = split3::launch_gemm3(h->stream, N, M, K, B1t, B2t, ldpb, sB, nullptr, nullptr, 0, sA, C, ldc, terms,
+                                 gemm_sms(h), h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune,
+                                 h->split_k ? partial : nullptr, partial_elems, &err, nullptr, nullptr,
+                                 (A->trans ? 1 : 0) | (b_mn ? 2 : 0), A->data, A->ld, w.maxA, 1);
+    else
+        n = split3::launch_gemm3(h->stream, M, N, K, A1, A2, ldpa, sA, B1t, B2t, ldpb, sB, C, ldc, terms,
+                                 gemm_sms(h), h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune,
+                                 h->split_k ? partial : nullptr, partial_elems, &err, nullptr, nullptr,
+                                 (b_mn ? 1 : 0) | (a_mn ? 2 : 0), fuse_b ? B->data : nullptr, B->ld, w.maxB);
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
     launches += n;
@@ -802,6 +828,13 @@ int split3_set_fused_split(split3_handle_t h, int mode, int64_t max_m) {
     if (!h || mode < 0 || mode > 2 || max_m < 0) return SPLIT3_ERR_INVALID_VALUE;
     h->fuse_b = mode;
     if (max_m > 0) h->fuse_b_max_m = max_m;
+    return SPLIT3_OK;
+}
+
+int split3_set_fused_split_a(split3_handle_t h, int mode, int64_t max_n) {
+    if (!h || mode < 0 || mode > 2 || max_n < 0) return SPLIT3_ERR_INVALID_VALUE;
+    h->fuse_a = mode;
+    if (max_n > 0) h->fuse_a_max_n = max_n;
     return SPLIT3_OK;
 }
 

@@ -200,13 +200,13 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ float4 ld_shared_v4(uint32_t addr) {
-    float4 v;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
-    return v;
+__device__ __forceinline__ void st_shared_f32(uint32_t addr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
-__device__ __forceinline__ void st_shared_v2u(uint32_t addr, uint2 v) {
-    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(v.x), "r"(v.y) : "memory");
+__device__ __forceinline__ float ld_shared_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
 }
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
@@ -268,6 +268,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
           "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
         : "r"(taddr));
 }
+// 32 lanes x 8 consecutive 32-bit columns -> 8 registers per thread.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld_wait() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -305,21 +311,26 @@ __host__ __device__ constexpr uint32_t make_idesc(int m, int n, bool bf16 = fals
          | ((uint32_t)(m >> 4) << 24);            // M >> 4
 }
 
-__device__ __forceinline__ void tile_coords(int64_t tile, int64_t num_m, int64_t num_n, int group_m,
-                                            int64_t& mb, int64_t& nb) {
-    const int64_t per_group = (int64_t)group_m * num_n;
-    const int64_t g = tile / per_group;
-    const int64_t first_m = g * group_m;
-    int64_t gsize = num_m - first_m;
+// Unit and tile indices are 32-bit on the device (the host rejects > 2^31 - 1 work units): fewer
+// live registers in the epilogue, whose 128-float FP32 master leaves little room.
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int group_m, int& mb, int& nb) {
+    const int per_group = group_m * num_n;
+    const int g = tile / per_group;
+    const int first_m = g * group_m;
+    int gsize = num_m - first_m;
     if (gsize > group_m) gsize = group_m;
-    const int64_t r = tile - g * per_group;
+    const int r = tile - g * per_group;
     mb = first_m + r % gsize;
     nb = r / gsize;
 }
 
+// Device copy of the host's SplitPlan in 32-bit fields.
+struct UnitPlan {
+    int whole, nsplit, slices;
+};
 
-__device__ __forceinline__ void decode_unit(int64_t u, const SplitPlan& p, int num_kb, int kps, int64_t& tile,
-                                            int& kb_begin, int& kb_end, int& slot) {
+__device__ __forceinline__ void decode_unit(int u, const UnitPlan& p, int num_kb, int kps, int& tile, int& kb_begin,
+                                            int& kb_end, int& slot) {
     if (u < p.whole) {
         tile = u;
         kb_begin = 0;
@@ -327,13 +338,13 @@ __device__ __forceinline__ void decode_unit(int64_t u, const SplitPlan& p, int n
         slot = -1;
         return;
     }
-    const int64_t v = u - p.whole;
-    const int64_t t = v % p.nsplit;
-    const int s = (int)(v / p.nsplit);
+    const int v = u - p.whole;
+    const int t = v % p.nsplit;
+    const int s = v / p.nsplit;
     tile = p.whole + t;
     kb_begin = s * kps;
     kb_end = kb_begin + kps < num_kb ? kb_begin + kps : num_kb;
-    slot = (int)v;   // = s * nsplit + t
+    slot = v;   // = s * nsplit + t
 }
 
 // Tile geometry per instantiation: BN_ = 256 (3-term, 1-term, bf16x3) or 128 (4-term: D_lo
@@ -488,14 +499,15 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     const int lane = threadIdx.x & 31;
     const uint32_t crank = cluster_rank();
     const bool leader = crank == 0;
-    const int64_t num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + BN_ - 1) / BN_;
+    const int num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + BN_ - 1) / BN_;
     const int num_kb = (K + BK - 1) / BK;
     // Work units (SplitPlan, host-chosen): units [0, whole) are whole tiles 0..whole-1; the
     // remaining `nsplit` tiles (the tail wave, or all tiles of a small problem) are cut into
     // `slices` K slices of kps k-blocks: unit whole + s*nsplit + t = slice s of tile whole + t.
-    const int kps = (num_kb + plan.slices - 1) / plan.slices;
-    const int64_t num_units = plan.whole + plan.nsplit * plan.slices;
-    const int64_t pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
+    const UnitPlan up{(int)plan.whole, (int)plan.nsplit, plan.slices};
+    const int kps = (num_kb + up.slices - 1) / up.slices;
+    const int num_units = up.whole + up.nsplit * up.slices;
+    const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&mapA1); tma_prefetch(&mapB1);
@@ -544,19 +556,19 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         int stage = 0;
         uint32_t phase = 0;
         unsigned wave_target = 0;   // cumulative arrivals expected up to this unit index (counter starts at 0)
-        int64_t idx = 0;
-        for (int64_t unit = pair; unit < num_units; unit += num_pairs, idx++) {
-            int64_t tile;
+        int idx = 0;
+        for (int unit = pair; unit < num_units; unit += num_pairs, idx++) {
+            int tile;
             int kb_begin, kb_end, slot;
-            decode_unit(unit, plan, num_kb, kps, tile, kb_begin, kb_end, slot);
+            decode_unit(unit, up, num_kb, kps, tile, kb_begin, kb_end, slot);
             if (wave_counter && idx > 0) {
-                int64_t active = num_units - idx * num_pairs;   // pairs with an idx-th unit
+                int active = num_units - idx * num_pairs;   // pairs with an idx-th unit
                 if (active > num_pairs) active = num_pairs;
                 wave_target += 2u * (unsigned)active;
                 if (elect_one()) wave_sync(wave_counter, wave_target);
                 __syncwarp();
             }
-            int64_t mb, nb;
+            int mb, nb;
             tile_coords(tile, num_m, num_n, tune.group_m, mb, nb);
             DBG_CHECK(mb >= 0 && mb < num_m && nb >= 0 && nb < num_n, 3, ((unsigned long long)mb << 32) | (unsigned)nb);
             DBG_CHECK(kb_begin < kb_end && kb_end <= num_kb, 5, ((unsigned long long)kb_begin << 32) | (unsigned)kb_end);
@@ -626,10 +638,10 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             uint32_t phase = 0;
             uint32_t cc = 0;       // global D_hi chunk counter
             uint32_t tc = 0;       // tile counter
-            for (int64_t unit = pair; unit < num_units; unit += num_pairs, tc++) {
-                int64_t tile_unused;
+            for (int unit = pair; unit < num_units; unit += num_pairs, tc++) {
+                int tile_unused;
                 int kb_begin, kb_end, slot;
-                decode_unit(unit, plan, num_kb, kps, tile_unused, kb_begin, kb_end, slot);
+                decode_unit(unit, up, num_kb, kps, tile_unused, kb_begin, kb_end, slot);
                 const uint32_t t_mid = tmem_base + COL_MID;
                 const uint32_t t_lo = tmem_base + COL_LO;
                 bool mid_ready = false;
@@ -746,10 +758,10 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         static_assert(NUM_CONV_WARPS == 2 && BK / 16 == 4, "two K steps per converter warp");
         int stage = 0;
         uint32_t phase = 0;
-        for (int64_t unit = pair; unit < num_units; unit += num_pairs) {
-            int64_t tile_unused;
+        for (int unit = pair; unit < num_units; unit += num_pairs) {
+            int tile_unused;
             int kb_begin, kb_end, slot;
-            decode_unit(unit, plan, num_kb, kps, tile_unused, kb_begin, kb_end, slot);
+            decode_unit(unit, up, num_kb, kps, tile_unused, kb_begin, kb_end, slot);
             for (int kb = kb_begin; kb < kb_end; kb++) {
                 mbar_wait(smem_u32(&ffull_bar[stage]), phase);
                 uint8_t* breg = smem + stage * STAGE_BYTES + B_OFF;
@@ -778,14 +790,20 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         const int sAB = *d_sA + (FB ? scale_exp_dev(*fb_maxB) : *d_sB);
         const bool fast = sAB >= -126 && sAB <= 127;
         const float fscale = fast ? __uint_as_float((unsigned)(sAB + 127) << 23) : 1.0f;
-        const bool vec_ok = (ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(C) & 15u) == 0);
+        // C = master * 2^sAB, exact unless the result is subnormal (one rounding); 2^sAB outside
+        // the fp32 normal range goes through fp64 (exact factor, then one rounding to fp32).  Applied
+        // as each value is stored, so no separate pass holds the whole master.
+        auto scl = [&](float x) {
+            return fast ? x * fscale
+                        : __double2float_rn(__dmul_rn((double)x, __longlong_as_double((long long)(sAB + 1023) << 52)));
+        };
         const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * NCOL);
         uint32_t cc = 0, tc = 0;
-        for (int64_t unit = pair; unit < num_units; unit += num_pairs, tc++) {
-            int64_t tile;
+        for (int unit = pair; unit < num_units; unit += num_pairs, tc++) {
+            int tile;
             int kb_begin, kb_end, slot;
-            decode_unit(unit, plan, num_kb, kps, tile, kb_begin, kb_end, slot);
-            int64_t mb, nb;
+            decode_unit(unit, up, num_kb, kps, tile, kb_begin, kb_end, slot);
+            int mb, nb;
             tile_coords(tile, num_m, num_n, tune.group_m, mb, nb);
             float master[NCOL];
 #pragma unroll
@@ -803,12 +821,11 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
             if (HAS_MID) {
                 mbar_wait(smem_u32(&mfull_bar[0]), tc & 1);
                 tc_fence_after();
+                if (TERMS == 4) {
 #pragma unroll
-                for (int c = 0; c < NCOL / 16; c++) {
-                    uint32_t mid[16];
-                    tmem_ld16(lane_base + COL_MID + c * 16, mid);
-                    if (TERMS == 4) {
-                        uint32_t lo[16];
+                    for (int c = 0; c < NCOL / 16; c++) {
+                        uint32_t mid[16], lo[16];
+                        tmem_ld16(lane_base + COL_MID + c * 16, mid);
                         tmem_ld16(lane_base + COL_LO + c * 16, lo);
                         tmem_ld_wait();
 #pragma unroll
@@ -816,16 +833,18 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                             master[c * 16 + j] = __fmaf_rn(
                                 __fmaf_rn(__uint_as_float(lo[j]), 0x1p-11f, __uint_as_float(mid[j])), 0x1p-11f,
                                 master[c * 16 + j]);
-                    } else if (BF3) {      // bf16 planes carry no scale: C = D_hi + D_mid
+                    }
+                } else {
+                    // 8 columns per load: the 128-float master leaves few registers
+#pragma unroll
+                    for (int c = 0; c < NCOL / 8; c++) {
+                        uint32_t mid[8];
+                        tmem_ld8(lane_base + COL_MID + c * 8, mid);
                         tmem_ld_wait();
 #pragma unroll
-                        for (int j = 0; j < 16; j++)
-                            master[c * 16 + j] = __fadd_rn(master[c * 16 + j], __uint_as_float(mid[j]));
-                    } else {
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int j = 0; j < 16; j++)
-                            master[c * 16 + j] = __fmaf_rn(__uint_as_float(mid[j]), 0x1p-11f, master[c * 16 + j]);
+                        for (int j = 0; j < 8; j++)
+                            master[c * 8 + j] = BF3 ? __fadd_rn(master[c * 8 + j], __uint_as_float(mid[j]))   // bf16: C = D_hi + D_mid
+                                                    : __fmaf_rn(__uint_as_float(mid[j]), 0x1p-11f, master[c * 8 + j]);
                     }
                 }
                 tc_fence_before();
@@ -842,53 +861,61 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                         make_float4(master[4 * j], master[4 * j + 1], master[4 * j + 2], master[4 * j + 3]);
                 continue;
             }
-            if (fast) {                                  // warp-uniform branch
-#pragma unroll
-                for (int j = 0; j < NCOL; j++) master[j] = master[j] * fscale;
-            } else {                                     // 2^sAB outside the fp32 normal range:
-                const double fd = __longlong_as_double((long long)(sAB + 1023) << 52);   // exact in fp64,
-#pragma unroll                                               // then one rounding to fp32
-                for (int j = 0; j < NCOL; j++) master[j] = __double2float_rn(__dmul_rn((double)master[j], fd));
-            }
-            const int64_t row = mb * 2 * BM + crank * BM + quad * 32 + lane;
-            const int64_t col0 = nb * BN_ + half * NCOL;
+            const int col0 = nb * BN_ + half * NCOL;
             if (tma_store) {
                 // stage 32 rows x 32 columns per step (row = lane, 16-B chunks XOR-swizzled by
                 // row % 8 as the map's SWIZZLE_128B expects: 4 wavefronts per warp store), then one
                 // lane stores the box with TMA (clipped at M, N); the buffer is reused once the
-                // previous store has read it
+                // previous store has read it.  tma_store == 2 (transposed C, the fused-A form
+                // C^T = B^T A^T): the box is staged transposed — lane L writes its 32 values down
+                // column L (one conflict-free wavefront per row) — and stored at (row, column)
+                // swapped into the map of the caller's C.
                 const uint32_t stg = smem_u32(staging + (warp - 2) * 4096);
-                const int32_t y = (int32_t)(mb * 2 * BM + crank * BM + quad * 32);
+                const int32_t r0 = (int32_t)(mb * 2 * BM + crank * BM + quad * 32);
 #pragma unroll
                 for (int c = 0; c < NCOL / 32; c++) {
                     if (lane == 0) bulk_wait_read0();
                     __syncwarp();
+                    if (tma_store == 2) {
 #pragma unroll
-                    for (int q = 0; q < 8; q++)
-                        st_shared_v4(stg + lane * 128 + ((q ^ (lane & 7)) * 16), master[c * 32 + 4 * q],
-                                     master[c * 32 + 4 * q + 1], master[c * 32 + 4 * q + 2], master[c * 32 + 4 * q + 3]);
+                        for (int j = 0; j < 32; j++)
+                            st_shared_f32(stg + j * 128 + ((((lane >> 2) ^ (j & 7)) * 16) | ((lane & 3) * 4)),
+                                          scl(master[c * 32 + j]));
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 8; q++)
+                            st_shared_v4(stg + lane * 128 + ((q ^ (lane & 7)) * 16), scl(master[c * 32 + 4 * q]),
+                                         scl(master[c * 32 + 4 * q + 1]), scl(master[c * 32 + 4 * q + 2]),
+                                         scl(master[c * 32 + 4 * q + 3]));
+                    }
                     fence_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        tma_store_2d(&mapC, stg, (int32_t)(col0 + c * 32), y);
+                        if (tma_store == 2) tma_store_2d(&mapC, stg, r0, (int32_t)(col0 + c * 32));
+                        else tma_store_2d(&mapC, stg, (int32_t)(col0 + c * 32), r0);
                         bulk_commit();
                     }
                 }
                 continue;
             }
-            if (row < M)
-            {
-                float* crow = C + row * ldc + col0;
-                if (vec_ok && col0 + NCOL <= N) {
+            // no TMA store (C not 16-B aligned, ldc % 4 != 0): the same 32 x 32 staging, then
+            // each lane stores one column of the staged rows (coalesced rows, clipped at M, N)
+            const uint32_t stg = smem_u32(staging + (warp - 2) * 4096);
+            const int row0 = mb * 2 * BM + crank * BM + quad * 32;
 #pragma unroll
-                    for (int j = 0; j < NCOL / 4; j++)
-                        reinterpret_cast<float4*>(crow)[j] =
-                            make_float4(master[4 * j], master[4 * j + 1], master[4 * j + 2], master[4 * j + 3]);
-                } else {
+            for (int c = 0; c < NCOL / 32; c++) {
 #pragma unroll
-                    for (int j = 0; j < NCOL; j++)
-                        if (col0 + j < N) crow[j] = master[j];
+                for (int q = 0; q < 8; q++)
+                    st_shared_v4(stg + lane * 128 + ((q ^ (lane & 7)) * 16), scl(master[c * 32 + 4 * q]),
+                                 scl(master[c * 32 + 4 * q + 1]), scl(master[c * 32 + 4 * q + 2]),
+                                 scl(master[c * 32 + 4 * q + 3]));
+                __syncwarp();
+                const int col = col0 + c * 32 + lane;
+                for (int r = 0; r < 32; r++) {
+                    const float v = ld_shared_f32(stg + r * 128 + ((((lane >> 2) ^ (r & 7)) * 16) | ((lane & 3) * 4)));
+                    if (row0 + r < M && col < N) C[(int64_t)(row0 + r) * ldc + col] = v;
                 }
+                __syncwarp();
             }
         }
     }
@@ -897,10 +924,10 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
 #if SPLIT3_DEBUG
     uint32_t dbg_epi_chunks = 0;     // warp 2's drained D_hi chunk count (recomputed: same loop shape)
     if (warp == 2 && leader) {
-        for (int64_t unit = pair; unit < num_units; unit += num_pairs) {
-            int64_t tile_unused;
+        for (int unit = pair; unit < num_units; unit += num_pairs) {
+            int tile_unused;
             int kb_begin, kb_end, slot;
-            decode_unit(unit, plan, num_kb, kps, tile_unused, kb_begin, kb_end, slot);
+            decode_unit(unit, up, num_kb, kps, tile_unused, kb_begin, kb_end, slot);
             dbg_epi_chunks += (uint32_t)((kb_end - kb_begin + promo_kb - 1) / promo_kb);
         }
     }
@@ -918,7 +945,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
         if (atomicAdd(wave_counter + 3, 1u) == gridDim.x - 1) {
 #if SPLIT3_DEBUG
             // every producer announced each of its units but the first: 2 CTAs x (units - 1) per pair
-            const int64_t busy = num_units < num_pairs ? num_units : num_pairs;
+            const int busy = num_units < num_pairs ? num_units : num_pairs;
             const unsigned expect = (unsigned)(2 * (num_units - busy));
             const unsigned got = atomicAdd(wave_counter, 0u);
             DBG_CHECK(got == expect, 7, ((unsigned long long)got << 32) | expect);
@@ -944,7 +971,10 @@ __global__ void __launch_bounds__(256) ksplit_reduce_kernel(const float* __restr
                                                             int64_t M, int64_t N, int group_m,
                                                             float* __restrict__ C, int64_t ldc,
                                                             const int32_t* __restrict__ d_sA,
-                                                            const int32_t* __restrict__ d_sB) {
+                                                            const int32_t* __restrict__ d_sB, int trans) {
+    // trans (the fused-A form C^T = B^T A^T): the kernel's (row, col) is C's (col, row); the block's
+    // kReduceRows x bn results go through shared memory so C's rows are written 64 B at a time
+    __shared__ float tT[kReduceRows][256 + 1];
     pdl_enter();
     const int sAB = *d_sA + *d_sB;
     const bool fast = sAB >= -126 && sAB <= 127;
@@ -954,16 +984,16 @@ __global__ void __launch_bounds__(256) ksplit_reduce_kernel(const float* __restr
     const int64_t blk = (int64_t)(2 * BM) * bn;
     const int64_t t = blockIdx.y;
     const int64_t num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + bn - 1) / bn;
-    int64_t mb, nb;
-    tile_coords(plan.whole + t, num_m, num_n, group_m, mb, nb);
+    int mb, nb;
+    tile_coords((int)(plan.whole + t), (int)num_m, (int)num_n, group_m, mb, nb);
     const int groups = bn / 4;                       // float4 column groups per row
     const int rows_per_pass = 256 / groups;
     const int g = threadIdx.x % groups;
-    const int64_t col = nb * bn + 4 * g;
+    const int64_t col = (int64_t)nb * bn + 4 * g;
     const bool vec = (ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(C) & 15u) == 0 && col + 4 <= N;
     for (int r = blockIdx.x * kReduceRows + threadIdx.x / groups; r < (int)(blockIdx.x + 1) * kReduceRows;
          r += rows_per_pass) {
-        const int64_t row = mb * 2 * BM + r;
+        const int64_t row = (int64_t)mb * 2 * BM + r;
         if (row >= M || col >= N) continue;
         const int64_t e = (int64_t)r * bn + 4 * g;
         float4 acc = *reinterpret_cast<const float4*>(P + t * blk + e);
@@ -972,6 +1002,12 @@ __global__ void __launch_bounds__(256) ksplit_reduce_kernel(const float* __restr
             acc.x = __fadd_rn(acc.x, v.x); acc.y = __fadd_rn(acc.y, v.y);
             acc.z = __fadd_rn(acc.z, v.z); acc.w = __fadd_rn(acc.w, v.w);
         }
+        if (trans) {
+            const int rr = r - (int)blockIdx.x * kReduceRows;
+            tT[rr][4 * g] = scale(acc.x); tT[rr][4 * g + 1] = scale(acc.y);
+            tT[rr][4 * g + 2] = scale(acc.z); tT[rr][4 * g + 3] = scale(acc.w);
+            continue;
+        }
         float* dst = C + row * ldc + col;
         if (vec) {
             *reinterpret_cast<float4*>(dst) = make_float4(scale(acc.x), scale(acc.y), scale(acc.z), scale(acc.w));
@@ -979,6 +1015,14 @@ __global__ void __launch_bounds__(256) ksplit_reduce_kernel(const float* __restr
             const float a[4] = {acc.x, acc.y, acc.z, acc.w};
             for (int j = 0; j < 4 && col + j < N; j++) dst[j] = scale(a[j]);
         }
+    }
+    if (!trans) return;
+    __syncthreads();
+    const int rr = threadIdx.x % kReduceRows;
+    const int64_t krow = (int64_t)mb * 2 * BM + blockIdx.x * kReduceRows + rr;   // C's column
+    for (int cc = threadIdx.x / kReduceRows; cc < bn; cc += 256 / kReduceRows) {
+        const int64_t kcol = (int64_t)nb * bn + cc;                            // C's row
+        if (krow < M && kcol < N) C[kcol * ldc + krow] = tT[rr][cc];
     }
 }
 
@@ -1175,7 +1219,7 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
                  const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB, float* C, int64_t ldc,
                  int terms, int num_sms, int promo_kb, unsigned* wave_counter, const GemmTuneIn& tin,
                  float* partial, int64_t partial_elems, int* err, const uint16_t* A3, const uint16_t* B3t,
-                 int mn, const float* Bf, int64_t ldb, const float* d_maxB) {
+                 int mn, const float* Bf, int64_t ldb, const float* d_maxB, int c_trans) {
     const bool b_mn = (mn & 1) != 0, a_mn = (mn & 2) != 0;
     CUtensorMap ma1, ma2, mb1, mb2, ma3, mb3;
     if (Bf) {   // fused B (3-term): fp32 B map in place of the B plane maps
@@ -1211,7 +1255,20 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     // TMA-store epilogue when C allows it (else per-thread float4 / scalar stores)
     CUtensorMap mc = ma1;
     int tma_store = 0;
-    if ((ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(C) & 15u) == 0 && make_c_map(&mc, C, M, N, ldc)) tma_store = 1;
+    const bool c_tma_ok = (ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(C) & 15u) == 0;
+    if (c_trans) {   // the caller's C is N x M (this GEMM computes its transpose): TMA stores only
+        if (!c_tma_ok) {
+            *err = 1;   // SPLIT3_ERR_INVALID_VALUE
+            return -1;
+        }
+        if (!make_c_map(&mc, C, N, M, ldc)) {
+            *err = 4;
+            return -1;
+        }
+        tma_store = 2;
+    } else if (c_tma_ok && make_c_map(&mc, C, M, N, ldc)) {
+        tma_store = 1;
+    }
     const int promo = promo_kb > 0 ? promo_kb : kDefaultPromoKb;
     GemmTune tune;
     tune.group_m = tin.group_m > 0 ? tin.group_m : kDefaultGroupM;
@@ -1219,6 +1276,11 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     tune.pol_a = pol(tin.pol_a);
     tune.pol_b = pol(tin.pol_b);
     SplitPlan plan = gemm3_split_plan(M, N, K, terms, num_sms, promo);
+    // the kernel indexes work units and tiles in 32 bits (far above any matrix that fits in HBM)
+    if (plan.whole + plan.nsplit * plan.slices > INT32_MAX || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) {
+        *err = 1;   // SPLIT3_ERR_INVALID_VALUE
+        return -1;
+    }
     if (plan.slices > 1 && (!partial || gemm3_partial_elems(plan, terms) > partial_elems)) {
         plan.whole += plan.nsplit;   // no room for partials: whole tiles only
         plan.nsplit = 0;
@@ -1238,7 +1300,8 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     if (plan.slices > 1) {
         const int bn = terms == 4 ? 128 : 256;
         const dim3 grid((unsigned)(2 * BM / kReduceRows), (unsigned)plan.nsplit);
-        launch_k(ksplit_reduce_kernel, grid, dim3(256), 0, st, partial, plan, bn, M, N, tune.group_m, C, ldc, d_sA, d_sB);
+        launch_k(ksplit_reduce_kernel, grid, dim3(256), 0, st, partial, plan, bn, M, N, tune.group_m, C, ldc, d_sA, d_sB,
+                 c_trans ? 1 : 0);
         if (cudaPeekAtLastError() != cudaSuccess) { *err = 4; return -1; }
         r += 1;
     }

@@ -148,6 +148,8 @@ int64_t gemm3_partial_elems(const SplitPlan& p, int terms);   // floats of parti
 // Fused B (terms == 3 only): Bf != NULL is the fp32 B itself (mn bit 0: K x N
 // row-major, else stored N x K; ldb % 4 == 0, 16-B aligned) and d_maxB its max-abs; the GEMM splits
 // it in shared memory (B1t/B2t are ignored) and writes the scale exponent to d_sB.
+// c_trans != 0: C (ldc) is the caller's N x M matrix and receives the TRANSPOSE of this M x N
+// product (the fused-A form C_caller = (B^T A^T)^T); C must be 16-B aligned with ldc % 4 == 0.
 // Returns kernels launched (1, or 2 with the split-K reduction) or -1 (*err set to a status).
 int launch_gemm3(cudaStream_t s, int64_t M, int64_t N, int64_t K,
                  const uint16_t* A1, const uint16_t* A2, int64_t ldpa, const int32_t* d_sA,
@@ -155,7 +157,7 @@ int launch_gemm3(cudaStream_t s, int64_t M, int64_t N, int64_t K,
                  float* C, int64_t ldc, int terms, int num_sms, int promo_kb,
                  unsigned* wave_counter, const GemmTuneIn& tune, float* partial, int64_t partial_elems,
                  int* err, const uint16_t* A3 = nullptr, const uint16_t* B3t = nullptr, int mn = 0,
-                 const float* Bf = nullptr, int64_t ldb = 0, const float* d_maxB = nullptr);
+                 const float* Bf = nullptr, int64_t ldb = 0, const float* d_maxB = nullptr, int c_trans = 0);
 
 // ---- mlp_kernels.cu (NEXT #3: the non-GEMM steps of a dense-network training step) --------
 int launch_bias_act(cudaStream_t s, int64_t M, int64_t N, const float* Z, int64_t ldz, const float* b, float* H,

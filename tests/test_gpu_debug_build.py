@@ -1,7 +1,7 @@
 """The checked debug build (libsplit3_debug.so, -DSPLIT3_DEBUG=1) — the substitute
 for compute-sanitizer on this GPU pool: mbarrier watchdogs and pipeline invariants inside the GEMM.
 
-  * over the shapes, term counts, operand layouts, split-K tails, the fused-B path and the 2-D
+  * over the shapes, term counts, operand layouts, split-K tails, the fused-B and fused-A paths and the 2-D
     driver's pieces of the parity suite, the debug build records no failure and its C is bitwise
     the release build's;
   * an injected fault (a TMA load that never happens) is caught by the watchdog: the record (in
@@ -46,6 +46,10 @@ h.set_fused_split(2)
 A = torch_matrix("uniform", 1024, 2048, seed=3); B = torch_matrix("uniform", 2048, 4096, seed=4)
 rec("fusedB", h.sgemm(A, B))
 h.set_fused_split(1)
+h.set_fused_split_a(2)
+rec("fusedA", h.sgemm(B.t().contiguous(), A.t().contiguous()))
+rec("fusedA_splitk", h.sgemm(torch_matrix("uniform", 2048, 4096, seed=5), torch_matrix("uniform", 4096, 256, seed=6)))
+h.set_fused_split_a(1)
 h.set_split_k(False)
 rec("wholetiles", h.sgemm(A, B))
 h.set_max_sms(132)

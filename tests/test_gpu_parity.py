@@ -197,6 +197,34 @@ def test_three_term_equals_one_term_when_residual_zero(h):
     assert np.array_equal(c3.view(np.uint32), c1.view(np.uint32))
 
 
+@pytest.mark.parametrize("shape", [(300, 200, 1000), (256, 256, 4096), (2304, 520, 640)])
+@pytest.mark.parametrize("e", [-70, -60, 56])
+def test_epilogue_scale_outside_fp32_normal_range(h, shape, e):
+    """a4's final factor 2^(sA+sB) outside the fp32 normal range (the epilogue's fp64 path; the
+    split-K reduction's too): A, B scaled by 2^e have the same planes as A, B (per-matrix power of
+    two, R1), so C_e must equal RN32(C * 2^(2e)) bit for bit — one rounding of the exact product.
+    e = -70 / -60: sA + sB ~ -170 / -150 (subnormal and flushed results); e = 56: ~ +82 (fast path,
+    control).  Shapes: fused B (M <= 2048), a split-K single tile, whole tiles; TMA-store C and a
+    strided C (scalar stores)."""
+    M, N, K = shape
+    A = numpy_matrix("uniform", M, K, seed=M + 7)
+    B = numpy_matrix("uniform", K, N, seed=N + 8)
+    f = np.float32(2.0 ** e)
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    Ae, Be = torch.from_numpy(A * f).cuda(), torch.from_numpy(B * f).cuda()
+    for terms in (3, 4, 1):
+        kw = dict(four_term=terms == 4, one_term=terms == 1)
+        C = h.sgemm(Ad, Bd, **kw).cpu().numpy()
+        want = (C.astype(np.float64) * 2.0 ** (2 * e)).astype(np.float32)
+        got = h.sgemm(Ae, Be, **kw).cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (terms, e)
+        Cbig = torch.full((M, N + 3), 7.0, device="cuda")
+        h.sgemm(Ae, Be, out=Cbig[:, 1:1 + N], **kw)
+        assert np.array_equal(Cbig[:, 1:1 + N].cpu().numpy().view(np.uint32), want.view(np.uint32)), (terms, e)
+    if e < 0:
+        assert np.count_nonzero(want) > 0 and np.any(np.abs(want[want != 0]) < np.float32(2.0 ** -126))
+
+
 def test_strided_operands_and_output(h, orc):
     M, N, K = 100, 90, 130
     Abig = torch.from_numpy(numpy_matrix("uniform", M, K + 6, seed=1)).cuda()

@@ -45,6 +45,8 @@ def timed(fn, reps):
 hs, hf = s3.Handle(0), s3.Handle(0)
 hs.set_fused_split(0)
 hf.set_fused_split(2)
+hs.set_fused_split_a(0)      # B's fusion alone (no fused-A auto choice for N < M)
+hf.set_fused_split_a(0)
 rows = []
 for shp in a.shapes.split(","):
     M, N, K = (int(x) for x in shp.split("x"))

@@ -17,6 +17,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 if os.environ.get("PAB_CHILD"):
+    if os.environ.get("EXP_ROOT"):   # another checkout's package (tools/exp/<tag>/, git-ignored)
+        sys.path.insert(0, os.environ["EXP_ROOT"])
     import pynvml
     import torch
 
@@ -84,7 +86,9 @@ for r in range(a.rounds):
         for item in kv:
             k, v = item.split("=")
             env[k] = v
-        if lib != "base":
+        if lib != "base" and os.path.isdir(os.path.join(ROOT, "tools", "exp", lib)):
+            env["EXP_ROOT"] = os.path.join(ROOT, "tools", "exp", lib)
+        elif lib != "base":
             env["EXP_LIB"] = os.path.join(ROOT, "tools", "exp", f"libsplit3_{lib}.so")
         out = subprocess.run([sys.executable, __file__], env=env, capture_output=True, text=True)
         try:
