@@ -427,6 +427,7 @@ def main():
         step()
     torch.cuda.synchronize()
     launches_per_step = h.last_launch_count() if not use_dist else tg.launches_per_step()
+    path = h.last_path() if not use_dist else 0     # SPLIT3_PATH_* bits of the step's call
 
     gpu_idx = local
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
@@ -499,7 +500,8 @@ def main():
                 "gemm_launches_per_step": ncalls / args.steps,
                 "split_ms_per_step": split_ms / args.steps if not use_dist else None,
                 "split_hbm_gbs": (12.0 * 2 * n * n / (split_ms / args.steps / 1e3) / 1e9)
-                if ncalls and split_ms > 0 and not use_dist else None}
+                if ncalls and split_ms > 0 and not use_dist else None,
+                "path_bits": path}
 
     cpu = None
     if rank == 0 and not use_dist and not args.no_cpu:

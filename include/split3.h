@@ -247,6 +247,13 @@ int split3_gemm_planes(split3_handle_t h, int64_t M, int64_t N, int64_t K,
  * gpu_launches count; memsets are not counted). */
 int split3_last_launch_count(split3_handle_t h);
 
+/* Which path the last split3_sgemm / split3_sgemm_ex call took (bitwise OR; 0 = the plain
+ * sequential path: max-abs, separate splits, GEMM).  For tests and the benchmark's report. */
+#define SPLIT3_PATH_FUSED_B 1   /* B split inside the GEMM (split3_set_fused_split) */
+#define SPLIT3_PATH_FUSED_A 2   /* A split inside the GEMM, C^T = B^T A^T (split3_set_fused_split_a) */
+#define SPLIT3_PATH_PREP    8   /* one-launch max-abs + split front end (small calls) */
+int split3_last_path(split3_handle_t h);
+
 /* ---- dense-network step helpers ----------------------------
  * The GEMMs of a dense-layer training step go through split3_sgemm_ex; these FP32 kernels do the
  * rest (SPEC.md mlp ledger: bias, activations, softmax/cross-entropy never in fp16).  All are

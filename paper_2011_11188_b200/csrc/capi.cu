@@ -29,6 +29,7 @@ struct split3_ctx {
     size_t ws_bytes = 0;
     long long last_bad = -1;
     int last_launches = 0;
+    int last_path = 0;   // SPLIT3_PATH_* bits of the last split3_sgemm_ex call
     int promo_kb = 0;   // 0 = library default
     int wave_sync = 1;  // GEMM wave lockstep hint (L2 locality)
     int split_k = 1;    // split-K tail for partial last waves (0: whole tiles only, split3_set_split_k)
@@ -305,6 +306,7 @@ int split3_sgemm_set_workspace(split3_handle_t h, void* dptr, size_t bytes) {
 int64_t split3_last_bad_index(split3_handle_t h) { return h ? h->last_bad : -1; }
 
 int split3_last_launch_count(split3_handle_t h) { return h ? h->last_launches : 0; }
+int split3_last_path(split3_handle_t h) { return h ? h->last_path : 0; }
 int64_t split3_host_redo_count(split3_handle_t h) { return h ? h->host_redo : -1; }
 
 int split3_maxabs(split3_handle_t h, int64_t rows, int64_t cols, const float* X, int64_t ldx,
@@ -494,6 +496,7 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     if ((flags & SPLIT3_BF16X3) && (flags & (SPLIT3_ONE_TERM | SPLIT3_FOUR_TERM))) return SPLIT3_ERR_INVALID_VALUE;
     h->last_launches = 0;
     h->last_bad = -1;
+    h->last_path = 0;
     if (M == 0 || N == 0) return SPLIT3_OK;
     if (!C || ldc < N) return SPLIT3_ERR_INVALID_VALUE;
     const int terms = terms_of(flags);
@@ -604,6 +607,7 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
             return SPLIT3_ERR_NOT_FINITE;
         }
     }
+    h->last_path = (fuse_b ? SPLIT3_PATH_FUSED_B : 0) | (fuse_a ? SPLIT3_PATH_FUSED_A : 0) | (prepped ? SPLIT3_PATH_PREP : 0);
     // a2: split into K-major planes (A: M x K, B: N x K)
     const uint16_t *A1 = A->hi, *A2 = A->lo, *B1t = B->hi, *B2t = B->lo;
     const int32_t *sA = A->d_sexp, *sB = B->d_sexp;

@@ -37,7 +37,7 @@ EXPORTS = (
     "split3_sgemm_workspace_size", "split3_sgemm_ex_workspace_size", "split3_sgemm_set_workspace", "split3_sgemm",
     "split3_sgemm_host_workspace_size", "split3_sgemm_host", "split3_last_bad_index", "split3_host_redo_count", "split3_host_last_layout",
     "split3_status_string", "split3_maxabs", "split3_split", "split3_gemm_planes",
-    "split3_last_launch_count", "split3_timing_enable", "split3_timing_read",
+    "split3_last_launch_count", "split3_last_path", "split3_timing_enable", "split3_timing_read",
     "split3_set_promotion", "split3_set_wave_sync", "split3_set_split_k", "split3_set_max_sms", "split3_set_schedule", "split3_set_fused_split", "split3_set_fused_split_a",
     "split3_sgemm_ex", "split3_presplit", "split3_presplit_stored", "split3_split_bf16x3", "split3_debug_read", "split3_debug_fault", "split3_bias_act", "split3_relu_backward",
     "split3_softmax_xent", "split3_bias_grad", "split3_sgd_update",
@@ -124,6 +124,7 @@ def load() -> ctypes.CDLL:
         lib.split3_host_redo_count.restype = _i64
         lib.split3_host_redo_count.argtypes = [_p]
         lib.split3_last_launch_count.argtypes = [_p]
+        lib.split3_last_path.argtypes = [_p]
         lib.split3_timing_enable.argtypes = [_p, ctypes.c_int]
         lib.split3_set_promotion.argtypes = [_p, ctypes.c_int]
         lib.split3_set_wave_sync.argtypes = [_p, ctypes.c_int]
@@ -355,6 +356,10 @@ class Handle:
         out = split3_host_layout()
         self._chk(self._lib.split3_host_last_layout(self._h, ctypes.byref(out)), "split3_host_last_layout")
         return out
+
+    def last_path(self) -> int:
+        """SPLIT3_PATH_* bits of the last call: 1 fused B, 2 fused A, 8 one-launch front end."""
+        return int(self._lib.split3_last_path(self._h))
 
     def last_launch_count(self) -> int:
         return int(self._lib.split3_last_launch_count(self._h))

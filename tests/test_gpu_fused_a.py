@@ -66,6 +66,7 @@ def test_fused_a_equals_transposed_and_plain(ha, hs, M, N, K, dist):
     A = torch_matrix(dist, M, K, seed=61)
     B = torch_matrix("uniform", K, N, seed=62)
     Ca = ha.sgemm(A, B).clone()
+    assert bool(ha.last_path() & 2) == _eligible(K, N)      # SPLIT3_PATH_FUSED_A
     Ct = _ref_t(hs, A, B)          # (B^T A^T)^T, separate split
     Cs = hs.sgemm(A, B)            # untransposed: same sums, another in-MMA order (module docstring)
     assert torch.equal(_bits(Ca), _bits(Ct if _eligible(K, N) else Cs))
