@@ -332,6 +332,19 @@ int split3_set_max_sms(split3_handle_t h, int sms);
  * SPLIT3_FUSE_B_MAX_M at handle creation.  INVALID_VALUE for mode outside 0..2 or max_m < 0. */
 int split3_set_fused_split(split3_handle_t h, int mode, int64_t max_m);
 
+/* Folded accumulator (SURVEY §8f NEXT #2's D_lo fold, generalised): the 3-term
+ * (4-term) products of each 64-wide k-block go into ONE TMEM accumulator T — [A2*B2 first], then
+ * A1*B2 + A2*B1 entered with tcgen05's scale-input-d (T <- products + 2^-11 T), then A1*B1 likewise
+ * — so T = D_hi + 2^-11 D_mid [+ 2^-22 D_lo] of the k-block, and the epilogue adds T into the FP32
+ * master with one RN every k-block (the promotion period is 1 whatever split3_set_promotion says).
+ * No separate D_mid / D_lo accumulators: two T buffers ping-pong in TMEM and the 4-term path keeps
+ * 256-wide tiles (the unfolded 4-term kernel needs 256 TMEM columns more and runs 256 x 128
+ * tiles).  Rounding differs from the unfolded kernel; same oracle tolerance.  mode 0: never;
+ * 1 (default): 4-term calls (measured +5 %); 2: 4- and 3-term calls (3-term: -1.6 %, one more
+ * promotion per k-block under the power cap).  Env: SPLIT3_FOLD.  INVALID_VALUE for mode outside
+ * 0..2. */
+int split3_set_fold(split3_handle_t h, int mode);
+
 /* Fused split of A (SURVEY §8f NEXT #2 for the other operand; Eq. A_1 applied inside the GEMM):
  * for a 3-term call whose A is an fp32 matrix (not pre-split; row-major M x K, or stored K x M
  * with transA = 1), 16-byte aligned with ld % 4 == 0, and whose C is 16-byte aligned with

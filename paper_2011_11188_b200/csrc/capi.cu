@@ -50,6 +50,10 @@ struct split3_ctx {
     // whenever eligible (before fused B).  env SPLIT3_FUSE_A, SPLIT3_FUSE_A_MAX_N
     int fuse_a = 0;
     int64_t fuse_a_max_n = 2048;
+    // folded accumulator (LAY_FOLD): 3-/4-term products of a k-block summed in ONE TMEM
+    // accumulator with tcgen05's scale-input-d, promoted every k-block.  0 never, 1 (default)
+    // 4-term calls, 2 4- and 3-term calls.  env SPLIT3_FOLD
+    int fold = 1;
     split3::GemmTuneIn tune;
     unsigned* d_counters = nullptr;   // 256 B of device scratch owned by the handle
     // host-buffer entry: copy-in / copy-out streams and events, created on first use
@@ -140,7 +144,9 @@ constexpr int kMaxSms = 148;
 int64_t partial_elems_bound(int64_t M, int64_t N, int64_t K, int terms) {
     int64_t mx = 0;
     for (int sms = 2; sms <= kMaxSms; sms += 2)
-        mx = std::max(mx, split3::gemm3_partial_elems(split3::gemm3_split_plan(M, N, K, terms, sms, 0), terms));
+        for (int fold = 0; fold < 2; fold++)   // (the folded 4-term kernel has 256-wide tiles)
+            mx = std::max(mx, split3::gemm3_partial_elems(split3::gemm3_split_plan(M, N, K, terms, sms, 0, fold != 0),
+                                                          terms, fold != 0));
     return mx;
 }
 
@@ -252,6 +258,7 @@ int split3_sgemm_create(split3_handle_t* h, int device, void* cuda_stream) {
     if (const char* e = getenv("SPLIT3_HOST_PANELS")) c->host_panels = std::min(std::max(atoi(e), 0), 4);
     if (const char* e = getenv("SPLIT3_FUSE_B_MAX_M")) c->fuse_b_max_m = atoll(e);
     if (const char* e = getenv("SPLIT3_FUSE_A")) c->fuse_a = atoi(e);
+    if (const char* e = getenv("SPLIT3_FOLD")) c->fold = std::min(std::max(atoi(e), 0), 2);
     if (const char* e = getenv("SPLIT3_FUSE_A_MAX_N")) c->fuse_a_max_n = atoll(e);
     *h = c;
     return SPLIT3_OK;
@@ -384,7 +391,8 @@ int split3_gemm_planes(split3_handle_t h, int64_t M, int64_t N, int64_t K, const
     int err = 0;
     int n = split3::launch_gemm3(h->stream, M, N, K, A1, A2, ldpa, d_sA, B1t, B2t, ldpb, d_sB, C,
                                  ldc, terms, gemm_sms(h), h->promo_kb,
-                                 h->wave_sync ? h->d_counters : nullptr, h->tune, nullptr, 0, &err);
+                                 h->wave_sync ? h->d_counters : nullptr, h->tune, nullptr, 0, &err, nullptr, nullptr,
+                                 0, nullptr, 0, nullptr, 0, h->fold);
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
     h->last_launches = n;
@@ -662,12 +670,13 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
         n = split3::launch_gemm3(h->stream, N, M, K, B1t, B2t, ldpb, sB, nullptr, nullptr, 0, sA, C, ldc, terms,
                                  gemm_sms(h), h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune,
                                  h->split_k ? partial : nullptr, partial_elems, &err, nullptr, nullptr,
-                                 (A->trans ? 1 : 0) | (b_mn ? 2 : 0), A->data, A->ld, w.maxA, 1);
+                                 (A->trans ? 1 : 0) | (b_mn ? 2 : 0), A->data, A->ld, w.maxA, 1, h->fold);
     else
         n = split3::launch_gemm3(h->stream, M, N, K, A1, A2, ldpa, sA, B1t, B2t, ldpb, sB, C, ldc, terms,
                                  gemm_sms(h), h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune,
                                  h->split_k ? partial : nullptr, partial_elems, &err, nullptr, nullptr,
-                                 (b_mn ? 1 : 0) | (a_mn ? 2 : 0), fuse_b ? B->data : nullptr, B->ld, w.maxB);
+                                 (b_mn ? 1 : 0) | (a_mn ? 2 : 0), fuse_b ? B->data : nullptr, B->ld, w.maxB, 0,
+                                 h->fold);
     if (n < 0) return err ? err : SPLIT3_ERR_CUDA;
     record(h, ev2);
     launches += n;
@@ -832,6 +841,12 @@ int split3_set_fused_split(split3_handle_t h, int mode, int64_t max_m) {
     if (!h || mode < 0 || mode > 2 || max_m < 0) return SPLIT3_ERR_INVALID_VALUE;
     h->fuse_b = mode;
     if (max_m > 0) h->fuse_b_max_m = max_m;
+    return SPLIT3_OK;
+}
+
+int split3_set_fold(split3_handle_t h, int mode) {
+    if (!h || mode < 0 || mode > 2) return SPLIT3_ERR_INVALID_VALUE;
+    h->fold = mode;
     return SPLIT3_OK;
 }
 
@@ -1042,7 +1057,7 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
         int r = split3::launch_gemm3(s0, mr, nc, K, w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa, w.ldpa, d_sA, w.B1t + c0,
                                      w.B2t + c0, ldpb, d_sB, dC + r0 * N + c0, N, terms_of(flags), gemm_sms(h),
                                      h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune, nullptr, 0, &err,
-                                     nullptr, nullptr, b_mn ? 1 : 0);
+                                     nullptr, nullptr, b_mn ? 1 : 0, nullptr, 0, nullptr, 0, h->fold);
         return r < 0 ? -(err ? err : SPLIT3_ERR_CUDA) : r;
     };
     auto copy_out = [&](int b, int j, cudaStream_t st) {

@@ -27,8 +27,12 @@
 //    master in registers, the final fma with D_mid, the exact 2^(sA+sB) rescale and TMA stores);
 //    fused-B builds add warps 10..11, converters that split B's fp32 tiles in shared memory;
 //  * TMEM (512 columns per CTA): 3-term D_hi [0,256) + D_mid [256,512) (one D_hi buffer: the MMA
-//    warp issues a k-block's D_mid MMAs before waiting for the drained D_hi); 4-term (BN = 128)
-//    D_hi ping-pong [0,256) + D_mid [256,384) + D_lo [384,512); 1-term D_hi ping-pong.
+//    warp issues a k-block's D_mid MMAs before waiting for the drained D_hi); unfolded 4-term
+//    (BN = 128) D_hi ping-pong [0,256) + D_mid [256,384) + D_lo [384,512); 1-term D_hi ping-pong;
+//  * folded accumulator (LAY bit 3, the 4-term default): per k-block ONE accumulator T takes
+//    A2*B2, then A1*B2 + A2*B1 entered with tcgen05 scale-input-d 11 (T <- P + 2^-11 T), then
+//    A1*B1 likewise; T ping-pongs in [0,256) / [256,512) and is promoted every k-block — no D_mid
+//    or D_lo accumulator, so 4-term keeps 256-wide tiles.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -49,6 +53,7 @@ constexpr int NUM_EPI_WARPS = 8;                    // 2 per TMEM lane quadrant
 constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;   // TMA warp, MMA warp, epilogue warps
 constexpr int NUM_CONV_WARPS = 2;                   // fused-B variant: fp32 -> plane converter warps
 constexpr int LAY_FB = 4;                           // LAY bit 2: B arrives as fp32, split in SMEM
+constexpr int LAY_FOLD = 8;                         // LAY bit 3: one accumulator per k-block (scale-input-d fold)
 template <int LAY>
 struct NThr { static constexpr int v = NUM_THREADS + ((LAY & LAY_FB) ? 32 * NUM_CONV_WARPS : 0); };
 constexpr uint32_t TMEM_COLS = 512;
@@ -249,6 +254,16 @@ __device__ __forceinline__ void mma_pair_reuse_a(uint32_t d_tmem, uint64_t adesc
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::2.kind::f16.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// D = A * B + 2^-11 * D (tcgen05 scale-input-d = 11): the folded accumulator's step from a
+// lower-weight group of products to the next one up (LAY_FOLD)
+__device__ __forceinline__ void mma_pair_fold11(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, 1, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p, 11;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc)
         : "memory");
 }
 // arrive (once) on the barrier at this offset in BOTH CTAs of the pair when the MMAs complete
@@ -456,6 +471,13 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     constexpr int PL = BF3 ? 3 : 2;
     constexpr bool FB = (LAY & LAY_FB) != 0;
     static_assert(!FB || TERMS == 3, "fused B: 3-term only");
+    // Folded accumulator (LAY_FOLD): per k-block ONE TMEM accumulator T takes, in order,
+    // [A2*B2 (4-term)], then A1*B2 + A2*B1 entered with scale-input-d 11 (T <- products + 2^-11 T),
+    // then A1*B1 entered likewise, so T = D_hi + 2^-11 D_mid [+ 2^-22 D_lo] of that k-block; the
+    // epilogue adds T into the FP32 master with RN every k-block (promotion period 1).  No D_mid /
+    // D_lo accumulators: two 256-column T buffers ping-pong, 4-term keeps 256-wide tiles.
+    constexpr bool FOLD = (LAY & LAY_FOLD) != 0;
+    static_assert(!FOLD || ((TERMS == 3 || TERMS == 4) && BN_ == 256), "fold: 3-/4-term, 256-wide tiles");
     using G = Geo<BN_, PL>;
     constexpr int F32_BYTES = G::BNH * BK * 4;   // fused B: one fp32 tile = the stage's B region
     static_assert(!FB || F32_BYTES == 2 * G::TILE_B_BYTES, "fused B: in-place split");
@@ -464,12 +486,12 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
     constexpr int TILE_B_BYTES = G::TILE_B_BYTES;
     constexpr int BNH = G::BNH;
     constexpr bool LOAD_LO = TERMS != 1;
-    constexpr bool HAS_MID = TERMS != 1;
+    constexpr bool HAS_MID = TERMS != 1 && !FOLD;
     // TMEM columns per CTA: 512.  D_hi chunk buffers (HB of them), then D_mid (+ D_lo).
-    constexpr int HB = (TERMS == 1 || BN_ == 128) ? 2 : 1;
+    constexpr int HB = (TERMS == 1 || BN_ == 128 || FOLD) ? 2 : 1;
     constexpr uint32_t COL_MID = HB * BN_;
     constexpr uint32_t COL_LO = COL_MID + BN_;
-    static_assert(HB * BN_ + (HAS_MID ? BN_ : 0) + (TERMS == 4 ? BN_ : 0) <= 512, "TMEM budget");
+    static_assert(HB * BN_ + (HAS_MID ? BN_ : 0) + (TERMS == 4 && !FOLD ? BN_ : 0) <= 512, "TMEM budget");
     constexpr uint32_t TX_BYTES =
         FB ? 2u * (2 * TILE_A_BYTES) : 2u * (LOAD_LO ? STAGE_BYTES : TILE_A_BYTES + TILE_B_BYTES);
     constexpr bool BMN = (LAY & 1) != 0, AMN = (LAY & 2) != 0;
@@ -719,8 +741,35 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ 
                     // wait and D_mid is already owned): per K = 16 step A1*B1 -> D_hi keeps A1 in the
                     // collector and A1*B2 -> D_mid reuses it, so A1 is read from shared memory once
                     // instead of twice.  Same accumulators, same per-accumulator order: same bits.
-                    const bool interleave = TERMS == 3 && !BF3 && !chunk_start && kb + 1 != kb_end && mid_ready;
-                    if (interleave) {
+                    const bool interleave = TERMS == 3 && !BF3 && !FOLD && !chunk_start && kb + 1 != kb_end && mid_ready;
+                    if (FOLD) {
+                        // one k-block per chunk: T[hb] = [A2B2], then + A1B2 + A2B1 entered with
+                        // T <- P + 2^-11 T, then + A1B1 likewise (every K = 16 step of a group
+                        // before the next group: the 2^-11 applies to the whole lower group)
+                        mbar_wait(smem_u32(&hempty_bar[hb]), hphase ^ 1);
+                        tc_fence_after();
+                        if (elect_one()) {
+                            if (TERMS == 4) {
+#pragma unroll
+                                for (int k = 0; k < BK / 16; k++)
+                                    mma_pair(t_hi, a2 + DKA * k, b2 + DKB * k, IDESC, k > 0 ? 1u : 0u);
+                            }
+#pragma unroll
+                            for (int k = 0; k < BK / 16; k++) {
+                                const uint64_t dk = DKA * k, dkb = DKB * k;
+                                if (TERMS == 4 && k == 0) mma_pair_fold11(t_hi, a1 + dk, b2 + dkb, IDESC);
+                                else mma_pair(t_hi, a1 + dk, b2 + dkb, IDESC, (TERMS == 4 || k > 0) ? 1u : 0u);
+                                mma_pair(t_hi, a2 + dk, b1 + dkb, IDESC, 1u);
+                            }
+#pragma unroll
+                            for (int k = 0; k < BK / 16; k++) {
+                                if (k == 0) mma_pair_fold11(t_hi, a1, b1, IDESC);
+                                else mma_pair(t_hi, a1 + DKA * k, b1 + DKB * k, IDESC, 1u);
+                            }
+                            mma_commit_pair(smem_u32(&hfull_bar[hb]));
+                        }
+                        __syncwarp();
+                    } else if (interleave) {
                         if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < BK / 16; k++) {
@@ -1181,8 +1230,8 @@ int gemm3_debug_fault(int fault) {
 #endif
 }
 
-SplitPlan gemm3_split_plan(int64_t M, int64_t N, int64_t K, int terms, int num_sms, int promo_kb) {
-    const int bn = terms == 4 ? 128 : 256;
+SplitPlan gemm3_split_plan(int64_t M, int64_t N, int64_t K, int terms, int num_sms, int promo_kb, bool fold) {
+    const int bn = (terms == 4 && !fold) ? 128 : 256;
     const int64_t tiles = ((M + 255) / 256) * ((N + bn - 1) / bn);
     const int64_t pairs = num_sms / 2;
     const int64_t num_kb = (K + 63) / 64;
@@ -1209,8 +1258,8 @@ SplitPlan gemm3_split_plan(int64_t M, int64_t N, int64_t K, int terms, int num_s
     return p;
 }
 
-int64_t gemm3_partial_elems(const SplitPlan& p, int terms) {
-    const int bn = terms == 4 ? 128 : 256;
+int64_t gemm3_partial_elems(const SplitPlan& p, int terms, bool fold) {
+    const int bn = (terms == 4 && !fold) ? 128 : 256;
     return p.slices > 1 ? (int64_t)p.slices * p.nsplit * 256 * bn : 0;
 }
 
@@ -1219,7 +1268,11 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
                  const uint16_t* B2t, int64_t ldpb, const int32_t* d_sB, float* C, int64_t ldc,
                  int terms, int num_sms, int promo_kb, unsigned* wave_counter, const GemmTuneIn& tin,
                  float* partial, int64_t partial_elems, int* err, const uint16_t* A3, const uint16_t* B3t,
-                 int mn, const float* Bf, int64_t ldb, const float* d_maxB, int c_trans) {
+                 int mn, const float* Bf, int64_t ldb, const float* d_maxB, int c_trans, int fold) {
+    // folded accumulator (LAY_FOLD): fold 1 = 4-term only (measured +5 % there, 3-term -1.6 %:
+    // profiles/fold_ab_*_r02.json), 2 = 3- and 4-term
+    const bool fd = (terms == 4 && fold >= 1) || (terms == 3 && fold >= 2);
+    const int bn_t = (terms == 4 && !fd) ? 128 : 256;         // tile width
     const bool b_mn = (mn & 1) != 0, a_mn = (mn & 2) != 0;
     CUtensorMap ma1, ma2, mb1, mb2, ma3, mb3;
     if (Bf) {   // fused B (3-term): fp32 B map in place of the B plane maps
@@ -1231,7 +1284,7 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     }
     const uint16_t* A2e = terms == 1 ? A1 : A2;
     const uint16_t* B2e = terms == 1 ? B1t : B2t;
-    const int bnh = (terms == 4 ? 128 : 256) / 2;
+    const int bnh = bn_t / 2;
     // B planes: K-major N x K (box 64 K x bnh N), or MN-major K x N (box 64 N x 64 K, bnh/64 per plane)
     auto map_b = [&](CUtensorMap* m, const uint16_t* p) {
         return b_mn ? make_plane_map(m, p, K, N, ldpb, BK) : make_plane_map(m, p, N, K, ldpb, bnh);
@@ -1269,19 +1322,19 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     } else if (c_tma_ok && make_c_map(&mc, C, M, N, ldc)) {
         tma_store = 1;
     }
-    const int promo = promo_kb > 0 ? promo_kb : kDefaultPromoKb;
+    const int promo = fd ? 1 : (promo_kb > 0 ? promo_kb : kDefaultPromoKb);   // fold: every k-block
     GemmTune tune;
     tune.group_m = tin.group_m > 0 ? tin.group_m : kDefaultGroupM;
     auto pol = [](int p) { return p == 1 ? kPolicyFirst : (p == 2 ? kPolicyLast : kPolicyNormal); };
     tune.pol_a = pol(tin.pol_a);
     tune.pol_b = pol(tin.pol_b);
-    SplitPlan plan = gemm3_split_plan(M, N, K, terms, num_sms, promo);
+    SplitPlan plan = gemm3_split_plan(M, N, K, terms, num_sms, promo, fd);
     // the kernel indexes work units and tiles in 32 bits (far above any matrix that fits in HBM)
     if (plan.whole + plan.nsplit * plan.slices > INT32_MAX || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) {
         *err = 1;   // SPLIT3_ERR_INVALID_VALUE
         return -1;
     }
-    if (plan.slices > 1 && (!partial || gemm3_partial_elems(plan, terms) > partial_elems)) {
+    if (plan.slices > 1 && (!partial || gemm3_partial_elems(plan, terms, fd) > partial_elems)) {
         plan.whole += plan.nsplit;   // no room for partials: whole tiles only
         plan.nsplit = 0;
         plan.slices = 1;
@@ -1290,15 +1343,15 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
     // fused B)
     LaunchFn fn;
     if (terms == 1) fn = pick<1, 256, 0>(mn);
-    else if (terms == 4) fn = pick<4, 128, 0>(mn);
+    else if (terms == 4) fn = fd ? pick<4, 256, LAY_FOLD>(mn) : pick<4, 128, 0>(mn);
     else if (terms == 6) fn = pick<6, 256, 0>(mn);
-    else if (Bf) fn = pick<3, 256, LAY_FB>(mn);
-    else fn = pick<3, 256, 0>(mn);
+    else if (Bf) fn = fd ? pick<3, 256, LAY_FB | LAY_FOLD>(mn) : pick<3, 256, LAY_FB>(mn);
+    else fn = fd ? pick<3, 256, LAY_FOLD>(mn) : pick<3, 256, 0>(mn);
     int r = fn(st, M, N, K, ma1, ma2, mb1, mb2, ma3, mb3, mc, tma_store, d_sA, d_sB, C, ldc, num_sms, promo,
                wave_counter, tune, plan, partial, Bf ? d_maxB : nullptr, Bf ? const_cast<int32_t*>(d_sB) : nullptr);
     if (r < 0) { *err = 4; return -1; }
     if (plan.slices > 1) {
-        const int bn = terms == 4 ? 128 : 256;
+        const int bn = bn_t;
         const dim3 grid((unsigned)(2 * BM / kReduceRows), (unsigned)plan.nsplit);
         launch_k(ksplit_reduce_kernel, grid, dim3(256), 0, st, partial, plan, bn, M, N, tune.group_m, C, ldc, d_sA, d_sB,
                  c_trans ? 1 : 0);

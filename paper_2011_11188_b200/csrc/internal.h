@@ -133,13 +133,13 @@ struct SplitPlan {
     int64_t nsplit;
     int slices;
 };
-SplitPlan gemm3_split_plan(int64_t M, int64_t N, int64_t K, int terms, int num_sms, int promo_kb);
+SplitPlan gemm3_split_plan(int64_t M, int64_t N, int64_t K, int terms, int num_sms, int promo_kb, bool fold = false);
 // debug build (SPLIT3_DEBUG=1): read / reset the GEMM's check record, inject a fault; release
 // builds return 0 (not available), -1 on a CUDA error, 1 on success
 int gemm3_debug_init();   // map the host record (handle creation)
 int gemm3_debug_read(unsigned long long* out8, int reset);
 int gemm3_debug_fault(int fault);
-int64_t gemm3_partial_elems(const SplitPlan& p, int terms);   // floats of partial workspace
+int64_t gemm3_partial_elems(const SplitPlan& p, int terms, bool fold = false);   // floats of partial workspace
 
 // terms: 1, 3, 4, or 6 (= bf16 x 3: planes A1..A3, B1t..B3t, 6 products, no scale).
 // mn bit 0: the B planes are MN-major, K x N row-major with leading dimension ldpb >= N (the
@@ -157,7 +157,8 @@ int launch_gemm3(cudaStream_t s, int64_t M, int64_t N, int64_t K,
                  float* C, int64_t ldc, int terms, int num_sms, int promo_kb,
                  unsigned* wave_counter, const GemmTuneIn& tune, float* partial, int64_t partial_elems,
                  int* err, const uint16_t* A3 = nullptr, const uint16_t* B3t = nullptr, int mn = 0,
-                 const float* Bf = nullptr, int64_t ldb = 0, const float* d_maxB = nullptr, int c_trans = 0);
+                 const float* Bf = nullptr, int64_t ldb = 0, const float* d_maxB = nullptr, int c_trans = 0,
+                 int fold = 0);
 
 // ---- mlp_kernels.cu (NEXT #3: the non-GEMM steps of a dense-network training step) --------
 int launch_bias_act(cudaStream_t s, int64_t M, int64_t N, const float* Z, int64_t ldz, const float* b, float* H,

@@ -38,7 +38,7 @@ EXPORTS = (
     "split3_sgemm_host_workspace_size", "split3_sgemm_host", "split3_last_bad_index", "split3_host_redo_count", "split3_host_last_layout",
     "split3_status_string", "split3_maxabs", "split3_split", "split3_gemm_planes",
     "split3_last_launch_count", "split3_last_path", "split3_timing_enable", "split3_timing_read",
-    "split3_set_promotion", "split3_set_wave_sync", "split3_set_split_k", "split3_set_max_sms", "split3_set_schedule", "split3_set_fused_split", "split3_set_fused_split_a",
+    "split3_set_promotion", "split3_set_wave_sync", "split3_set_split_k", "split3_set_max_sms", "split3_set_schedule", "split3_set_fused_split", "split3_set_fused_split_a", "split3_set_fold",
     "split3_sgemm_ex", "split3_presplit", "split3_presplit_stored", "split3_split_bf16x3", "split3_debug_read", "split3_debug_fault", "split3_bias_act", "split3_relu_backward",
     "split3_softmax_xent", "split3_bias_grad", "split3_sgd_update",
 )
@@ -133,6 +133,7 @@ def load() -> ctypes.CDLL:
         lib.split3_set_schedule.argtypes = [_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         lib.split3_set_fused_split.argtypes = [_p, ctypes.c_int, _i64]
         lib.split3_set_fused_split_a.argtypes = [_p, ctypes.c_int, _i64]
+        lib.split3_set_fold.argtypes = [_p, ctypes.c_int]
         lib.split3_sgemm_ex.argtypes = [_p, _i64, _i64, _i64, ctypes.POINTER(split3_matrix),
                                         ctypes.POINTER(split3_matrix), _p, _i64, ctypes.c_uint32]
         lib.split3_debug_read.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
@@ -329,6 +330,11 @@ class Handle:
     def set_fused_split(self, mode: int, max_m: int = 0):
         """Fused split of an fp32 B inside the GEMM (NEXT #2): 0 off, 1 auto (M <= max_m), 2 always."""
         self._set("split3_set_fused_split", int(mode), int(max_m))
+
+    def set_fold(self, mode: int):
+        """Folded accumulator (a k-block's 3 (4) products in one TMEM accumulator via scale-input-d):
+        0 never, 1 4-term calls (default), 2 4- and 3-term calls."""
+        self._set("split3_set_fold", int(mode))
 
     def set_fused_split_a(self, mode: int, max_n: int = 0):
         """Fused split of an fp32 A (NEXT #2) through C^T = B^T A^T: 0 off, 1 auto (N <= max_n and

@@ -1,7 +1,7 @@
 """The checked debug build (libsplit3_debug.so, -DSPLIT3_DEBUG=1) — the substitute
 for compute-sanitizer on this GPU pool: mbarrier watchdogs and pipeline invariants inside the GEMM.
 
-  * over the shapes, term counts, operand layouts, split-K tails, the fused-B and fused-A paths and the 2-D
+  * over the shapes, term counts, operand layouts, split-K tails, the fused-B and fused-A paths, the folded accumulator and the 2-D
     driver's pieces of the parity suite, the debug build records no failure and its C is bitwise
     the release build's;
   * an injected fault (a TMA load that never happens) is caught by the watchdog: the record (in
@@ -49,7 +49,13 @@ h.set_fused_split(1)
 h.set_fused_split_a(2)
 rec("fusedA", h.sgemm(B.t().contiguous(), A.t().contiguous()))
 rec("fusedA_splitk", h.sgemm(torch_matrix("uniform", 2048, 4096, seed=5), torch_matrix("uniform", 4096, 256, seed=6)))
-h.set_fused_split_a(1)
+h.set_fused_split_a(0)
+h.set_fold(2)
+for terms in (3, 4):
+    rec(f"fold{terms}", h.sgemm(A, B, four_term=terms == 4))
+    rec(f"fold{terms}_splitk", h.sgemm(torch_matrix("uniform", 300, 8192, seed=11), torch_matrix("uniform", 8192, 520, seed=12),
+                                        four_term=terms == 4))
+h.set_fold(1)
 h.set_split_k(False)
 rec("wholetiles", h.sgemm(A, B))
 h.set_max_sms(132)
