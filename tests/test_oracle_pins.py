@@ -293,6 +293,29 @@ def test_dropped_term_identity(orc):
     assert np.linalg.norm(d) <= 2.0 ** -22 * nA1 * nB1
 
 
+def test_four_term_is_exact_when_the_split_is(orc):
+    """Eq. A_1 with an exact residual (x = a1 A1 + a2 A2 exactly) makes the 4-term
+    Eq. A_2 the exact product and the 3-term value the product minus exactly the dropped term
+    (PAPER.md:21-24).  Entries +-16392 / +-16408 (s = 0): 16392 = 16384 + 8 ties to the even
+    16384 (A2 = RN16(2^11 8) = 16384), 16408 = 16400 + 8 ties to 16416 (A2 = -16384) — hand-derived
+    planes; the GPU's folded accumulator is pinned on the same inputs (test_gpu_fold.py)."""
+    rng = np.random.default_rng(5)
+    vals = np.array([16392, -16392, 16408, -16408], dtype=np.float32)
+    A = vals[rng.integers(0, 4, (40, 2))]
+    B = vals[rng.integers(0, 4, (2, 30))]
+    a1, a2, sA = orc.split(A)
+    assert sA == 0
+    want1 = np.where(np.abs(A) == 16392, 16384.0, 16416.0) * np.sign(A)
+    want2 = np.where(np.abs(A) == 16392, 16384.0, -16384.0) * np.sign(A)
+    assert np.array_equal(orc.dec16(a1), want1) and np.array_equal(orc.dec16(a2), want2)
+    exact = A.astype(np.float64) @ B.astype(np.float64)
+    assert np.array_equal(orc.sgemm(A, B, terms=4), exact)
+    b1, b2, sB = orc.split(B)
+    drop = np.ldexp(orc.dec16(a2) @ orc.dec16(b2), sA + sB - 22)
+    assert np.array_equal(orc.sgemm(A, B, terms=3), exact - drop)
+    assert np.count_nonzero(drop) > 0
+
+
 def test_accuracy_separation_n64(orc):
     """Config D1: 3-term error vs FP64 << naive FP16 (1-term) error, 20 seeds."""
     e3s, e1s, e4s = [], [], []
