@@ -252,6 +252,7 @@ int split3_last_launch_count(split3_handle_t h);
 #define SPLIT3_PATH_FUSED_B 1   /* B split inside the GEMM (split3_set_fused_split) */
 #define SPLIT3_PATH_FUSED_A 2   /* A split inside the GEMM, C^T = B^T A^T (split3_set_fused_split_a) */
 #define SPLIT3_PATH_PREP    8   /* one-launch max-abs + split front end (small calls) */
+#define SPLIT3_PATH_FOLD   16   /* folded accumulator (split3_set_fold) */
 int split3_last_path(split3_handle_t h);
 
 /* ---- dense-network step helpers ----------------------------
@@ -340,9 +341,9 @@ int split3_set_fused_split(split3_handle_t h, int mode, int64_t max_m);
  * No separate D_mid / D_lo accumulators: two T buffers ping-pong in TMEM and the 4-term path keeps
  * 256-wide tiles (the unfolded 4-term kernel needs 256 TMEM columns more and runs 256 x 128
  * tiles).  Rounding differs from the unfolded kernel; same oracle tolerance.  mode 0: never;
- * 1 (default): 4-term calls (measured +5 %); 2: 4- and 3-term calls (3-term: -1.6 %, one more
- * promotion per k-block under the power cap).  Env: SPLIT3_FOLD.  INVALID_VALUE for mode outside
- * 0..2. */
+ * 1 (default): 4-term calls with M*N*K >= 8192^3 (the power-capped regime, measured +5.4 % at
+ * N = 16384; smaller single calls run 2-6 % slower folded); 2: every 4- and 3-term call (3-term:
+ * -1.6 %).  Env: SPLIT3_FOLD.  INVALID_VALUE for mode outside 0..2. */
 int split3_set_fold(split3_handle_t h, int mode);
 
 /* Fused split of A (SURVEY §8f NEXT #2 for the other operand; Eq. A_1 applied inside the GEMM):

@@ -52,7 +52,7 @@ struct split3_ctx {
     int64_t fuse_a_max_n = 2048;
     // folded accumulator (LAY_FOLD): 3-/4-term products of a k-block summed in ONE TMEM
     // accumulator with tcgen05's scale-input-d, promoted every k-block.  0 never, 1 (default)
-    // 4-term calls, 2 4- and 3-term calls.  env SPLIT3_FOLD
+    // 4-term calls of >= 8192^3 multiply-adds, 2 every 4- and 3-term call.  env SPLIT3_FOLD
     int fold = 1;
     split3::GemmTuneIn tune;
     unsigned* d_counters = nullptr;   // 256 B of device scratch owned by the handle
@@ -615,7 +615,8 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
             return SPLIT3_ERR_NOT_FINITE;
         }
     }
-    h->last_path = (fuse_b ? SPLIT3_PATH_FUSED_B : 0) | (fuse_a ? SPLIT3_PATH_FUSED_A : 0) | (prepped ? SPLIT3_PATH_PREP : 0);
+    h->last_path = (fuse_b ? SPLIT3_PATH_FUSED_B : 0) | (fuse_a ? SPLIT3_PATH_FUSED_A : 0) | (prepped ? SPLIT3_PATH_PREP : 0) |
+                   (split3::gemm3_fold_chosen(M, N, K, terms, h->fold) ? SPLIT3_PATH_FOLD : 0);
     // a2: split into K-major planes (A: M x K, B: N x K)
     const uint16_t *A1 = A->hi, *A2 = A->lo, *B1t = B->hi, *B2t = B->lo;
     const int32_t *sA = A->d_sexp, *sB = B->d_sexp;
@@ -1050,6 +1051,8 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
     if (cudaMemsetAsync(h->ws, 0, 32, s0) != cudaSuccess || cudaMemsetAsync(maxblk, 0, 4 * kSlots, s0) != cudaSuccess ||
         cudaMemsetAsync(minblk, 0xFF, 4 * kSlots, s0) != cudaSuccess)
         return SPLIT3_ERR_CUDA;
+    // every piece takes the whole problem's accumulator (folded or not): the device call's bits
+    const int fold_whole = split3::gemm3_fold_chosen(M, N, K, terms_of(flags), h->fold) ? 2 : 0;
     auto gemm_piece = [&](int b, int j, const int32_t* d_sA, const int32_t* d_sB) {
         const int64_t r0 = blk_r0[b], mr = blk_mr[b], c0 = pan_c0[j], nc = pan_nc[j];
         int err = 0;
@@ -1057,7 +1060,7 @@ int split3_sgemm_host(split3_handle_t h, int64_t M, int64_t N, int64_t K, const 
         int r = split3::launch_gemm3(s0, mr, nc, K, w.A1 + r0 * w.ldpa, w.A2 + r0 * w.ldpa, w.ldpa, d_sA, w.B1t + c0,
                                      w.B2t + c0, ldpb, d_sB, dC + r0 * N + c0, N, terms_of(flags), gemm_sms(h),
                                      h->promo_kb, h->wave_sync ? h->d_counters : nullptr, h->tune, nullptr, 0, &err,
-                                     nullptr, nullptr, b_mn ? 1 : 0, nullptr, 0, nullptr, 0, h->fold);
+                                     nullptr, nullptr, b_mn ? 1 : 0, nullptr, 0, nullptr, 0, fold_whole);
         return r < 0 ? -(err ? err : SPLIT3_ERR_CUDA) : r;
     };
     auto copy_out = [&](int b, int j, cudaStream_t st) {

@@ -1258,6 +1258,15 @@ SplitPlan gemm3_split_plan(int64_t M, int64_t N, int64_t K, int terms, int num_s
     return p;
 }
 
+// Folded accumulator (LAY_FOLD): fold 1 = 4-term calls of at least 8192^3 multiply-adds (the
+// power-capped regime: N = 16384 sustained +5.4 %; single 4096^3 .. 4096 x 8192^2 calls at
+// higher clocks -2 .. -6 %, 8192^3 +1 %: profiles/fold_ab_*_r02.json, fold_bench_r02.json),
+// 2 = every 3- and 4-term call (3-term: -1.6 % sustained).
+bool gemm3_fold_chosen(int64_t M, int64_t N, int64_t K, int terms, int fold) {
+    const bool big = (double)M * (double)N * (double)K >= 549755813888.0;   // 2^39 = 8192^3
+    return (terms == 4 && (fold >= 2 || (fold == 1 && big))) || (terms == 3 && fold >= 2);
+}
+
 int64_t gemm3_partial_elems(const SplitPlan& p, int terms, bool fold) {
     const int bn = (terms == 4 && !fold) ? 128 : 256;
     return p.slices > 1 ? (int64_t)p.slices * p.nsplit * 256 * bn : 0;
@@ -1269,9 +1278,7 @@ int launch_gemm3(cudaStream_t st, int64_t M, int64_t N, int64_t K, const uint16_
                  int terms, int num_sms, int promo_kb, unsigned* wave_counter, const GemmTuneIn& tin,
                  float* partial, int64_t partial_elems, int* err, const uint16_t* A3, const uint16_t* B3t,
                  int mn, const float* Bf, int64_t ldb, const float* d_maxB, int c_trans, int fold) {
-    // folded accumulator (LAY_FOLD): fold 1 = 4-term only (measured +5 % there, 3-term -1.6 %:
-    // profiles/fold_ab_*_r02.json), 2 = 3- and 4-term
-    const bool fd = (terms == 4 && fold >= 1) || (terms == 3 && fold >= 2);
+    const bool fd = gemm3_fold_chosen(M, N, K, terms, fold);   // folded accumulator (LAY_FOLD)
     const int bn_t = (terms == 4 && !fd) ? 128 : 256;         // tile width
     const bool b_mn = (mn & 1) != 0, a_mn = (mn & 2) != 0;
     CUtensorMap ma1, ma2, mb1, mb2, ma3, mb3;

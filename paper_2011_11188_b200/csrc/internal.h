@@ -139,7 +139,8 @@ SplitPlan gemm3_split_plan(int64_t M, int64_t N, int64_t K, int terms, int num_s
 int gemm3_debug_init();   // map the host record (handle creation)
 int gemm3_debug_read(unsigned long long* out8, int reset);
 int gemm3_debug_fault(int fault);
-int64_t gemm3_partial_elems(const SplitPlan& p, int terms, bool fold = false);   // floats of partial workspace
+int64_t gemm3_partial_elems(const SplitPlan& p, int terms, bool fold = false);
+bool gemm3_fold_chosen(int64_t M, int64_t N, int64_t K, int terms, int fold);   // the handle's fold mode   // floats of partial workspace
 
 // terms: 1, 3, 4, or 6 (= bf16 x 3: planes A1..A3, B1t..B3t, 6 products, no scale).
 // mn bit 0: the B planes are MN-major, K x N row-major with leading dimension ldpb >= N (the

@@ -148,6 +148,14 @@ class CudaOps:
         self.gather_sms = int(gemm_sms_during_gather)
         h.set_split_k(False)
 
+    def begin(self, M, N, K, four_term):
+        """The global problem's accumulator choice for every piece: the library folds 4-term calls
+        of >= 8192^3 multiply-adds (split3_set_fold mode 1); a piece decides on its own shape, so
+        the driver pins the whole problem's choice (mode 2 = fold, 0 = not) to keep the pieces'
+        bits the one-GPU call's."""
+        if four_term:
+            self.h.set_fold(2 if M * N * K >= 2 ** 39 else 0)
+
     def maxabs_into(self, X, d_max1):
         self.h.maxabs(X, d_max1)
         self.launches += self.h.last_launch_count()
@@ -203,6 +211,8 @@ def sgemm_2d(A_blk: torch.Tensor, B_blk: torch.Tensor, M: int, N: int, ops, grou
     pr, pc = grid_for(world)
     i, j = coords(rank, world)
     K = A_blk.shape[1]
+    if hasattr(ops, "begin"):
+        ops.begin(M, N, K, four_term)
     if groups is None:
         groups = make_groups(world)
     row_groups, col_groups = groups
@@ -313,6 +323,8 @@ def sgemm_2d_replicated(A: torch.Tensor, B: torch.Tensor, ops, out: torch.Tensor
     rank = dist.get_rank()
     M, K = A.shape
     N = B.shape[1]
+    if hasattr(ops, "begin"):
+        ops.begin(M, N, K, four_term)
     r0, r1, c0, c1 = c_tile(M, N, world, rank)
     Ap, Bp = A[r0:r1], B[:, c0:c1]            # row panel i (contiguous rows), column panel j (ld = N)
     mx = torch.zeros(2, dtype=torch.float32, device=A.device)

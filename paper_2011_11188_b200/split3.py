@@ -333,7 +333,7 @@ class Handle:
 
     def set_fold(self, mode: int):
         """Folded accumulator (a k-block's 3 (4) products in one TMEM accumulator via scale-input-d):
-        0 never, 1 4-term calls (default), 2 4- and 3-term calls."""
+        0 never, 1 4-term calls of >= 8192^3 multiply-adds (default), 2 every 4- and 3-term call."""
         self._set("split3_set_fold", int(mode))
 
     def set_fused_split_a(self, mode: int, max_n: int = 0):
@@ -364,7 +364,8 @@ class Handle:
         return out
 
     def last_path(self) -> int:
-        """SPLIT3_PATH_* bits of the last call: 1 fused B, 2 fused A, 8 one-launch front end."""
+        """SPLIT3_PATH_* bits of the last call: 1 fused B, 2 fused A, 8 one-launch front end,
+        16 folded accumulator."""
         return int(self._lib.split3_last_path(self._h))
 
     def last_launch_count(self) -> int:

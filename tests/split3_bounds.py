@@ -54,9 +54,10 @@ def _elementwise_bound_fold(orc, A, B, terms, slices=16):
 
 
 def _assert_elementwise(orc, C, Cs, A, B, terms, fold=None):
-    """fold: the folded accumulator's bound (None: the library default, folded for 4-term)"""
+    """fold: the folded accumulator's bound (None: the library default — folded for 4-term calls of
+    at least 8192^3 multiply-adds)"""
     if fold is None:
-        fold = terms == 4
+        fold = terms == 4 and A.shape[0] * B.shape[1] * A.shape[1] >= 2 ** 39
     bound = (_elementwise_bound_fold(orc, A, B, terms) if fold else _elementwise_bound(orc, A, B, terms)) \
         + 2.0 ** -24 * np.abs(Cs)
     err = np.abs(C.astype(np.float64) - Cs)

@@ -179,6 +179,20 @@ def test_fold_repeatable_and_graph(hf):
     assert torch.equal(_bits(C), _bits(C0))
 
 
+def test_fold_default_rule():
+    """default handle: 4-term calls of >= 8192^3 multiply-adds fold (SPLIT3_PATH_FOLD), smaller
+    4-term calls and every 3-term call do not"""
+    h = s3.Handle(0)
+    A = torch_matrix("uniform", 8192, 8192, seed=51)
+    B = torch_matrix("uniform", 8192, 8192, seed=52)
+    h.sgemm(A, B, four_term=True)
+    assert h.last_path() & 16
+    h.sgemm(A, B)
+    assert not h.last_path() & 16
+    h.sgemm(A[:4096].contiguous(), B, four_term=True)
+    assert not h.last_path() & 16
+
+
 def test_fold_validation(hf):
     assert s3.split3.load().split3_set_fold(hf._h, 3) == 1      # SPLIT3_ERR_INVALID_VALUE
     with pytest.raises(s3.Split3Error):

@@ -457,6 +457,25 @@ def test_host_pipeline_bitwise_equals_device(h, M, N):
         assert torch.equal(Ch.view(torch.int32), ref.view(torch.int32))
 
 
+def test_host_pipeline_bitwise_equals_device_folded_four_term():
+    """A 4-term call of 8192^3 multiply-adds folds (split3_set_fold's default rule): the host
+    pipeline's row-block GEMMs take the WHOLE problem's choice, so its C is the device call's bit
+    for bit (device handle with split-K off: whole tiles, as the host pieces)"""
+    import paper_2011_11188_b200 as s3
+
+    n = 8192
+    hd = s3.Handle(0)
+    hd.set_split_k(False)
+    A = torch_matrix("uniform", n, n, seed=3, device="cuda")
+    B = torch_matrix("uniform", n, n, seed=4, device="cuda")
+    ref = hd.sgemm(A, B, four_term=True).cpu()
+    assert hd.last_path() & 16                      # SPLIT3_PATH_FOLD
+    Ah, Bh = A.cpu().pin_memory(), B.cpu().pin_memory()
+    Ch = torch.empty((n, n), dtype=torch.float32).pin_memory()
+    hd.sgemm_host_ptr(n, n, n, Ah.data_ptr(), Bh.data_ptr(), Ch.data_ptr(), 1)   # SPLIT3_FOUR_TERM
+    assert torch.equal(Ch.view(torch.int32), ref.view(torch.int32))
+
+
 def test_planes_exhaustive_fp32_range(h, orc):
     """Every fp32 bit pattern with |x| < 2^15 (2 x 0x47000000 ~ 2.4e9 values, in 2^28-pattern
     chunks): GPU planes == oracle planes, bit for bit (the GPU cvt.rn.f16.f32 pin).
