@@ -23,6 +23,9 @@ static int cpu_checks(void) {
     CHECK(split3_sgemm_workspace_size(100, 60, 33, 0) > 0, "workspace size");
     CHECK(split3_sgemm(NULL, 1, 1, 1, NULL, 1, NULL, 1, NULL, 1, 0) == SPLIT3_ERR_INVALID_VALUE, "null handle");
     CHECK(split3_sgemm_destroy(NULL) == SPLIT3_OK, "destroy NULL");
+    CHECK(split3_set_fold(NULL, 1) == SPLIT3_ERR_INVALID_VALUE, "fold NULL handle");
+    CHECK(split3_set_fused_split_a(NULL, 1, 0) == SPLIT3_ERR_INVALID_VALUE, "fused A NULL handle");
+    CHECK(split3_last_path(NULL) == 0, "path NULL handle");
     printf("cpu ok\n");
     return 0;
 }
@@ -55,6 +58,18 @@ static int gpu_checks(void) {
         CHECK(cudaMemcpy(hC, C, M * N * 4, cudaMemcpyDeviceToHost) == cudaSuccess, "copy back");
         for (int64_t i = 0; i < M * N; i++) CHECK((double)hC[i] == ref[i], "integer product exact");
     }
+    /* round-2 knobs: the folded accumulator (every 3-/4-term call) and fused A (C = (B^T A^T)^T):
+       integer inputs stay exact whatever the path */
+    CHECK(split3_set_fold(h, 3) == SPLIT3_ERR_INVALID_VALUE && split3_set_fold(h, 2) == SPLIT3_OK, "fold mode");
+    CHECK(split3_set_fused_split_a(h, 2, 0) == SPLIT3_OK, "fused A mode");
+    for (int f = 0; f < 2; f++) {
+        CHECK(split3_sgemm(h, M, N, K, A, K, B, N, C, N, flags[f]) == SPLIT3_OK, "sgemm (fold, fused A)");
+        CHECK((split3_last_path(h) & (SPLIT3_PATH_FOLD | SPLIT3_PATH_FUSED_A)) ==
+                  (f == 0 ? (SPLIT3_PATH_FOLD | SPLIT3_PATH_FUSED_A) : SPLIT3_PATH_FOLD), "path bits");
+        CHECK(cudaMemcpy(hC, C, M * N * 4, cudaMemcpyDeviceToHost) == cudaSuccess, "copy back");
+        for (int64_t i = 0; i < M * N; i++) CHECK((double)hC[i] == ref[i], "integer product exact (fold)");
+    }
+    CHECK(split3_set_fold(h, 1) == SPLIT3_OK && split3_set_fused_split_a(h, 0, 0) == SPLIT3_OK, "defaults");
     memset(hC, 0, M * N * 4);
     CHECK(split3_sgemm_host(h, M, N, K, hA, hB, hC, 0) == SPLIT3_OK, "host entry");
     for (int64_t i = 0; i < M * N; i++) CHECK((double)hC[i] == ref[i], "host entry exact");
