@@ -327,7 +327,8 @@ int split3_set_max_sms(split3_handle_t h, int sms);
  * the max-abs pass reads B beforehand).  The planes, and therefore C, are bit-identical to the separate split.
  * mode 0: off; 1 (default): when M <= max_m (default 2048: each B tile is converted once per
  * 256-row tile row, and the extra shared-memory traffic slows the GEMM ~11 %, which the saved
- * 8 B/element of B's split outweighs for small M), or for any M when the call is small enough for
+ * 8 B/element of B's split outweighs for small M), when M <= 2 max_m and K * N <= 2^25 (B's split is
+ * then a larger share of the call), or for any M when the call is small enough for
  * the one-launch front end (SPLIT3_PREP_MAX; fused B is 5-25 % faster there); 2: whenever
  * eligible.  max_m = 0 keeps the current threshold.  Env: SPLIT3_FUSE_B,
  * SPLIT3_FUSE_B_MAX_M at handle creation.  INVALID_VALUE for mode outside 0..2 or max_m < 0. */

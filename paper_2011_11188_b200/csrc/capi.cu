@@ -39,7 +39,8 @@ struct split3_ctx {
     int mn_major = 1;   // MN-major planes for a row-major B / a transposed A (no transposing split);
                         // env SPLIT3_MN_MAJOR=0: off (K-major planes, transposing split)
     // fused B: an fp32 B is split inside the GEMM (converter warps) instead of
-    // by a separate pass.  0 off, 1 auto (M <= fuse_b_max_m, or a small call of any M),
+    // by a separate pass.  0 off, 1 auto (M <= fuse_b_max_m, M <= 2 fuse_b_max_m with K*N <= 2^25,
+    // or a small call of any M),
     // 2 whenever eligible (measured: profiles/fused_b_r01.md).  env SPLIT3_FUSE_B, SPLIT3_FUSE_B_MAX_M
     int fuse_b = 1;
     int64_t fuse_b_max_m = 2048;
@@ -538,10 +539,14 @@ int split3_sgemm_ex(split3_handle_t h, int64_t M, int64_t N, int64_t K, const sp
     const bool fuse_a = needA && terms == 3 && aligned(A->data, 16) && (A->ld % 4) == 0 && aligned(C, 16) &&
                         (ldc % 4) == 0 &&
                         (h->fuse_a == 2 || (h->fuse_a == 1 && N <= h->fuse_a_max_n && N < M && !small_call));
-    // fused B: M <= fuse_b_max_m, or any M for a small call (measured faster than the one-launch
-    // front end at every small shape, 5-25 %: profiles/small_fused_bench_r02.json)
+    // fused B: M <= fuse_b_max_m; or M <= 2 fuse_b_max_m with a B of at most 2^25 elements (its
+    // split is then a larger share of the call: 4096^3 +1.6 %, 4096 x 8192 x 4096 +3.5 %, while
+    // 4096 x 8192^2 loses 0.5-6.5 %: profiles/fused_b_bench_midM_r02.json); or any M for a small
+    // call (faster than the one-launch front end at every small shape, 5-25 %:
+    // profiles/small_fused_bench_r02.json)
+    const bool mid_m = M <= 2 * h->fuse_b_max_m && N * K <= ((int64_t)1 << 25);
     const bool fuse_b = !fuse_a && needB && terms == 3 && aligned(B->data, 16) && (B->ld % 4) == 0 &&
-                        (h->fuse_b == 2 || (h->fuse_b == 1 && (M <= h->fuse_b_max_m || small_call)));
+                        (h->fuse_b == 2 || (h->fuse_b == 1 && (M <= h->fuse_b_max_m || mid_m || small_call)));
     // (both operands pre-split: no max-abs at all, nothing to reset)
     if (!fast_max && (needA || needB) && cudaMemsetAsync(h->ws, 0, 32, h->stream) != cudaSuccess)
         return SPLIT3_ERR_CUDA;
