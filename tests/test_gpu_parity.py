@@ -352,9 +352,10 @@ def test_tc_accumulation_probe(h):
 
 # --------------------------------------------- full size (bench configuration) -----
 
-@pytest.mark.parametrize("N,terms", [(4096, 3), (4096, 4), (16384, 3)])
+@pytest.mark.parametrize("N,terms", [(4096, 3), (4096, 4), (16384, 3), (16384, 4)])
 def test_full_size_sampled_parity(h, orc, N, terms):
-    """configs[1] sizes, launched exactly as bench.py does; oracle on sampled outputs."""
+    """configs[1] sizes, launched exactly as bench.py does (16384 4-term: the folded accumulator);
+    oracle on sampled outputs."""
     A = torch_matrix("uniform", N, N, seed=11, device="cuda")
     B = torch_matrix("uniform", N, N, seed=12, device="cuda")
     C = h.sgemm(A, B, four_term=terms == 4)
