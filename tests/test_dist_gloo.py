@@ -16,6 +16,30 @@ import torch.multiprocessing as mp
 from paper_2011_11188_b200 import dist as d2
 
 
+def test_cuda_ops_pin_the_whole_problems_fold_choice():
+    """CudaOps.begin: a 4-term problem of >= 8192^3 multiply-adds folds (the library's mode-1
+    rule on the WHOLE problem), so every piece is pinned to fold (mode 2) — or to no fold (mode 0)
+    for a smaller problem whose pieces would decide alike; 3-term calls leave the handle alone"""
+    class FakeHandle:
+        def __init__(self):
+            self.calls = []
+
+        def set_split_k(self, on):
+            self.calls.append(("split_k", on))
+
+        def set_fold(self, mode):
+            self.calls.append(("fold", mode))
+
+    h = FakeHandle()
+    ops = d2.CudaOps(h)
+    assert h.calls == [("split_k", False)]
+    ops.begin(65536, 65536, 65536, True)
+    ops.begin(8192, 8192, 8192, True)
+    ops.begin(8192, 8192, 4096, True)
+    ops.begin(65536, 65536, 65536, False)
+    assert h.calls[1:] == [("fold", 2), ("fold", 2), ("fold", 0)]
+
+
 def test_grid_and_ownership_math():
     assert d2.grid_for(1) == (1, 1)
     assert d2.grid_for(2) == (1, 2)
