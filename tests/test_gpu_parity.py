@@ -225,6 +225,34 @@ def test_epilogue_scale_outside_fp32_normal_range(h, shape, e):
         assert np.count_nonzero(want) > 0 and np.any(np.abs(want[want != 0]) < np.float32(2.0 ** -126))
 
 
+def test_default_call_planes_vs_oracle(orc):
+    """The planes the default call leaves in its workspace (A: M x K K-major, B: K x N MN-major,
+    both split without a transpose; capi.cu carve) equal the oracle's bit for bit; the call is the
+    two-matrix max-abs, the two splits and the GEMM (+ split-K reduction)"""
+    import paper_2011_11188_b200 as s3
+
+    hh = s3.Handle(0)
+    M, N, K = 4100, 1028, 1032                 # not small, M > 4096: no fused B
+    A = torch_matrix("loguni", M, K, seed=61, device="cuda")
+    B = torch_matrix("loguni", K, N, seed=62, device="cuda")
+    hh.sgemm(A, B)
+    torch.cuda.synchronize()
+    assert hh.last_path() == 0 and hh.last_launch_count() <= 5, (hh.last_path(), hh.last_launch_count())
+    pl = s3.split3.plane_ld
+    pa = (max(M * pl(K), K * pl(M)) * 2 + 255) // 256 * 256
+    pb = (max(N * pl(K), K * pl(N)) * 2 + 255) // 256 * 256
+    raw = hh._ws.view(torch.uint8)
+
+    def plane(off, rows, ld, cols):
+        return raw[off:off + rows * ld * 2].view(torch.int16).view(rows, ld)[:, :cols].cpu().numpy().view(np.uint16)
+
+    a1, a2, _ = orc.split(A.cpu().numpy())
+    b1, b2, _ = orc.split(B.cpu().numpy())
+    assert np.array_equal(plane(256, M, pl(K), K), a1) and np.array_equal(plane(256 + pa, M, pl(K), K), a2)
+    o = 256 + 2 * pa
+    assert np.array_equal(plane(o, K, pl(N), N), b1) and np.array_equal(plane(o + pb, K, pl(N), N), b2)
+
+
 def test_strided_operands_and_output(h, orc):
     M, N, K = 100, 90, 130
     Abig = torch.from_numpy(numpy_matrix("uniform", M, K + 6, seed=1)).cuda()
